@@ -1,0 +1,435 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 Tersoff hot path (driver contract: one JSON line).
+
+Metric (BASELINE.json): Tersoff atom-steps/s -- atoms x E+F evaluations per
+second -- with the achieved fraction of the FP64 pipe peak.
+
+Workload: BASELINE config 2, the largest single-GPU configuration the metric
+is quoted on: 64,000-atom Si diamond (20^3 cells, a=5.431, sigma=0.1 seed
+1002), Si(C) Tersoff parameters, skin 0.3, fp64.  One "step" = one energy +
+force + virial evaluation at the current positions: the kernel re-packs the
+skin list at r_cut (pack_adjacency) and evaluates every Tersoff term
+(kernels.compute semantics).  The neighbour list is built once outside the
+timed region, as the reference harness does (bench.py:116-118).  Inputs are
+resident in HBM for `value`; the 64k-atom working set (~6 MB) fits in L2, so
+L2 is flushed (a 256 MiB write) between timed steps.
+
+  e2e         the same evaluation through the public API compute() with the
+              positions in pinned host memory: H2D of positions+species and
+              D2H of forces, per-atom energies, energy/virial/stats per step.
+  roofline    the Tersoff kernel's algorithmic fp64 flops (SURVEY 8(d) op
+              counts per live pair / live triplet) / its CUDA-event time, against
+              the FP64 DFMA peak measured on this GPU at start-up.
+  cpu_baseline  the CPU oracle (a C restatement of the reference ScalarOpt,
+              oracle/) on this host's cores, rank 0, N=1.
+
+  --impl reference   the reference's CPU implementation of the path on the
+              host cores (the oracle port; the Python reference cannot travel).
+
+Multi-GPU (torchrun, N>1): every rank evaluates its own replica of the
+workload (weak scaling); time = max over ranks of the device-timed loop.
+"""
+
+import argparse
+import json
+import os
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "Tersoff atom-steps/s (E+F evals)"
+UNIT = "atom-steps/s"
+
+# fp64-weighted op counts of the reference ScalarOpt
+# expression tree (add/mul = 1, div 15, sqrt 13, exp 31, sin = cos 26, pow 125)
+FLOPS_PAIR = 19 + 25 + 3 * 15 + 2 * 31 + 4 * 125 + 8 + 13   # + distance
+FLOPS_TRIP = 32 + 55 + 4 * 15 + 31
+FLOPS_TAPER = 2 + 3 + 15 + 26 + 26                           # per tapered f_C
+
+
+def algorithmic_flops(stats):
+    return (FLOPS_PAIR * stats[2] + FLOPS_TAPER * stats[4]
+            + FLOPS_TRIP * stats[3] + FLOPS_TAPER * stats[5])
+
+
+class ClockSampler:
+    """Samples SM clock and throttle reasons with NVML during the timed region."""
+
+    BITS = {0x4: "sw_power_cap", 0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown",
+            0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown"}
+
+    def __init__(self, torch_dev):
+        self.samples, self.reasons = [], set()
+        self.max_mhz = None
+        self._stop = threading.Event()
+        self.ok = False
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            h = None
+            try:
+                import torch
+                uuid = str(torch.cuda.get_device_properties(torch_dev).uuid)
+                if not uuid.startswith("GPU-"):
+                    uuid = "GPU-" + uuid
+                h = pynvml.nvmlDeviceGetHandleByUUID(uuid)
+            except Exception:
+                vis = os.environ.get("CUDA_VISIBLE_DEVICES", "")
+                idx = int(vis.split(",")[torch_dev]) if vis and vis.split(",")[0].isdigit() \
+                    else torch_dev
+                h = pynvml.nvmlDeviceGetHandleByIndex(idx)
+            self.nv, self.h = pynvml, h
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception as e:  # pragma: no cover
+            self.err = str(e)
+
+    def _run(self):
+        nv, h = self.nv, self.h
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM))
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+                for bit, name in self.BITS.items():
+                    if r & bit:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(0.01)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.ok:
+            self._stop.set()
+            self.t.join()
+
+    def summary(self):
+        if not self.ok:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvml unavailable"]}
+        med = float(np.median(self.samples)) if self.samples else None
+        return {"sm_mhz": med, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                "samples": len(self.samples)}
+
+
+def dist_setup():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def cpu_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def oracle_baseline(state, table, budget_s=12.0, min_evals=2, threads=None):
+    """Time the CPU oracle (reference ScalarOpt restated in C, OpenMP over
+    atom ranges) on this host: NL built outside the timer, then E+F
+    evaluations (pack + kernel) until `budget_s`."""
+    from oracle import oracle as O
+    threads = threads or cpu_cores()
+    off, nb = O.build_neighbor_list(state.positions, state.box.lengths, state.box.periodic,
+                                    table.r_cut, 0.3, threads=threads)
+    t0 = time.perf_counter()
+    evals = 0
+    while True:
+        O.compute(state.positions, state.species, state.box.lengths, state.box.periodic,
+                  off, nb, table, threads=threads)
+        evals += 1
+        el = time.perf_counter() - t0
+        if (el >= budget_s and evals >= min_evals) or evals >= 10000:
+            break
+    return state.natoms * evals / el, threads, evals, el
+
+
+def reference_arm(args):
+    ws, rank, _ = dist_setup()
+    if rank != 0:
+        return
+    from paper_1710_00882_b200 import structures
+    from paper_1710_00882_b200.paramfile import builtin_params
+    from oracle import oracle as O
+    state, tname = structures.config(args.config)
+    table = builtin_params(tname)
+    threads = cpu_cores()
+    off, nb = O.build_neighbor_list(state.positions, state.box.lengths, state.box.periodic,
+                                    table.r_cut, 0.3, threads=threads)
+
+    def one():
+        O.compute(state.positions, state.species, state.box.lengths, state.box.periodic,
+                  off, nb, table, precision=args.precision_ref, threads=threads)
+
+    for _ in range(args.warmup):
+        one()
+    # bounded sample: the whole run stays within ~2 minutes
+    t0 = time.perf_counter()
+    one()
+    per = time.perf_counter() - t0
+    steps = args.steps
+    budget = 120.0
+    timed = max(1, min(steps, int(budget / max(per, 1e-6))))
+    t0 = time.perf_counter()
+    for _ in range(timed):
+        one()
+    el = time.perf_counter() - t0
+    value = state.natoms * timed / el
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": timed, "warmup": args.warmup, "ms_per_step": 1e3 * el / timed,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64" if args.precision_ref == "double" else "f32/f64",
+        "data": "synthetic", "impl": "reference",
+        "config": {"workload": f"BASELINE config {args.config}: {state.natoms} Si diamond "
+                               f"E+F(+virial) evaluation, skin 0.3",
+                   "atoms": state.natoms, "precision": args.precision_ref},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
+                         "sample": f"{timed} full E+F evaluations of the {state.natoms}-atom "
+                                   f"system (of {steps} requested; bounded to ~{budget:.0f} s), "
+                                   f"NL built outside the timer; oracle/ C restatement of "
+                                   f"ScalarOpt, OpenMP over {threads} threads"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def gpu_arm(args):
+    import torch
+    ws, rank, local = dist_setup()
+    dev = local if ws > 1 else 0
+    torch.cuda.set_device(dev)
+    if ws > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+    import paper_1710_00882_b200 as B
+    from paper_1710_00882_b200 import _native, structures
+    from paper_1710_00882_b200.paramfile import builtin_params
+
+    state, tname = structures.config(args.config)
+    table = builtin_params(tname)
+    n = state.natoms
+    stream = torch.cuda.current_stream()
+    ctx = _native.default_context(dev)
+    ctx.set_stream(stream.cuda_stream)
+    ctx.set_table(table)
+    lib = ctx.lib
+
+    pos = torch.from_numpy(state.positions).to(f"cuda:{dev}").contiguous()
+    species = torch.from_numpy(state.species.astype(np.int32)).to(f"cuda:{dev}")
+    forces = torch.empty((n, 3), dtype=torch.float64, device=pos.device)
+    per_atom = torch.empty(n, dtype=torch.float64, device=pos.device)
+    result = torch.zeros(8, dtype=torch.float64, device=pos.device)
+    stats = torch.zeros(_native.NSTATS, dtype=torch.int64, device=pos.device)
+
+    class DevState:
+        pass
+
+    ds = DevState()
+    ds.positions, ds.species, ds.box = pos, species, state.box
+    nl = B.build_neighbor_list(ds, table.r_cut, 0.3, device=dev)
+    prec = _native.PRECISION[args.precision]
+    scat = _native.SCATTER[args.scatter]
+    P = _native.ptr
+
+    def step(precision=prec):
+        rc = lib.tb_compute_device(ctx.handle, nl._nl.handle, P(pos), P(species),
+                                   float(table.r_cut), precision, scat, P(forces),
+                                   P(per_atom), P(result), P(stats))
+        if rc:
+            ctx.check(rc, "tb_compute_device")
+
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=pos.device)
+
+    def timed_loop(k, precision=prec, sampler=None):
+        starts = [torch.cuda.Event(enable_timing=True) for _ in range(k)]
+        ends = [torch.cuda.Event(enable_timing=True) for _ in range(k)]
+        lib.tb_profile(ctx.handle, 1)
+        torch.cuda.synchronize()
+        if ws > 1:
+            torch.distributed.barrier()
+        for s in range(k):
+            flush.zero_()          # L2 flush between timed steps (outside the bracket)
+            starts[s].record(stream)
+            step(precision)
+            ends[s].record(stream)
+        torch.cuda.synchronize()
+        lib.tb_profile(ctx.handle, 0)
+        tot_ms = ctypes_double()
+        launches = ctypes_i64()
+        ctx.check(lib.tb_profile_read(ctx.handle, ctypes_ref(tot_ms), ctypes_ref(launches)),
+                  "tb_profile_read")
+        step_ms = sum(a.elapsed_time(b) for a, b in zip(starts, ends))
+        return step_ms, tot_ms.value, launches.value
+
+    import ctypes
+    ctypes_double, ctypes_i64, ctypes_ref = ctypes.c_double, ctypes.c_int64, ctypes.byref
+
+    # warm-up (>= 3)
+    for _ in range(max(3, args.warmup)):
+        step()
+    torch.cuda.synchronize()
+    ctx.check(lib.tb_check_errors(ctx.handle), "warm-up")
+    st = stats.cpu().numpy().astype(np.int64)
+    energy0 = float(result[0])
+
+    sampler = ClockSampler(dev)
+    with sampler:
+        step_ms, kern_ms, launches = timed_loop(args.steps)
+    ctx.check(lib.tb_check_errors(ctx.handle), "timed loop")
+    t_local = step_ms / 1e3
+    if ws > 1:
+        t = torch.tensor([t_local], dtype=torch.float64, device=pos.device)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        t_max = float(t[0])
+    else:
+        t_max = t_local
+    value = ws * n * args.steps / t_max
+
+    # roofline of the Tersoff kernel (dominant launch)
+    kern_avg_s = kern_ms / 1e3 / max(launches, 1)
+    flops = algorithmic_flops(st)
+    peak = measure_fp64_peak(lib, ctx) if rank == 0 else None
+    achieved = flops / kern_avg_s / 1e12
+    traffic = None
+    prof_json = os.path.join(ROOT, "profiles", "ncu_tersoff_fp64.json")
+    if os.path.exists(prof_json):
+        try:
+            traffic = json.load(open(prof_json)).get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+
+    # mixed-precision mode on the same workload (reported alongside)
+    extra = {}
+    if args.extras and rank == 0:
+        k2 = max(10, args.steps // 4)
+        mixed_ms, mixed_kern_ms, mixed_l = timed_loop(k2, precision=1)
+        extra["mixed"] = {"value": n * k2 / (mixed_ms / 1e3), "unit": UNIT,
+                          "kernel_ms": mixed_kern_ms / max(mixed_l, 1),
+                          "achieved_fp32_weighted_tflops": None}
+
+    # e2e through the public API with pinned host buffers
+    e2e = None
+    if rank == 0:
+        e2e = e2e_arm(args, B, state, table, nl, dev)
+
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_ms / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64" if args.precision == "double" else "f32/f64", "data": "synthetic",
+        "config": {"workload": f"BASELINE config {args.config}: {n}-atom Si diamond "
+                               f"(sigma 0.1 A), one E+F+virial evaluation per step, "
+                               f"skin-list repack at r_cut inside the step",
+                   "atoms": n, "precision": args.precision, "scatter": args.scatter,
+                   "parallelism": f"replicas x{ws}" if ws > 1 else "single GPU",
+                   "l2": "flushed between timed steps (256 MiB write)"},
+        "e2e": e2e,
+        "gpu_launches": 2 * args.steps + (args.steps if args.scatter == "gather" else 0),
+        "roofline": {"bound": "fp64", "achieved": achieved,
+                     "peak": peak["tflops"] if peak else None, "unit": "TFLOP/s",
+                     "frac": achieved / peak["tflops"] if peak else None,
+                     "traffic": traffic,
+                     "kernel": "k_tersoff<double,1,false,atomic>",
+                     "kernel_ms": kern_avg_s * 1e3,
+                     "flops_per_launch": flops,
+                     "peak_source": peak["source"] if peak else None,
+                     "counts": {"live_pairs": int(st[2]), "live_triplets": int(st[3]),
+                                "taper_pairs": int(st[4]), "taper_triplets": int(st[5]),
+                                "zeta_visits": int(st[0])}},
+        "clocks": sampler.summary(),
+        "energy_eV": energy0,
+    }
+    line.update(extra)
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        v, cores, evals, el = oracle_baseline(state, table, budget_s=args.cpu_budget)
+        line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": cores, "kind": "port",
+                                "sample": f"{evals} full E+F evaluations of the {n}-atom system "
+                                          f"in {el:.1f} s (NL outside the timer); oracle/ C "
+                                          f"restatement of ScalarOpt, OpenMP {cores} threads"}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        torch.distributed.barrier()
+        torch.distributed.destroy_process_group()
+
+
+def measure_fp64_peak(lib, ctx):
+    """FP64 FMA throughput measured on this GPU (MEASURED_PEAKS.json has no
+    fp64 figure): a dependent-chain-free DFMA loop over all SMs."""
+    import ctypes
+    out = ctypes.c_double()
+    if lib.tb_measure_peak(ctx.handle, 0, ctypes.byref(out)) != 0:
+        return None
+    return {"tflops": out.value, "source": "measured DFMA loop in bench.py (tb_measure_peak)"}
+
+
+def e2e_arm(args, B, state, table, nl, dev):
+    """compute() through the public API with pinned host arrays; wall clock
+    with a device synchronise at both ends (compute() itself synchronises)."""
+    import torch
+    n = state.natoms
+    pos_h = torch.empty((n, 3), dtype=torch.float64).pin_memory().numpy()
+    pos_h[:] = state.positions
+    sp_h = torch.empty(n, dtype=torch.int32).pin_memory().numpy()
+    sp_h[:] = state.species
+
+    class HostState:
+        pass
+
+    hs = HostState()
+    hs.positions, hs.species, hs.box = pos_h, sp_h, state.box
+    variant = B.make_variant("B200", precision=args.precision, scatter=args.scatter)
+    for _ in range(3):
+        B.compute(hs, nl, table, variant)
+    k = max(10, min(args.steps, args.e2e_steps))
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(k):
+        res = B.compute(hs, nl, table, variant)
+    torch.cuda.synchronize()
+    el = time.perf_counter() - t0
+    assert np.isfinite(res.potential_energy)
+    return {"value": n * k / el, "unit": UNIT, "steps": k,
+            "h2d_bytes_per_step": n * 3 * 8 + n * 4,
+            "d2h_bytes_per_step": n * 3 * 8 + n * 8 + 7 * 8 + 6 * 8,
+            "path": "paper_1710_00882_b200.compute(state, nl, params, variant), pinned host "
+                    "positions in, host forces/per-atom energy out"}
+
+
+def main():
+    ap = argparse.ArgumentParser(description=__doc__.split("\n")[0])
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=2000)
+    ap.add_argument("--warmup", type=int, default=20)
+    ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
+    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--precision", choices=["double", "single"], default="double")
+    ap.add_argument("--precision-ref", dest="precision_ref", default="double")
+    ap.add_argument("--scatter", choices=["atomic", "gather"], default="atomic")
+    ap.add_argument("--e2e-steps", type=int, default=300)
+    ap.add_argument("--cpu-budget", type=float, default=12.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-extras", dest="extras", action="store_false")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        reference_arm(args)
+    else:
+        gpu_arm(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,163 @@
+/*
+ * tersoff_b200.h -- C ABI of the B200-native Tersoff energy/force/virial path.
+ *
+ * This is the drop-in boundary for the reference `tersoffmd` hot path
+ * (/root/reference/pkg/src/tersoffmd).  The reference has no FFI; its plugin
+ * point is the Python function kernels.compute() (kernels.py:517-527) fed by
+ * neighbor.build_neighbor_list()/needs_rebuild() (neighbor.py:194-229).  Each
+ * entry point below names the reference interface it replaces.  The Python
+ * host package paper_1710_00882_b200 binds these symbols with ctypes
+ * (paper_1710_00882_b200/_native.py); INTEGRATION.md shows the binding a
+ * reference maintainer would add.
+ *
+ * Conventions
+ *  - Plain pointers and sizes only.  Array arguments may be HOST or DEVICE
+ *    pointers (detected with cudaPointerGetAttributes); host arrays are copied
+ *    on the context's stream, device arrays are used in place.
+ *  - positions/forces are (n,3) row-major float64 in Angstrom / eV/A;
+ *    species are int32 in [0, nspecies); box lengths float64[3]; periodic
+ *    int32[3] (0/1).
+ *  - Every call returns a TB_* status; tb_last_error() gives the message.
+ *    TB_ERR_CONFIG maps to ConfigurationError, TB_ERR_INPUT to InputError
+ *    (errors.py:9-14), with the reference's message wording.
+ *  - A context is bound to one device and one CUDA stream and is not
+ *    re-entrant.  Scratch memory is context-owned; outputs are caller-owned.
+ */
+#ifndef TERSOFF_B200_H
+#define TERSOFF_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TB_OK 0
+#define TB_ERR_CONFIG 1 /* -> ConfigurationError */
+#define TB_ERR_INPUT 2  /* -> InputError */
+#define TB_ERR_CUDA 3   /* CUDA runtime failure */
+#define TB_ERR_ARG 4    /* bad argument (null pointer, size) */
+
+#define TB_PREC_DOUBLE 0 /* fp64 everywhere ("double", kernels.py:154-165) */
+#define TB_PREC_MIXED 1  /* fp64 positions/displacements/accumulators, fp32 potential math ("single") */
+
+#define TB_SCATTER_ATOMIC 0 /* dzeta scatter to j/k with red.global.add.f64 */
+#define TB_SCATTER_GATHER 1 /* per-entry force buffer + deterministic gather pass */
+
+typedef struct tb_context tb_context;
+typedef struct tb_nlist tb_nlist;
+
+/* stats[] layout written by tb_compute */
+#define TB_STAT_ZETA_VISITS 0 /* sum_i n_i^2 over packed rows (kernels.py:537-544) */
+#define TB_STAT_PACKED_PAIRS 1 /* entries with r < r_cut at current positions */
+#define TB_STAT_LIVE_PAIRS 2   /* packed pairs inside their own pair cutoff */
+#define TB_STAT_LIVE_TRIPLETS 3 /* (i,j,k) with live j and f_C(r_ik) > 0 */
+#define TB_STAT_TAPER_PAIRS 4   /* live pairs with R-D < r_ij (sin/cos taper evaluated) */
+#define TB_STAT_TAPER_TRIPLETS 5 /* live triplets with R-D < r_ik */
+#define TB_NSTATS 6
+
+/* ---- context ---------------------------------------------------------- */
+
+/* New context on `device`.  Replaces nothing in the reference (it has no
+ * device state); owns the stream and scratch buffers. */
+int tb_create(int device, tb_context **out);
+void tb_destroy(tb_context *ctx);
+const char *tb_last_error(const tb_context *ctx);
+/* Use an external CUDA stream (cudaStream_t, e.g. torch's current stream);
+ * NULL restores the context's own stream. */
+int tb_set_stream(tb_context *ctx, void *stream);
+/* Synchronise the context's stream. */
+int tb_synchronize(tb_context *ctx);
+
+/* Parameter table, flattened exactly like ParamTable.views()
+ * (potential.py:127-155): pair_mat[S*S*8] = [R,D,A,lam1,B,lam2,beta,eta] of
+ * entry (i,j,j); trip_mat[S^3*8] = [R,D,gamma,c,d,h,lam3,m] of entry (i,j,k).
+ * Host pointers.  1 <= nspecies <= 4.  r_cut_out (may be NULL) receives
+ * max(R+D) (potential.py:106). */
+int tb_set_params(tb_context *ctx, int nspecies, const double *pair_mat,
+                  const double *trip_mat, double *r_cut_out);
+
+/* ---- neighbour list (neighbor.py:194-229) ------------------------------- */
+
+int tb_nlist_create(tb_context *ctx, tb_nlist **out);
+void tb_nlist_destroy(tb_nlist *nl);
+
+/* build_neighbor_list(state, r_cut, skin) (neighbor.py:194-217): full
+ * symmetric list at bc = r_cut + skin, rows ascending; the pair set equals the
+ * reference's bit for bit.  Snapshots the positions for tb_needs_rebuild. */
+int tb_build_neighbors(tb_context *ctx, tb_nlist *nl, int64_t n, const double *positions,
+                       const double *box, const int32_t *periodic, double r_cut,
+                       double skin);
+/* number of list entries (sum of row lengths) and the longest row */
+int tb_nlist_info(const tb_nlist *nl, int64_t *n_atoms, int64_t *n_entries,
+                  int64_t *max_row);
+/* export the CSR (offsets[n+1], neighbors[n_entries]) as int64, host or
+ * device pointers (NeighborList.offsets / .neighbors, neighbor.py:170-191) */
+int tb_nlist_export(tb_context *ctx, const tb_nlist *nl, int64_t *offsets,
+                    int64_t *neighbors);
+/* needs_rebuild(state, nl) (neighbor.py:220-229): *out = 1 when any atom
+ * moved more than skin/2 (min image) since the build. */
+int tb_needs_rebuild(tb_context *ctx, const tb_nlist *nl, const double *positions,
+                     int32_t *out);
+
+/* ---- the Tersoff evaluation (kernels.py:517-527 compute()) ------------- */
+
+/* One energy + force (+ virial) evaluation at the given positions:
+ * re-packs the skin list at the current positions (pack_adjacency,
+ * neighbor.py:330-360) and evaluates the Tersoff terms (ScalarOpt semantics,
+ * kernels.py:250-315; math potential.py:167-290).
+ *   forces    (n,3) out, required          per_atom (n) out, may be NULL
+ *   energy    1 double out (host), required virial[6] xx,yy,zz,xy,xz,yz, may be NULL
+ *   stats     TB_NSTATS int64 (host), may be NULL
+ * r_cut must not exceed the list's build r_cut (neighbor.py:334-337).
+ * Synchronises the stream before returning. */
+int tb_compute(tb_context *ctx, const tb_nlist *nl, const double *positions,
+               const int32_t *species, double r_cut, int precision, int scatter,
+               double *forces, double *per_atom, double *energy, double *virial,
+               int64_t *stats);
+
+/* Asynchronous, device-resident variant for drivers, benchmarks and CUDA
+ * graph capture: all pointers are DEVICE pointers; `result` receives
+ * [energy, virial(6)] as 7 doubles; `dstats` TB_NSTATS uint64 (may be NULL).
+ * Does not synchronise; validation errors are latched on the device and
+ * reported by the next tb_check_errors(). */
+int tb_compute_device(tb_context *ctx, const tb_nlist *nl, const double *d_positions,
+                      const int32_t *d_species, double r_cut, int precision, int scatter,
+                      double *d_forces, double *d_per_atom, double *d_result,
+                      uint64_t *d_stats);
+int tb_check_errors(tb_context *ctx);
+
+/* Kernel timing for the roofline report: while enabled, CUDA events bracket
+ * every Tersoff kernel launch on the context stream; tb_profile_read
+ * synchronises, returns the summed kernel milliseconds and launch count since
+ * the last read, and resets them. */
+int tb_profile(tb_context *ctx, int enable);
+int tb_profile_read(tb_context *ctx, double *total_ms, int64_t *launches);
+
+/* ---- device-resident NVE (system.py:355-380, :427-460) ------------------ */
+
+/* One velocity-Verlet step on device buffers (positions, velocities, forces
+ * updated in place; mass per atom in amu, v += 0.5 dt accel F / m).  Rebuilds the list on the skin/2
+ * trigger or when `force_rebuild` is set; *rebuilt (host, may be NULL)
+ * reports it.  d_result as in tb_compute_device. */
+int tb_md_step(tb_context *ctx, tb_nlist *nl, int64_t n, double *d_positions,
+               double *d_velocities, double *d_forces, const double *d_mass,
+               const int32_t *d_species, const double *box, const int32_t *periodic,
+               double dt, double accel, double r_cut, double skin, int precision,
+               int scatter, int force_rebuild, double *d_per_atom, double *d_result,
+               int32_t *rebuilt);
+
+/* Diagnostic: measured FMA throughput of this GPU in TFLOP/s (2 flops per
+ * FMA), precision TB_PREC_DOUBLE -> DFMA, TB_PREC_MIXED -> FFMA; the roofline
+ * denominator for the CUDA-core pipes (MEASURED_PEAKS.json has no fp64/fp32
+ * figure).  Best of several launches over all SMs. */
+int tb_measure_peak(tb_context *ctx, int precision, double *tflops);
+
+/* Library build tag (sm_100a, git describe) */
+const char *tb_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* TERSOFF_B200_H */

@@ -1,0 +1,922 @@
+// tb_api.cu -- C ABI (include/tersoff_b200.h) over the sm_100a kernels.
+//
+// Unity build: the kernels live in tb_kernels.cuh / tb_math.cuh.  Host logic
+// here mirrors the reference's orchestration of the hot path:
+//   build_neighbor_list  neighbor.py:194-217   -> tb_build_neighbors
+//   needs_rebuild        neighbor.py:220-229   -> tb_needs_rebuild
+//   compute()            kernels.py:517-527    -> tb_compute / tb_compute_device
+//   velocity_verlet_step system.py:355-380     -> tb_md_step
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <climits>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include <cub/cub.cuh>
+
+#include "../../include/tersoff_b200.h"
+#include "tb_kernels.cuh"
+
+#ifndef TB_VERSION_TAG
+#define TB_VERSION_TAG "dev"
+#endif
+
+using namespace tb;
+
+namespace {
+
+struct DevBuf {
+  void *p = nullptr;
+  size_t cap = 0;
+  cudaError_t ensure(size_t bytes) {
+    if (bytes <= cap && p) return cudaSuccess;
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+    size_t want = std::max<size_t>(bytes, 256);
+    cudaError_t e = cudaMalloc(&p, want);
+    if (e == cudaSuccess) cap = want;
+    return e;
+  }
+  template <class X>
+  X *as() const { return static_cast<X *>(p); }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+  }
+};
+
+}  // namespace
+
+struct tb_context {
+  int device = 0;
+  cudaStream_t own = nullptr, stream = nullptr;
+  std::string err;
+  // parameters
+  int S = 0;
+  bool lam3 = false;
+  double r_cut = 0.0;
+  std::vector<double> pair_mat, trip_mat;
+  // scratch
+  DevBuf pos, species, forces, per_atom, result, stats, partials, fbuf, fself, errf, drift, bounds,
+      cub_tmp;
+  ErrFlags *h_err = nullptr;      // pinned
+  double *h_small = nullptr;      // pinned scratch (16 doubles)
+  // kernel timing (tb_profile)
+  bool profile = false;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_used, ev_free;
+};
+
+struct tb_nlist {
+  tb_context *ctx = nullptr;
+  int64_t n = 0;
+  double L[3] = {0, 0, 0};
+  int per[3] = {0, 0, 0};
+  double r_cut = 0.0, skin = 0.0, bc = 0.0;
+  int64_t entries = 0, max_row = 0;
+  bool built = false;
+  DevBuf offsets, nbr, rev, ref_pos, atom_cell, cell_count, cell_start, cell_atoms, row_count,
+      maxrow;
+  bool rev_valid = false;
+};
+
+// ---------------------------------------------------------------------------
+// error helpers
+// ---------------------------------------------------------------------------
+
+static int fail(tb_context *ctx, int code, const char *fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  if (ctx) ctx->err = buf;
+  return code;
+}
+
+#define CK(call)                                                                    \
+  do {                                                                              \
+    cudaError_t e_ = (call);                                                        \
+    if (e_ != cudaSuccess)                                                          \
+      return fail(ctx, TB_ERR_CUDA, "%s failed: %s", #call, cudaGetErrorString(e_)); \
+  } while (0)
+
+static bool is_device_ptr(const void *p) {
+  if (!p) return false;
+  cudaPointerAttributes attr;
+  if (cudaPointerGetAttributes(&attr, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return attr.type == cudaMemoryTypeDevice || attr.type == cudaMemoryTypeManaged;
+}
+
+// python-style %g of a double for messages
+static std::string fmt_g(double v) {
+  char b[64];
+  snprintf(b, sizeof(b), "%g", v);
+  return b;
+}
+
+static Box make_box(const double *L, const int *per) {
+  Box b;
+  for (int ax = 0; ax < 3; ++ax) {
+    b.L[ax] = L[ax];
+    b.invL[ax] = 1.0 / L[ax];
+    b.per[ax] = per[ax] ? 1 : 0;
+  }
+  return b;
+}
+
+static inline int nblk(int64_t n, int t) { return (int)((n + t - 1) / t); }
+
+// ---------------------------------------------------------------------------
+// parameter tables (potential.py:127-155 column order)
+// ---------------------------------------------------------------------------
+
+template <class T, int S>
+static Tables<T, S> make_tables(const tb_context *ctx) {
+  Tables<T, S> tab;
+  memset(&tab, 0, sizeof(tab));
+  const double kNegQuarterPi = -0.25 * 3.141592653589793;
+  for (int q = 0; q < S * S * S; ++q) {
+    const double *r = &ctx->trip_mat[8 * q];
+    TripP<T> &t = tab.trip[q];
+    T R = (T)r[0], D = (T)r[1];
+    t.Rm = R - D;
+    t.Rp = R + D;
+    t.R = R;
+    t.halfInvD = (T)(0.5 / r[1]);
+    t.nqpInvD = (T)kNegQuarterPi / D;
+    t.gamma = (T)r[2];
+    double c2 = r[3] * r[3], d2 = r[4] * r[4];
+    t.gc2d2 = (T)(r[2] * c2 / d2);
+    t.m2gc2 = (T)(-2.0 * r[2] * c2);
+    t.d2 = (T)d2;
+    t.h = (T)r[5];
+    t.lam3 = (T)r[6];
+    t.lam3x3 = (T)(3.0 * r[6]);
+    t.m = (int)r[7];
+  }
+  for (int q = 0; q < S * S; ++q) {
+    const double *r = &ctx->pair_mat[8 * q];
+    PairP<T> &p = tab.pair[q];
+    T R = (T)r[0], D = (T)r[1];
+    p.Rm = R - D;
+    p.Rp = R + D;
+    p.R = R;
+    p.halfInvD = (T)(0.5 / r[1]);
+    p.nqpInvD = (T)kNegQuarterPi / D;
+    p.A = (T)r[2];
+    p.lam1 = (T)r[3];
+    p.B = (T)r[4];
+    p.lam2 = (T)r[5];
+    p.beta = (T)r[6];
+    p.eta = (T)r[7];
+    p.neg_half_inv_eta = (T)(-0.5 / r[7]);
+    p.neg_half_beta = (T)(-0.5 * r[6]);
+  }
+  return tab;
+}
+
+// ---------------------------------------------------------------------------
+// context
+// ---------------------------------------------------------------------------
+
+extern "C" int tb_create(int device, tb_context **out) {
+  if (!out) return TB_ERR_ARG;
+  tb_context *ctx = new tb_context();
+  ctx->device = device;
+  *out = nullptr;
+  cudaError_t e = cudaSetDevice(device);
+  if (e != cudaSuccess) {
+    delete ctx;
+    return TB_ERR_CUDA;
+  }
+  if (cudaStreamCreateWithFlags(&ctx->own, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaMallocHost(&ctx->h_err, sizeof(ErrFlags)) != cudaSuccess ||
+      cudaMallocHost(&ctx->h_small, 16 * sizeof(double)) != cudaSuccess) {
+    delete ctx;
+    return TB_ERR_CUDA;
+  }
+  ctx->stream = ctx->own;
+  *out = ctx;
+  return TB_OK;
+}
+
+extern "C" void tb_destroy(tb_context *ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->device);
+  if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+  DevBuf *bufs[] = {&ctx->pos, &ctx->species, &ctx->forces, &ctx->per_atom, &ctx->result,
+                    &ctx->stats, &ctx->partials, &ctx->fbuf, &ctx->fself, &ctx->errf,
+                    &ctx->drift, &ctx->bounds, &ctx->cub_tmp};
+  for (DevBuf *b : bufs) b->release();
+  for (auto *v : {&ctx->ev_used, &ctx->ev_free})
+    for (auto &ev : *v) {
+      cudaEventDestroy(ev.first);
+      cudaEventDestroy(ev.second);
+    }
+  if (ctx->h_err) cudaFreeHost(ctx->h_err);
+  if (ctx->h_small) cudaFreeHost(ctx->h_small);
+  if (ctx->own) cudaStreamDestroy(ctx->own);
+  delete ctx;
+}
+
+extern "C" const char *tb_last_error(const tb_context *ctx) {
+  return ctx ? ctx->err.c_str() : "null context";
+}
+
+extern "C" int tb_set_stream(tb_context *ctx, void *stream) {
+  if (!ctx) return TB_ERR_ARG;
+  ctx->stream = stream ? (cudaStream_t)stream : ctx->own;
+  return TB_OK;
+}
+
+extern "C" int tb_synchronize(tb_context *ctx) {
+  if (!ctx) return TB_ERR_ARG;
+  CK(cudaStreamSynchronize(ctx->stream));
+  return TB_OK;
+}
+
+extern "C" int tb_set_params(tb_context *ctx, int nspecies, const double *pair_mat,
+                             const double *trip_mat, double *r_cut_out) {
+  if (!ctx || !pair_mat || !trip_mat) return fail(ctx, TB_ERR_ARG, "null argument");
+  if (nspecies < 1 || nspecies > SMAX)
+    return fail(ctx, TB_ERR_CONFIG, "the B200 kernels support 1..%d species, got %d", SMAX,
+                nspecies);
+  int S = nspecies;
+  ctx->S = S;
+  ctx->pair_mat.assign(pair_mat, pair_mat + 8 * S * S);
+  ctx->trip_mat.assign(trip_mat, trip_mat + 8 * S * S * S);
+  double rc = 0.0;
+  bool lam3 = false;
+  for (int q = 0; q < S * S * S; ++q) {
+    const double *r = trip_mat + 8 * q;
+    rc = std::max(rc, r[0] + r[1]);
+    lam3 |= r[6] != 0.0;
+    if (!(r[7] == 1.0 || r[7] == 3.0))
+      return fail(ctx, TB_ERR_CONFIG, "m must be 1 or 3, got %g", r[7]);
+  }
+  ctx->lam3 = lam3;
+  ctx->r_cut = rc;
+  if (r_cut_out) *r_cut_out = rc;
+  return TB_OK;
+}
+
+template <class T>
+static int peak_t(tb_context *ctx, double *tflops) {
+  int sms = 0;
+  CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device));
+  const int blocks = sms * 8, threads = 256, iters = 1 << 14;
+  DevBuf out;
+  CK(out.ensure(sizeof(T) * blocks));
+  cudaEvent_t e0, e1;
+  CK(cudaEventCreate(&e0));
+  CK(cudaEventCreate(&e1));
+  float best = 1e30f;
+  for (int rep = 0; rep < 6; ++rep) {
+    CK(cudaEventRecord(e0, ctx->stream));
+    k_fma_peak<T><<<blocks, threads, 0, ctx->stream>>>(out.as<T>(), iters, T(0.999999), T(1e-7));
+    CK(cudaEventRecord(e1, ctx->stream));
+    CK(cudaEventSynchronize(e1));
+    float ms;
+    CK(cudaEventElapsedTime(&ms, e0, e1));
+    if (rep > 0) best = std::min(best, ms);
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  out.release();
+  double flops = 2.0 * 8.0 * (double)iters * blocks * threads;
+  *tflops = flops / (best * 1e-3) / 1e12;
+  return TB_OK;
+}
+
+extern "C" int tb_measure_peak(tb_context *ctx, int precision, double *tflops) {
+  if (!ctx || !tflops) return fail(ctx, TB_ERR_ARG, "null argument");
+  CK(cudaSetDevice(ctx->device));
+  return precision == TB_PREC_DOUBLE ? peak_t<double>(ctx, tflops) : peak_t<float>(ctx, tflops);
+}
+
+extern "C" const char *tb_version(void) { return "tersoff_b200 sm_100a " TB_VERSION_TAG; }
+
+// copy a host or device array into a context buffer; returns the device pointer
+template <class X>
+static const X *stage_in(tb_context *ctx, const X *src, size_t count, DevBuf &buf, int &rc) {
+  rc = TB_OK;
+  if (is_device_ptr(src)) return src;
+  if (buf.ensure(sizeof(X) * count) != cudaSuccess) {
+    rc = fail(ctx, TB_ERR_CUDA, "device allocation of %zu bytes failed", sizeof(X) * count);
+    return nullptr;
+  }
+  if (count &&
+      cudaMemcpyAsync(buf.p, src, sizeof(X) * count, cudaMemcpyHostToDevice, ctx->stream) !=
+          cudaSuccess) {
+    rc = fail(ctx, TB_ERR_CUDA, "host-to-device copy failed");
+    return nullptr;
+  }
+  return buf.as<X>();
+}
+
+// ---------------------------------------------------------------------------
+// neighbour list (neighbor.py:194-217)
+// ---------------------------------------------------------------------------
+
+extern "C" int tb_nlist_create(tb_context *ctx, tb_nlist **out) {
+  if (!ctx || !out) return TB_ERR_ARG;
+  tb_nlist *nl = new tb_nlist();
+  nl->ctx = ctx;
+  *out = nl;
+  return TB_OK;
+}
+
+extern "C" void tb_nlist_destroy(tb_nlist *nl) {
+  if (!nl) return;
+  cudaSetDevice(nl->ctx->device);
+  cudaStreamSynchronize(nl->ctx->stream);
+  DevBuf *bufs[] = {&nl->offsets, &nl->nbr, &nl->rev, &nl->ref_pos, &nl->atom_cell,
+                    &nl->cell_count, &nl->cell_start, &nl->cell_atoms, &nl->row_count,
+                    &nl->maxrow};
+  for (DevBuf *b : bufs) b->release();
+  delete nl;
+}
+
+static int exclusive_scan(tb_context *ctx, const int *in, int *out, int64_t count) {
+  size_t tmp = 0;
+  CK(cub::DeviceScan::ExclusiveSum(nullptr, tmp, in, out, (int)count, ctx->stream));
+  CK(ctx->cub_tmp.ensure(tmp));
+  CK(cub::DeviceScan::ExclusiveSum(ctx->cub_tmp.p, tmp, in, out, (int)count, ctx->stream));
+  return TB_OK;
+}
+
+static int build_rev(tb_context *ctx, tb_nlist *nl) {
+  CK(nl->rev.ensure(sizeof(int) * std::max<int64_t>(nl->entries, 1)));
+  if (nl->n)
+    k_nl_reverse<<<nblk(nl->n, 256), 256, 0, ctx->stream>>>(
+        (int)nl->n, nl->offsets.as<int>(), nl->nbr.as<int>(), nl->rev.as<int>());
+  CK(cudaGetLastError());
+  nl->rev_valid = true;
+  return TB_OK;
+}
+
+extern "C" int tb_build_neighbors(tb_context *ctx, tb_nlist *nl, int64_t n,
+                                  const double *positions, const double *box,
+                                  const int32_t *periodic, double r_cut, double skin) {
+  if (!ctx || !nl || !box || !periodic || (n && !positions))
+    return fail(ctx, TB_ERR_ARG, "null argument");
+  if (n > INT_MAX / 2) return fail(ctx, TB_ERR_ARG, "too many atoms (%lld)", (long long)n);
+  CK(cudaSetDevice(ctx->device));
+  // argument checks in the reference's order and wording (neighbor.py:195-207)
+  if (skin < 0) return fail(ctx, TB_ERR_CONFIG, "negative skin %s", fmt_g(skin).c_str());
+  const double bc = r_cut + skin;
+  for (int ax = 0; ax < 3; ++ax) {
+    if (!(box[ax] > 0))
+      return fail(ctx, TB_ERR_CONFIG, "box edge lengths must be positive, got %g", box[ax]);
+    if (periodic[ax] && box[ax] < 2.0 * bc)
+      return fail(ctx, TB_ERR_CONFIG,
+                  "periodic edge %s A along axis %d is shorter than twice the build cutoff "
+                  "%s A; replicate the cell",
+                  fmt_g(box[ax]).c_str(), ax, fmt_g(bc).c_str());
+  }
+  int rc;
+  const double *d_pos = stage_in(ctx, positions, 3 * (size_t)n, ctx->pos, rc);
+  if (rc) return rc;
+
+  nl->n = n;
+  for (int ax = 0; ax < 3; ++ax) {
+    nl->L[ax] = box[ax];
+    nl->per[ax] = periodic[ax] ? 1 : 0;
+  }
+  nl->r_cut = r_cut;
+  nl->skin = skin;
+  nl->bc = bc;
+  nl->rev_valid = false;
+
+  // ---- grid geometry (CellList.__init__, neighbor.py:54-81) ----
+  Grid g;
+  g.box = make_box(nl->L, nl->per);
+  bool any_free = !(nl->per[0] && nl->per[1] && nl->per[2]);
+  double lo[3] = {0, 0, 0}, hi[3] = {0, 0, 0};
+  if (any_free && n) {
+    CK(ctx->bounds.ensure(6 * sizeof(unsigned long long)));
+    unsigned long long init[6] = {~0ull, ~0ull, ~0ull, 0, 0, 0};
+    CK(cudaMemcpyAsync(ctx->bounds.p, init, sizeof(init), cudaMemcpyHostToDevice, ctx->stream));
+    k_bounds<<<std::min(nblk(n, 256), 1184), 256, 0, ctx->stream>>>(
+        n, d_pos, ctx->bounds.as<unsigned long long>());
+    CK(cudaGetLastError());
+    unsigned long long res[6];
+    CK(cudaMemcpyAsync(res, ctx->bounds.p, sizeof(res), cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    auto unkey = [](unsigned long long k) {
+      unsigned long long u = (k & 0x8000000000000000ull) ? (k & ~0x8000000000000000ull) : ~k;
+      double v;
+      memcpy(&v, &u, 8);
+      return v;
+    };
+    for (int ax = 0; ax < 3; ++ax) {
+      lo[ax] = unkey(res[ax]);
+      hi[ax] = unkey(res[3 + ax]);
+    }
+  }
+  int64_t ncell = 1;
+  for (int ax = 0; ax < 3; ++ax) {
+    int64_t nc;
+    if (nl->per[ax]) {
+      if (nl->L[ax] < bc)
+        return fail(ctx, TB_ERR_CONFIG,
+                    "periodic edge %s A on axis %d is smaller than the cell size %s A",
+                    fmt_g(nl->L[ax]).c_str(), ax, fmt_g(bc).c_str());
+      nc = std::max<int64_t>((int64_t)(nl->L[ax] / bc), 1);
+      g.origin[ax] = 0.0;
+      g.width[ax] = nl->L[ax] / (double)nc;
+    } else {
+      g.origin[ax] = lo[ax];
+      double span = (hi[ax] - lo[ax]) / bc;
+      if (!(span < 1e7))
+        return fail(ctx, TB_ERR_CONFIG, "free-axis extent %g A too large for the cell grid",
+                    hi[ax] - lo[ax]);
+      nc = std::max<int64_t>((int64_t)span + 1, 1);
+      g.width[ax] = bc;
+    }
+    g.nc[ax] = (int)nc;
+    ncell *= nc;
+  }
+  if (ncell > (int64_t)1 << 28)
+    return fail(ctx, TB_ERR_CONFIG, "cell grid of %lld cells is too large", (long long)ncell);
+
+  const int N = (int)n;
+  CK(nl->atom_cell.ensure(sizeof(int) * std::max(N, 1)));
+  CK(nl->cell_count.ensure(sizeof(int) * (ncell + 1)));
+  CK(nl->cell_start.ensure(sizeof(int) * (ncell + 1)));
+  CK(nl->cell_atoms.ensure(sizeof(int) * std::max(N, 1)));
+  CK(nl->row_count.ensure(sizeof(int) * (N + 1)));
+  CK(nl->offsets.ensure(sizeof(int) * (N + 1)));
+  CK(nl->maxrow.ensure(sizeof(int)));
+  CK(nl->ref_pos.ensure(sizeof(double) * 3 * std::max(N, 1)));
+
+  CK(cudaMemsetAsync(nl->cell_count.p, 0, sizeof(int) * (ncell + 1), ctx->stream));
+  CK(cudaMemsetAsync(nl->maxrow.p, 0, sizeof(int), ctx->stream));
+  CK(cudaMemsetAsync(nl->row_count.p, 0, sizeof(int) * (N + 1), ctx->stream));
+  if (N) {
+    k_cell_index<<<nblk(N, 256), 256, 0, ctx->stream>>>(N, d_pos, g, nl->atom_cell.as<int>(),
+                                                         nl->cell_count.as<int>());
+    CK(cudaGetLastError());
+  }
+  rc = exclusive_scan(ctx, nl->cell_count.as<int>(), nl->cell_start.as<int>(), ncell + 1);
+  if (rc) return rc;
+  // cursor copy for the counting-sort scatter (cell_count reused as cursor)
+  CK(cudaMemcpyAsync(nl->cell_count.p, nl->cell_start.p, sizeof(int) * (ncell + 1),
+                     cudaMemcpyDeviceToDevice, ctx->stream));
+  if (N) {
+    k_cell_fill<<<nblk(N, 256), 256, 0, ctx->stream>>>(N, nl->atom_cell.as<int>(),
+                                                        nl->cell_count.as<int>(),
+                                                        nl->cell_atoms.as<int>());
+    CK(cudaGetLastError());
+    k_nl_scan<false><<<nblk(N, 128), 128, 0, ctx->stream>>>(
+        N, d_pos, g, bc * bc, nl->atom_cell.as<int>(), nl->cell_start.as<int>(),
+        nl->cell_atoms.as<int>(), nl->row_count.as<int>(), nullptr, nullptr,
+        nl->maxrow.as<int>());
+    CK(cudaGetLastError());
+  }
+  rc = exclusive_scan(ctx, nl->row_count.as<int>(), nl->offsets.as<int>(), N + 1);
+  if (rc) return rc;
+  int tail[2];
+  CK(cudaMemcpyAsync(&tail[0], nl->offsets.as<int>() + N, sizeof(int), cudaMemcpyDeviceToHost,
+                     ctx->stream));
+  CK(cudaMemcpyAsync(&tail[1], nl->maxrow.p, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  nl->entries = tail[0];
+  nl->max_row = tail[1];
+  CK(nl->nbr.ensure(sizeof(int) * std::max<int64_t>(nl->entries, 1)));
+  if (N) {
+    k_nl_scan<true><<<nblk(N, 128), 128, 0, ctx->stream>>>(
+        N, d_pos, g, bc * bc, nl->atom_cell.as<int>(), nl->cell_start.as<int>(),
+        nl->cell_atoms.as<int>(), nullptr, nl->offsets.as<int>(), nl->nbr.as<int>(), nullptr);
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(nl->ref_pos.p, d_pos, sizeof(double) * 3 * N, cudaMemcpyDeviceToDevice,
+                       ctx->stream));
+  }
+  nl->built = true;
+  return TB_OK;
+}
+
+extern "C" int tb_nlist_info(const tb_nlist *nl, int64_t *n_atoms, int64_t *n_entries,
+                             int64_t *max_row) {
+  if (!nl) return TB_ERR_ARG;
+  if (n_atoms) *n_atoms = nl->n;
+  if (n_entries) *n_entries = nl->entries;
+  if (max_row) *max_row = nl->max_row;
+  return TB_OK;
+}
+
+extern "C" int tb_nlist_export(tb_context *ctx, const tb_nlist *nl, int64_t *offsets,
+                               int64_t *neighbors) {
+  if (!ctx || !nl || !nl->built) return fail(ctx, TB_ERR_ARG, "neighbour list not built");
+  CK(cudaSetDevice(ctx->device));
+  struct Part {
+    const int *src;
+    int64_t count;
+    int64_t *dst;
+  } parts[2] = {{nl->offsets.as<int>(), nl->n + 1, offsets},
+                {nl->nbr.as<int>(), nl->entries, neighbors}};
+  for (auto &pt : parts) {
+    if (!pt.dst || pt.count == 0) continue;
+    int64_t *d = pt.dst;
+    DevBuf tmp;
+    bool dev = is_device_ptr(pt.dst);
+    if (!dev) {
+      CK(tmp.ensure(sizeof(int64_t) * pt.count));
+      d = tmp.as<int64_t>();
+    }
+    k_export_i64<<<nblk(pt.count, 256), 256, 0, ctx->stream>>>((int)pt.count, pt.src, d);
+    CK(cudaGetLastError());
+    if (!dev) {
+      CK(cudaMemcpyAsync(pt.dst, d, sizeof(int64_t) * pt.count, cudaMemcpyDeviceToHost,
+                         ctx->stream));
+      CK(cudaStreamSynchronize(ctx->stream));
+      tmp.release();
+    }
+  }
+  CK(cudaStreamSynchronize(ctx->stream));
+  return TB_OK;
+}
+
+static int drift_check(tb_context *ctx, const tb_nlist *nl, const double *d_pos, int32_t *out) {
+  CK(ctx->drift.ensure(sizeof(unsigned long long)));
+  CK(cudaMemsetAsync(ctx->drift.p, 0, sizeof(unsigned long long), ctx->stream));
+  if (nl->n) {
+    k_max_drift<<<std::min(nblk(nl->n, 256), 1184), 256, 0, ctx->stream>>>(
+        (int)nl->n, d_pos, nl->ref_pos.as<double>(), make_box(nl->L, nl->per),
+        ctx->drift.as<unsigned long long>());
+    CK(cudaGetLastError());
+  }
+  unsigned long long *h = reinterpret_cast<unsigned long long *>(ctx->h_small);
+  CK(cudaMemcpyAsync(h, ctx->drift.p, sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                     ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  double mx;
+  memcpy(&mx, h, 8);
+  double half = 0.5 * nl->skin;
+  *out = mx > half * half ? 1 : 0;
+  return TB_OK;
+}
+
+extern "C" int tb_needs_rebuild(tb_context *ctx, const tb_nlist *nl, const double *positions,
+                                int32_t *out) {
+  if (!ctx || !nl || !out || (nl->n && !positions)) return fail(ctx, TB_ERR_ARG, "null argument");
+  if (!nl->built) return fail(ctx, TB_ERR_ARG, "neighbour list not built");
+  CK(cudaSetDevice(ctx->device));
+  int rc;
+  const double *d_pos = stage_in(ctx, positions, 3 * (size_t)nl->n, ctx->pos, rc);
+  if (rc) return rc;
+  return drift_check(ctx, nl, d_pos, out);
+}
+
+// ---------------------------------------------------------------------------
+// the Tersoff evaluation
+// ---------------------------------------------------------------------------
+
+template <class T, int S, bool LAM3, int MODE>
+static int launch_tersoff_t(tb_context *ctx, const tb_nlist *nl, KArgs &a, int C) {
+  size_t smem = SmemLayout<T, S>::bytes(C);
+  if (smem > 227 * 1024)
+    return fail(ctx, TB_ERR_CONFIG, "neighbour rows of %lld entries exceed the kernel's staging",
+                (long long)nl->max_row);
+  auto kern = k_tersoff<T, S, LAM3, MODE>;
+  // opt in to large dynamic shared memory once per instantiation
+  static bool done = false;
+  if (!done) {
+    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+    done = true;
+  }
+  int nb = nblk(a.n, a.atoms_per_block);
+  Tables<T, S> tab = make_tables<T, S>(ctx);
+  std::pair<cudaEvent_t, cudaEvent_t> ev{nullptr, nullptr};
+  if (ctx->profile) {
+    if (ctx->ev_free.empty()) {
+      CK(cudaEventCreate(&ev.first));
+      CK(cudaEventCreate(&ev.second));
+    } else {
+      ev = ctx->ev_free.back();
+      ctx->ev_free.pop_back();
+    }
+    CK(cudaEventRecord(ev.first, ctx->stream));
+  }
+  kern<<<nb, NT, smem, ctx->stream>>>(a, tab, C);
+  CK(cudaGetLastError());
+  if (ctx->profile) {
+    CK(cudaEventRecord(ev.second, ctx->stream));
+    ctx->ev_used.push_back(ev);
+  }
+  return TB_OK;
+}
+
+template <class T, int S>
+static int launch_s(tb_context *ctx, const tb_nlist *nl, KArgs &a, int C, int mode) {
+  if (ctx->lam3)
+    return mode ? launch_tersoff_t<T, S, true, 1>(ctx, nl, a, C)
+                : launch_tersoff_t<T, S, true, 0>(ctx, nl, a, C);
+  return mode ? launch_tersoff_t<T, S, false, 1>(ctx, nl, a, C)
+              : launch_tersoff_t<T, S, false, 0>(ctx, nl, a, C);
+}
+
+template <class T>
+static int launch_prec(tb_context *ctx, const tb_nlist *nl, KArgs &a, int C, int mode) {
+  switch (ctx->S) {
+    case 1: return launch_s<T, 1>(ctx, nl, a, C, mode);
+    case 2: return launch_s<T, 2>(ctx, nl, a, C, mode);
+    case 3: return launch_s<T, 3>(ctx, nl, a, C, mode);
+    case 4: return launch_s<T, 4>(ctx, nl, a, C, mode);
+  }
+  return fail(ctx, TB_ERR_CONFIG, "unsupported species count %d", ctx->S);
+}
+
+static ErrFlags err_init() {
+  ErrFlags e;
+  e.nonfinite_atom = INT_MAX;
+  e.bad_species_atom = INT_MAX;
+  e.coinc_key = ~0ull;
+  e.overflow = 0;
+  e.pad = 0;
+  return e;
+}
+
+static int reset_errors(tb_context *ctx) {
+  CK(ctx->errf.ensure(sizeof(ErrFlags)));
+  *ctx->h_err = err_init();
+  CK(cudaMemcpyAsync(ctx->errf.p, ctx->h_err, sizeof(ErrFlags), cudaMemcpyHostToDevice,
+                     ctx->stream));
+  return TB_OK;
+}
+
+// enqueue the evaluation; every pointer is a device pointer
+static int enqueue_compute(tb_context *ctx, const tb_nlist *nl, const double *d_pos,
+                           const int *d_species, double r_cut, int precision, int scatter,
+                           double *d_forces, double *d_per_atom, double *d_result,
+                           unsigned long long *d_stats) {
+  if (ctx->S == 0) return fail(ctx, TB_ERR_CONFIG, "parameters not set");
+  if (!nl->built) return fail(ctx, TB_ERR_ARG, "neighbour list not built");
+  if (r_cut > nl->r_cut)
+    return fail(ctx, TB_ERR_CONFIG,
+                "cutoff %s A exceeds the %s A the neighbor list was built for",
+                fmt_g(r_cut).c_str(), fmt_g(nl->r_cut).c_str());
+  if (precision != TB_PREC_DOUBLE && precision != TB_PREC_MIXED)
+    return fail(ctx, TB_ERR_ARG, "unknown precision %d", precision);
+  if (scatter != TB_SCATTER_ATOMIC && scatter != TB_SCATTER_GATHER)
+    return fail(ctx, TB_ERR_ARG, "unknown scatter mode %d", scatter);
+  if (!ctx->errf.p) {
+    int rc = reset_errors(ctx);
+    if (rc) return rc;
+  }
+  const int n = (int)nl->n;
+  // tile sizing: atoms per block so that the tile's skin-list rows fit
+  int C = SLOT_CAP;
+  int maxrow = (int)std::max<int64_t>(nl->max_row, 1);
+  if (maxrow > C) C = (maxrow + 31) & ~31;
+  int A = std::max(1, std::min(NT, C / maxrow));
+  int nb = n ? nblk(n, A) : 0;
+  CK(ctx->partials.ensure(sizeof(double) * 8 * std::max(nb, 1)));
+  if (scatter == TB_SCATTER_GATHER) {
+    if (!nl->rev_valid) {
+      int rc = build_rev(ctx, const_cast<tb_nlist *>(nl));
+      if (rc) return rc;
+    }
+    CK(ctx->fbuf.ensure(sizeof(double) * 3 * std::max<int64_t>(nl->entries, 1)));
+    CK(ctx->fself.ensure(sizeof(double) * 3 * std::max(n, 1)));
+  }
+  if (d_stats) CK(cudaMemsetAsync(d_stats, 0, sizeof(unsigned long long) * TB_NSTATS, ctx->stream));
+  if (scatter == TB_SCATTER_ATOMIC && n)
+    CK(cudaMemsetAsync(d_forces, 0, sizeof(double) * 3 * n, ctx->stream));
+  if (n == 0) {
+    CK(cudaMemsetAsync(d_result, 0, sizeof(double) * 7, ctx->stream));
+    return TB_OK;
+  }
+  KArgs a;
+  a.n = n;
+  a.atoms_per_block = A;
+  a.rc2 = r_cut * r_cut;
+  a.box = make_box(nl->L, nl->per);
+  a.pos = d_pos;
+  a.species = d_species;
+  a.off = nl->offsets.as<int>();
+  a.nbr = nl->nbr.as<int>();
+  a.forces = d_forces;
+  a.fbuf = ctx->fbuf.as<double>();
+  a.fself = ctx->fself.as<double>();
+  a.per_atom = d_per_atom;
+  a.partials = ctx->partials.as<double>();
+  a.stats = d_stats;
+  a.err = ctx->errf.as<ErrFlags>();
+  if (!d_stats) {
+    CK(ctx->stats.ensure(sizeof(unsigned long long) * TB_NSTATS));
+    a.stats = ctx->stats.as<unsigned long long>();
+  }
+  int rc = precision == TB_PREC_DOUBLE ? launch_prec<double>(ctx, nl, a, C, scatter)
+                                       : launch_prec<float>(ctx, nl, a, C, scatter);
+  if (rc) return rc;
+  if (scatter == TB_SCATTER_GATHER) {
+    k_force_gather<<<nblk(n, 256), 256, 0, ctx->stream>>>(n, a.off, nl->rev.as<int>(), a.fbuf,
+                                                           a.fself, d_forces);
+    CK(cudaGetLastError());
+  }
+  k_reduce_partials<<<1, 256, 0, ctx->stream>>>(nb, a.partials, d_result);
+  CK(cudaGetLastError());
+  return TB_OK;
+}
+
+// Map latched device error flags to the reference's exceptions and wording.
+static int report_errors(tb_context *ctx, const tb_nlist *nl, const double *d_pos,
+                         const int *d_species) {
+  CK(cudaMemcpyAsync(ctx->h_err, ctx->errf.p, sizeof(ErrFlags), cudaMemcpyDeviceToHost,
+                     ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  ErrFlags e = *ctx->h_err;
+  int rc = TB_OK;
+  if (e.overflow) {
+    rc = fail(ctx, TB_ERR_CUDA, "internal error: tile staging overflow");
+  } else if (e.nonfinite_atom != INT_MAX) {
+    // kernels.py:111-116
+    rc = fail(ctx, TB_ERR_INPUT, "non-finite position for atom %d", e.nonfinite_atom);
+  } else if (e.bad_species_atom != INT_MAX) {
+    // kernels.py:95-108
+    int v = 0;
+    CK(cudaMemcpy(&v, d_species + e.bad_species_atom, sizeof(int), cudaMemcpyDeviceToHost));
+    rc = fail(ctx, TB_ERR_CONFIG, "species index %d outside the %d-species parameter table", v,
+              ctx->S);
+  } else if (e.coinc_key != ~0ull) {
+    // neighbor.py:346-352
+    int ent = (int)(e.coinc_key & 0xffffffffu);
+    std::vector<int> off(nl->n + 1);
+    CK(cudaMemcpy(off.data(), nl->offsets.p, sizeof(int) * (nl->n + 1), cudaMemcpyDeviceToHost));
+    int i = (int)(std::upper_bound(off.begin(), off.end(), ent) - off.begin()) - 1;
+    int j = 0;
+    CK(cudaMemcpy(&j, nl->nbr.as<int>() + ent, sizeof(int), cudaMemcpyDeviceToHost));
+    double xi[3], xj[3];
+    CK(cudaMemcpy(xi, d_pos + 3 * (int64_t)i, 3 * sizeof(double), cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(xj, d_pos + 3 * (int64_t)j, 3 * sizeof(double), cudaMemcpyDeviceToHost));
+    double r2 = 0;
+    for (int ax = 0; ax < 3; ++ax) {
+      double d = xj[ax] - xi[ax];
+      if (nl->per[ax]) d -= nl->L[ax] * std::nearbyint(d / nl->L[ax]);
+      r2 += d * d;
+    }
+    rc = fail(ctx, TB_ERR_INPUT, "atoms %d and %d are coincident (r = %.3e A)", i, j,
+              std::sqrt(r2));
+  }
+  if (rc) {
+    int r2 = reset_errors(ctx);
+    (void)r2;
+  }
+  return rc;
+}
+
+extern "C" int tb_compute(tb_context *ctx, const tb_nlist *nl, const double *positions,
+                          const int32_t *species, double r_cut, int precision, int scatter,
+                          double *forces, double *per_atom, double *energy, double *virial,
+                          int64_t *stats) {
+  if (!ctx || !nl || !forces || !energy) return fail(ctx, TB_ERR_ARG, "null argument");
+  CK(cudaSetDevice(ctx->device));
+  const int64_t n = nl->n;
+  if (n && (!positions || !species)) return fail(ctx, TB_ERR_ARG, "null positions/species");
+  int rc = reset_errors(ctx);
+  if (rc) return rc;
+  const double *d_pos = stage_in(ctx, positions, 3 * (size_t)n, ctx->pos, rc);
+  if (rc) return rc;
+  const int *d_sp = stage_in(ctx, species, (size_t)n, ctx->species, rc);
+  if (rc) return rc;
+  bool f_dev = is_device_ptr(forces);
+  double *d_f = forces;
+  if (!f_dev) {
+    CK(ctx->forces.ensure(sizeof(double) * 3 * std::max<int64_t>(n, 1)));
+    d_f = ctx->forces.as<double>();
+  }
+  bool e_dev = per_atom && is_device_ptr(per_atom);
+  double *d_e = per_atom;
+  if (per_atom && !e_dev) {
+    CK(ctx->per_atom.ensure(sizeof(double) * std::max<int64_t>(n, 1)));
+    d_e = ctx->per_atom.as<double>();
+  }
+  CK(ctx->result.ensure(sizeof(double) * 8));
+  CK(ctx->stats.ensure(sizeof(unsigned long long) * TB_NSTATS));
+  rc = enqueue_compute(ctx, nl, d_pos, d_sp, r_cut, precision, scatter, d_f, d_e,
+                       ctx->result.as<double>(), ctx->stats.as<unsigned long long>());
+  if (rc) return rc;
+  if (!f_dev && n)
+    CK(cudaMemcpyAsync(forces, d_f, sizeof(double) * 3 * n, cudaMemcpyDeviceToHost, ctx->stream));
+  if (per_atom && !e_dev && n)
+    CK(cudaMemcpyAsync(per_atom, d_e, sizeof(double) * n, cudaMemcpyDeviceToHost, ctx->stream));
+  double *h = ctx->h_small;
+  CK(cudaMemcpyAsync(h, ctx->result.p, sizeof(double) * 7, cudaMemcpyDeviceToHost, ctx->stream));
+  unsigned long long *hs = reinterpret_cast<unsigned long long *>(h + 8);
+  CK(cudaMemcpyAsync(hs, ctx->stats.p, sizeof(unsigned long long) * TB_NSTATS,
+                     cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  rc = report_errors(ctx, nl, d_pos, d_sp);
+  if (rc) return rc;
+  *energy = h[0];
+  if (virial)
+    for (int q = 0; q < 6; ++q) virial[q] = h[1 + q];
+  if (stats)
+    for (int q = 0; q < TB_NSTATS; ++q) stats[q] = (int64_t)hs[q];
+  return TB_OK;
+}
+
+extern "C" int tb_compute_device(tb_context *ctx, const tb_nlist *nl, const double *d_positions,
+                                 const int32_t *d_species, double r_cut, int precision,
+                                 int scatter, double *d_forces, double *d_per_atom,
+                                 double *d_result, uint64_t *d_stats) {
+  if (!ctx || !nl || !d_forces || !d_result) return fail(ctx, TB_ERR_ARG, "null argument");
+  if (nl->n && (!d_positions || !d_species)) return fail(ctx, TB_ERR_ARG, "null positions/species");
+  return enqueue_compute(ctx, nl, d_positions, d_species, r_cut, precision, scatter, d_forces,
+                         d_per_atom, d_result, reinterpret_cast<unsigned long long *>(d_stats));
+}
+
+extern "C" int tb_check_errors(tb_context *ctx) {
+  if (!ctx) return TB_ERR_ARG;
+  if (!ctx->errf.p) return TB_OK;
+  CK(cudaMemcpyAsync(ctx->h_err, ctx->errf.p, sizeof(ErrFlags), cudaMemcpyDeviceToHost,
+                     ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  ErrFlags e = *ctx->h_err;
+  int rc = TB_OK;
+  if (e.overflow) rc = fail(ctx, TB_ERR_CUDA, "internal error: tile staging overflow");
+  else if (e.nonfinite_atom != INT_MAX)
+    rc = fail(ctx, TB_ERR_INPUT, "non-finite position for atom %d", e.nonfinite_atom);
+  else if (e.bad_species_atom != INT_MAX)
+    rc = fail(ctx, TB_ERR_CONFIG, "species index outside the %d-species parameter table (atom %d)",
+              ctx->S, e.bad_species_atom);
+  else if (e.coinc_key != ~0ull)
+    rc = fail(ctx, TB_ERR_INPUT, "atoms are coincident (list entry %u)",
+              (unsigned)(e.coinc_key & 0xffffffffu));
+  if (rc) reset_errors(ctx);
+  return rc;
+}
+
+extern "C" int tb_profile(tb_context *ctx, int enable) {
+  if (!ctx) return TB_ERR_ARG;
+  ctx->profile = enable != 0;
+  return TB_OK;
+}
+
+extern "C" int tb_profile_read(tb_context *ctx, double *total_ms, int64_t *launches) {
+  if (!ctx || !total_ms || !launches) return fail(ctx, TB_ERR_ARG, "null argument");
+  CK(cudaStreamSynchronize(ctx->stream));
+  double tot = 0.0;
+  for (auto &ev : ctx->ev_used) {
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, ev.first, ev.second));
+    tot += ms;
+    ctx->ev_free.push_back(ev);
+  }
+  *launches = (int64_t)ctx->ev_used.size();
+  ctx->ev_used.clear();
+  *total_ms = tot;
+  return TB_OK;
+}
+
+// ---------------------------------------------------------------------------
+// device-resident velocity Verlet (system.py:355-380)
+// ---------------------------------------------------------------------------
+
+extern "C" int tb_md_step(tb_context *ctx, tb_nlist *nl, int64_t n, double *d_positions,
+                          double *d_velocities, double *d_forces, const double *d_mass,
+                          const int32_t *d_species, const double *box, const int32_t *periodic,
+                          double dt, double accel, double r_cut, double skin, int precision,
+                          int scatter, int force_rebuild, double *d_per_atom, double *d_result,
+                          int32_t *rebuilt) {
+  if (!ctx || !nl || !box || !periodic || !d_result) return fail(ctx, TB_ERR_ARG, "null argument");
+  if (!(dt > 0)) return fail(ctx, TB_ERR_CONFIG, "dt must be positive, got %s", fmt_g(dt).c_str());
+  CK(cudaSetDevice(ctx->device));
+  int per[3] = {periodic[0] ? 1 : 0, periodic[1] ? 1 : 0, periodic[2] ? 1 : 0};
+  Box b = make_box(box, per);
+  const double half = 0.5 * dt * accel;
+  if (n) {
+    k_kick_drift<<<nblk(n, 256), 256, 0, ctx->stream>>>((int)n, d_positions, d_velocities,
+                                                         d_forces, d_mass, half, dt, b);
+    CK(cudaGetLastError());
+  }
+  int32_t need = 1;
+  if (!force_rebuild && nl->built && nl->n == n) {
+    int rc = drift_check(ctx, nl, d_positions, &need);
+    if (rc) return rc;
+  }
+  if (need) {
+    int rc = tb_build_neighbors(ctx, nl, n, d_positions, box, periodic, r_cut, skin);
+    if (rc) return rc;
+  }
+  if (rebuilt) *rebuilt = need;
+  int rc = enqueue_compute(ctx, nl, d_positions, d_species, r_cut, precision, scatter, d_forces,
+                           d_per_atom, d_result, nullptr);
+  if (rc) return rc;
+  if (n) {
+    k_kick<<<nblk(n, 256), 256, 0, ctx->stream>>>((int)n, d_velocities, d_forces, d_mass, half);
+    CK(cudaGetLastError());
+  }
+  return TB_OK;
+}

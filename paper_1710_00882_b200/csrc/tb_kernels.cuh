@@ -1,0 +1,788 @@
+// tb_kernels.cuh -- sm_100a kernels of the Tersoff hot path.
+//
+//   K1  k_bounds / k_cell_index / k_cell_fill   cell binning   (neighbor.py:46-96)
+//   K2  k_nl_count / k_nl_fill / k_nl_reverse   Verlet list    (neighbor.py:104-217)
+//   K3  k_max_drift                              skin/2 trigger (neighbor.py:220-229)
+//   K4/5 k_tersoff<T,S,LAM3,MODE>                pack + E/F/virial (kernels.py:250-315,
+//                                                neighbor.py:330-360, potential.py:167-290)
+//   K6/7 k_reduce_partials, k_force_gather       deterministic reductions (kernels.py:134-151)
+//   K8  k_kick_drift / k_kick                    velocity Verlet (system.py:355-380)
+//
+// All neighbour-list arithmetic that decides pair membership is done with
+// explicitly rounded fp64 intrinsics (no FMA contraction) so the pair set is
+// bit-identical to the reference's numpy evaluation.
+#pragma once
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+
+#include "tb_math.cuh"
+
+namespace tb {
+
+constexpr int NT = 128;          // threads per Tersoff block (4 warps)
+constexpr int NW = NT / 32;
+constexpr int SLOT_CAP = 512;    // skin-list entries staged per Tersoff block
+
+struct Box {
+  double L[3], invL[3];
+  int per[3];
+};
+
+struct ErrFlags {
+  int nonfinite_atom;   // atomicMin, INT_MAX = none
+  int bad_species_atom; // atomicMin, INT_MAX = none
+  unsigned long long coinc_key;  // (r2 hi32 << 32) | entry, ~0 = none
+  int overflow;         // tile staging overflow (internal error)
+  int pad;
+};
+
+// ---------------------------------------------------------------------------
+// exact fp64 helpers
+// ---------------------------------------------------------------------------
+
+// numpy np.remainder (npy_divmod): coords %= L (neighbor.py:84-86),
+// SimulationBox.wrap (system.py:41-46)
+__device__ __forceinline__ double np_remainder(double a, double b) {
+  double mod = fmod(a, b);
+  if (mod != 0.0) {
+    if ((b < 0.0) != (mod < 0.0)) mod = __dadd_rn(mod, b);
+  } else {
+    mod = copysign(0.0, b);
+  }
+  return mod;
+}
+
+// min_image on one axis (neighbor.py:36-43): d - L * rint(d / L).  d*invL
+// selects the same integer as the correctly rounded d/L except within a few
+// ulp of a half-integer; there the exact quotient is taken.
+__device__ __forceinline__ double min_image(double d, double L, double invL) {
+  double y = __dmul_rn(d, invL);
+  double q = rint(y);
+  if (0.5 - fabs(y - q) < 1e-9) q = rint(__ddiv_rn(d, L));
+  return __dsub_rn(d, __dmul_rn(L, q));
+}
+
+// displacement x_j - x_i with min image and r2 = (dx*dx + dy*dy) + dz*dz
+__device__ __forceinline__ double disp_r2(const double *xi, const double *xj, const Box &b,
+                                          double d[3]) {
+#pragma unroll
+  for (int ax = 0; ax < 3; ++ax) {
+    double v = __dsub_rn(xj[ax], xi[ax]);
+    d[ax] = b.per[ax] ? min_image(v, b.L[ax], b.invL[ax]) : v;
+  }
+  return __dadd_rn(__dadd_rn(__dmul_rn(d[0], d[0]), __dmul_rn(d[1], d[1])),
+                   __dmul_rn(d[2], d[2]));
+}
+
+__device__ __forceinline__ void load3(const double *__restrict__ p, int64_t i, double o[3]) {
+  o[0] = __ldg(p + 3 * i);
+  o[1] = __ldg(p + 3 * i + 1);
+  o[2] = __ldg(p + 3 * i + 2);
+}
+
+// ---------------------------------------------------------------------------
+// K1: cell binning (neighbor.py:54-96)
+// ---------------------------------------------------------------------------
+
+struct Grid {
+  int nc[3];
+  double origin[3], width[3];
+  Box box;
+};
+
+// per-axis min/max of positions for free axes (neighbor.py:71-76)
+__global__ void k_bounds(int64_t n, const double *__restrict__ pos,
+                         unsigned long long *__restrict__ out /* 6: min xyz, max xyz as ordered bits */) {
+  // order-preserving map of doubles to uint64 for atomicMin/Max
+  auto key = [](double v) {
+    unsigned long long u = __double_as_longlong(v);
+    return (u & 0x8000000000000000ull) ? ~u : (u | 0x8000000000000000ull);
+  };
+  unsigned long long mn[3] = {~0ull, ~0ull, ~0ull}, mx[3] = {0, 0, 0};
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+#pragma unroll
+    for (int ax = 0; ax < 3; ++ax) {
+      unsigned long long k = key(pos[3 * i + ax]);
+      mn[ax] = k < mn[ax] ? k : mn[ax];
+      mx[ax] = k > mx[ax] ? k : mx[ax];
+    }
+  }
+#pragma unroll
+  for (int ax = 0; ax < 3; ++ax) {
+    for (int o = 16; o > 0; o >>= 1) {
+      unsigned long long a = __shfl_down_sync(0xffffffffu, mn[ax], o);
+      unsigned long long b = __shfl_down_sync(0xffffffffu, mx[ax], o);
+      mn[ax] = a < mn[ax] ? a : mn[ax];
+      mx[ax] = b > mx[ax] ? b : mx[ax];
+    }
+    if ((threadIdx.x & 31) == 0) {
+      atomicMin(out + ax, mn[ax]);
+      atomicMax(out + 3 + ax, mx[ax]);
+    }
+  }
+}
+
+__device__ __forceinline__ void cell_coords(const double *p, const Grid &g, int c[3]) {
+#pragma unroll
+  for (int ax = 0; ax < 3; ++ax) {
+    double x = __dsub_rn(p[ax], g.origin[ax]);
+    if (g.box.per[ax]) x = np_remainder(x, g.box.L[ax]);
+    double f = floor(__ddiv_rn(x, g.width[ax]));
+    long long v = (long long)f;
+    v = v < 0 ? 0 : v;
+    v = v > g.nc[ax] - 1 ? g.nc[ax] - 1 : v;
+    c[ax] = (int)v;
+  }
+}
+
+__global__ void k_cell_index(int n, const double *__restrict__ pos, Grid g,
+                             int *__restrict__ atom_cell, int *__restrict__ cell_count) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double p[3];
+  load3(pos, i, p);
+  int c[3];
+  cell_coords(p, g, c);
+  int id = (c[0] * g.nc[1] + c[1]) * g.nc[2] + c[2];
+  atom_cell[i] = id;
+  atomicAdd(cell_count + id, 1);
+}
+
+__global__ void k_cell_fill(int n, const int *__restrict__ atom_cell, int *__restrict__ cursor,
+                            int *__restrict__ cell_atoms) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  int slot = atomicAdd(cursor + atom_cell[i], 1);
+  cell_atoms[slot] = i;
+}
+
+// ---------------------------------------------------------------------------
+// K2: full Verlet list at bc (neighbor.py:104-217)
+// ---------------------------------------------------------------------------
+
+// distinct stencil cells along one axis (wraparound de-dup, neighbor.py:121-135)
+__device__ __forceinline__ int stencil_axis(int c, int nc, int per, int out[3]) {
+  int k = 0;
+  for (int s = -1; s <= 1; ++s) {
+    int q = c + s;
+    if (per) {
+      q = ((q % nc) + nc) % nc;
+    } else if (q < 0 || q >= nc) {
+      continue;
+    }
+    bool dup = false;
+    for (int t = 0; t < k; ++t) dup |= out[t] == q;
+    if (!dup) out[k++] = q;
+  }
+  return k;
+}
+
+template <bool FILL>
+__global__ void k_nl_scan(int n, const double *__restrict__ pos, Grid g, double bc2,
+                          const int *__restrict__ atom_cell, const int *__restrict__ cell_start,
+                          const int *__restrict__ cell_atoms, int *__restrict__ row_count,
+                          const int *__restrict__ offsets, int *__restrict__ nbr,
+                          int *__restrict__ max_row) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double xi[3];
+  load3(pos, i, xi);
+  int id = atom_cell[i];
+  int c[3] = {id / (g.nc[1] * g.nc[2]), (id / g.nc[2]) % g.nc[1], id % g.nc[2]};
+  int sx[3], sy[3], sz[3];
+  int nx = stencil_axis(c[0], g.nc[0], g.box.per[0], sx);
+  int ny = stencil_axis(c[1], g.nc[1], g.box.per[1], sy);
+  int nz = stencil_axis(c[2], g.nc[2], g.box.per[2], sz);
+  int cnt = 0;
+  int base = FILL ? offsets[i] : 0;
+  for (int a = 0; a < nx; ++a)
+    for (int b = 0; b < ny; ++b)
+      for (int q = 0; q < nz; ++q) {
+        int cid = (sx[a] * g.nc[1] + sy[b]) * g.nc[2] + sz[q];
+        int s1 = cell_start[cid + 1];
+        for (int s = cell_start[cid]; s < s1; ++s) {
+          int j = cell_atoms[s];
+          if (j == i) continue;
+          double xj[3], d[3];
+          load3(pos, j, xj);
+          double r2 = disp_r2(xi, xj, g.box, d);
+          if (r2 < bc2) {
+            if (FILL) nbr[base + cnt] = j;
+            cnt++;
+          }
+        }
+      }
+  if (FILL) {
+    // rows ascending by j (neighbor.py:210-212); rows are short
+    int *row = nbr + base;
+    for (int u = 1; u < cnt; ++u) {
+      int v = row[u];
+      int w = u - 1;
+      while (w >= 0 && row[w] > v) {
+        row[w + 1] = row[w];
+        --w;
+      }
+      row[w + 1] = v;
+    }
+  } else {
+    row_count[i] = cnt;
+    atomicMax(max_row, cnt);
+  }
+}
+
+// rev[e] = index of (j -> i) in row j for entry e = (i -> j): drives the
+// deterministic gather of per-entry forces.
+__global__ void k_nl_reverse(int n, const int *__restrict__ offsets, const int *__restrict__ nbr,
+                             int *__restrict__ rev) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  for (int e = offsets[i]; e < offsets[i + 1]; ++e) {
+    int j = nbr[e];
+    int lo = offsets[j], hi = offsets[j + 1];
+    while (lo < hi) {
+      int mid = (lo + hi) >> 1;
+      if (nbr[mid] < i) lo = mid + 1;
+      else hi = mid;
+    }
+    rev[e] = lo;
+  }
+}
+
+__global__ void k_export_i64(int m, const int *__restrict__ in, int64_t *__restrict__ out) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < m) out[i] = in[i];
+}
+
+// ---------------------------------------------------------------------------
+// K3: skin/2 trigger (neighbor.py:220-229)
+// ---------------------------------------------------------------------------
+
+__global__ void k_max_drift(int n, const double *__restrict__ pos, const double *__restrict__ ref,
+                            Box box, unsigned long long *__restrict__ out) {
+  unsigned long long best = 0;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    double a[3], b[3], d[3];
+    load3(ref, i, a);
+    load3(pos, i, b);
+    double r2 = disp_r2(a, b, box, d);
+    unsigned long long k = __double_as_longlong(r2);  // r2 >= 0: bits are ordered
+    best = k > best ? k : best;
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    unsigned long long v = __shfl_down_sync(0xffffffffu, best, o);
+    best = v > best ? v : best;
+  }
+  if ((threadIdx.x & 31) == 0) atomicMax(out, best);
+}
+
+// ---------------------------------------------------------------------------
+// block helpers
+// ---------------------------------------------------------------------------
+
+// exclusive scan of one int per thread across the NT-thread block
+__device__ __forceinline__ int block_excl_scan(int v, int *s_w, int &total) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  int x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    int y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) s_w[w] = x;
+  __syncthreads();
+  int off = 0, tot = 0;
+#pragma unroll
+  for (int q = 0; q < NW; ++q) {
+    int s = s_w[q];
+    off += q < w ? s : 0;
+    tot += s;
+  }
+  __syncthreads();
+  total = tot;
+  return off + x - v;
+}
+
+template <class V>
+__device__ __forceinline__ V warp_sum(V v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// ---------------------------------------------------------------------------
+// K4/K5: the Tersoff evaluation
+// ---------------------------------------------------------------------------
+
+struct KArgs {
+  int n;
+  int atoms_per_block;
+  double rc2;                     // global packing cutoff^2 (neighbor.py:344)
+  Box box;
+  const double *__restrict__ pos;
+  const int *__restrict__ species;
+  const int *__restrict__ off;    // skin list CSR
+  const int *__restrict__ nbr;
+  double *__restrict__ forces;    // ATOMIC: (n,3) zero-initialised accumulators
+  double *__restrict__ fbuf;      // GATHER: per skin-list entry force (3 doubles)
+  double *__restrict__ fself;     // GATHER: per-atom self force
+  double *__restrict__ per_atom;  // may be null
+  double *__restrict__ partials;  // per block: [E, W xx yy zz xy xz yz, pad]
+  unsigned long long *__restrict__ stats;  // TB_NSTATS counters
+  ErrFlags *__restrict__ err;
+};
+
+template <class T, int S>
+struct SmemLayout {
+  // byte offsets inside dynamic shared memory for a block with C slots
+  static __host__ __device__ size_t bytes(int C) {
+    size_t b = 0;
+    b += sizeof(Tables<T, S>);              // tables (S > 1 path reads them here)
+    b = (b + 15) & ~size_t(15);
+    b += sizeof(double) * 3 * C;            // s_f
+    b += sizeof(T) * (4 + 2 * S + 3) * C;   // ex ey ez r, fc[S], dfc[S], dz, v, dvdr
+    b += sizeof(int) * 2 * C;               // j, entry
+    b += sizeof(short) * C;                 // local atom
+    b += sizeof(unsigned char) * C;         // species of j
+    b = (b + 15) & ~size_t(15);
+    b += sizeof(double) * 3 * NT;           // tile positions
+    b += sizeof(int) * (4 * NT + 2 + 8);    // si, roff, cnt, soff, warp scratch
+    return b + 64;
+  }
+};
+
+template <class T, int S, bool LAM3, int MODE>
+__global__ void __launch_bounds__(NT, 3)
+    k_tersoff(const KArgs a, const __grid_constant__ Tables<T, S> gtab, int C) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  // ---- carve shared memory (see SmemLayout) ----
+  unsigned char *p = smem;
+  Tables<T, S> *s_tab = reinterpret_cast<Tables<T, S> *>(p);
+  p += (sizeof(Tables<T, S>) + 15) & ~size_t(15);
+  double *s_fx = reinterpret_cast<double *>(p); p += sizeof(double) * C;
+  double *s_fy = reinterpret_cast<double *>(p); p += sizeof(double) * C;
+  double *s_fz = reinterpret_cast<double *>(p); p += sizeof(double) * C;
+  T *s_ex = reinterpret_cast<T *>(p); p += sizeof(T) * C;
+  T *s_ey = reinterpret_cast<T *>(p); p += sizeof(T) * C;
+  T *s_ez = reinterpret_cast<T *>(p); p += sizeof(T) * C;
+  T *s_r = reinterpret_cast<T *>(p); p += sizeof(T) * C;
+  T *s_fc = reinterpret_cast<T *>(p); p += sizeof(T) * S * C;   // [S][C]
+  T *s_dfc = reinterpret_cast<T *>(p); p += sizeof(T) * S * C;  // [S][C]
+  T *s_dz = reinterpret_cast<T *>(p); p += sizeof(T) * C;
+  T *s_v = reinterpret_cast<T *>(p); p += sizeof(T) * C;
+  T *s_dvdr = reinterpret_cast<T *>(p); p += sizeof(T) * C;
+  int *s_j = reinterpret_cast<int *>(p); p += sizeof(int) * C;
+  int *s_ent = reinterpret_cast<int *>(p); p += sizeof(int) * C;
+  short *s_atom = reinterpret_cast<short *>(p); p += sizeof(short) * C;
+  unsigned char *s_sp = p; p += C;
+  p = smem + ((p - smem + 15) & ~size_t(15));
+  double *s_xi = reinterpret_cast<double *>(p); p += sizeof(double) * 3 * NT;
+  int *s_si = reinterpret_cast<int *>(p); p += sizeof(int) * NT;
+  int *s_roff = reinterpret_cast<int *>(p); p += sizeof(int) * (NT + 1);
+  int *s_cnt = reinterpret_cast<int *>(p); p += sizeof(int) * NT;
+  int *s_soff = reinterpret_cast<int *>(p); p += sizeof(int) * (NT + 1);
+  int *s_w = reinterpret_cast<int *>(p); p += sizeof(int) * 8;
+
+  const int tid = threadIdx.x;
+  const int lane = tid & 31, wid = tid >> 5;
+  const int atom0 = blockIdx.x * a.atoms_per_block;
+  const int na = min(a.atoms_per_block, a.n - atom0);
+
+  const Tables<T, S> &tab = (S > 1) ? *s_tab : gtab;
+  if (S > 1) {
+    // species-indexed tables are read with divergent indices: stage in smem
+    const int *src = reinterpret_cast<const int *>(&gtab);
+    int *dst = reinterpret_cast<int *>(s_tab);
+    for (int q = tid; q < (int)(sizeof(Tables<T, S>) / sizeof(int)); q += NT) dst[q] = src[q];
+  }
+
+  // ---- phase 0a: tile atoms ----
+  for (int t = tid; t <= na; t += NT) s_roff[t] = a.off[atom0 + t];
+  if (tid < na) {
+    int i = atom0 + tid;
+    double x[3];
+    load3(a.pos, i, x);
+    s_xi[3 * tid] = x[0];
+    s_xi[3 * tid + 1] = x[1];
+    s_xi[3 * tid + 2] = x[2];
+    if (!(isfinite(x[0]) && isfinite(x[1]) && isfinite(x[2]))) atomicMin(&a.err->nonfinite_atom, i);
+    int si = a.species[i];
+    if (si < 0 || si >= S) {
+      atomicMin(&a.err->bad_species_atom, i);
+      si = 0;
+    }
+    s_si[tid] = si;
+    s_cnt[tid] = 0;
+  }
+  __syncthreads();
+
+  // ---- phase 0b: pack -- re-filter the skin list at current positions
+  //      (pack_adjacency, neighbor.py:330-360), order-preserving compaction ----
+  const int e0 = s_roff[0];
+  const int ne = s_roff[na] - e0;
+  if (ne > C) {
+    if (tid == 0) atomicExch(&a.err->overflow, 1);
+    return;
+  }
+  int nlive = 0;
+  for (int base = 0; base < ne; base += NT) {
+    int e = base + tid;
+    bool live = false;
+    int la = 0, j = 0;
+    double d[3] = {0, 0, 0}, r2 = 0;
+    if (e < ne) {
+      // owning tile atom: last la with s_roff[la] <= e0 + e
+      int lo = 0, hi = na;  // invariant s_roff[lo] <= e0+e < s_roff[hi]
+      while (hi - lo > 1) {
+        int mid = (lo + hi) >> 1;
+        if (s_roff[mid] <= e0 + e) lo = mid;
+        else hi = mid;
+      }
+      la = lo;
+      j = a.nbr[e0 + e];
+      double xj[3];
+      load3(a.pos, j, xj);
+      r2 = disp_r2(&s_xi[3 * la], xj, a.box, d);
+      live = r2 < a.rc2;
+      if (MODE == 1 && !live) {
+        double *fb = a.fbuf + 3 * (int64_t)(e0 + e);
+        fb[0] = 0.0;
+        fb[1] = 0.0;
+        fb[2] = 0.0;
+      }
+    }
+    unsigned bal = __ballot_sync(0xffffffffu, live);
+    if (lane == 0) s_w[wid] = __popc(bal);
+    __syncthreads();
+    int woff = 0, tot = 0;
+#pragma unroll
+    for (int q = 0; q < NW; ++q) {
+      woff += q < wid ? s_w[q] : 0;
+      tot += s_w[q];
+    }
+    if (live) {
+      int slot = nlive + woff + __popc(bal & ((1u << lane) - 1u));
+      double r = sqrt(r2);
+      double inv = 1.0 / r;
+      s_ex[slot] = (T)(d[0] * inv);
+      s_ey[slot] = (T)(d[1] * inv);
+      s_ez[slot] = (T)(d[2] * inv);
+      s_r[slot] = (T)r;
+      s_j[slot] = j;
+      s_ent[slot] = e0 + e;
+      s_atom[slot] = (short)la;
+      int sj = a.species[j];
+      sj = (sj < 0 || sj >= S) ? 0 : sj;
+      s_sp[slot] = (unsigned char)sj;
+      const int si = s_si[la];
+#pragma unroll
+      for (int q = 0; q < S; ++q) {  // f_C(r) of this slot acting as k in (i, q, slot)
+        T fc, dfc;
+        cutoff((T)r, tab.trip[(si * S + q) * S + sj], fc, dfc);
+        s_fc[q * C + slot] = fc;
+        s_dfc[q * C + slot] = dfc;
+      }
+      atomicAdd(&s_cnt[la], 1);
+      if (r2 < 1e-16) {
+        unsigned long long key =
+            ((unsigned long long)(__double_as_longlong(r2) >> 32) << 32) | (unsigned)(e0 + e);
+        atomicMin(&a.err->coinc_key, key);
+      }
+    }
+    nlive += tot;
+    __syncthreads();
+  }
+
+  // per-atom slot ranges and the zeta_visits counter (sum n_i^2, kernels.py:537-544)
+  {
+    int c = tid < na ? s_cnt[tid] : 0;
+    int tot;
+    int ex = block_excl_scan(c, s_w, tot);
+    if (tid < na) s_soff[tid] = ex;
+    if (tid == 0) s_soff[na] = tot;
+    unsigned long long sq = (unsigned long long)c * (unsigned long long)c;
+    sq = warp_sum(sq);
+    if (lane == 0 && sq) atomicAdd(&a.stats[0], sq);
+    unsigned long long pk = warp_sum((unsigned long long)c);
+    if (lane == 0 && pk) atomicAdd(&a.stats[1], pk);
+  }
+  __syncthreads();
+
+  // ---- phase 1: zeta_ij, then the pair part (V, dV/dr, delta_zeta) ----
+  unsigned long long live_pairs = 0, live_trips = 0, taper_pairs = 0, taper_trips = 0;
+  for (int s = tid; s < nlive; s += NT) {
+    const int la = s_atom[s];
+    const int si = s_si[la];
+    const int sa = s_sp[s];
+    const int b0 = s_soff[la], b1 = s_soff[la + 1];
+    const T ra = s_r[s];
+    const PairP<T> &pp = tab.pair[si * S + sa];
+    T v = T(0), dvdr = T(0), dz = T(0);
+    if (ra < pp.Rp) {
+      live_pairs++;
+      taper_pairs += ra > pp.Rm;
+      const T eax = s_ex[s], eay = s_ey[s], eaz = s_ez[s];
+      T zeta = T(0);
+      for (int b = b0; b < b1; ++b) {
+        if (b == s) continue;
+        const T fcb = s_fc[sa * C + b];
+        if (fcb == T(0)) continue;
+        live_trips++;
+        taper_trips += fcb != T(1);
+        const int sb = s_sp[b];
+        const TripP<T> &tp = tab.trip[(si * S + sa) * S + sb];
+        T cost = eax * s_ex[b] + eay * s_ey[b] + eaz * s_ez[b];
+        cost = fmin(T(1), fmax(T(-1), cost));
+        T g, dg;
+        angular(cost, tp, g, dg);
+        T term = fcb * g;
+        if (LAM3) {
+          T ex, darg;
+          lam3_term(ra - s_r[b], tp, ex, darg);
+          term *= ex;
+        }
+        zeta += term;
+      }
+      pair_part(ra, zeta, pp, v, dvdr, dz);
+    }
+    s_dz[s] = dz;
+    s_v[s] = v;
+    s_dvdr[s] = dvdr;
+  }
+  {
+    unsigned long long lp = warp_sum(live_pairs), lt = warp_sum(live_trips);
+    unsigned long long tp = warp_sum(taper_pairs), tt = warp_sum(taper_trips);
+    if (lane == 0 && (lp | lt)) {
+      atomicAdd(&a.stats[2], lp);
+      atomicAdd(&a.stats[3], lt);
+      atomicAdd(&a.stats[4], tp);
+      atomicAdd(&a.stats[5], tt);
+    }
+  }
+  __syncthreads();
+
+  // ---- phase 2: total force on each neighbour slot from the energy terms
+  //      centred on its atom i.  Lane a gathers every dzeta-weighted gradient
+  //      that lands on a:  (i,a,b) with a as j and (i,b,a) with a as k,
+  //      both along e_a and w_ab = (e_b - cos e_a)/r_a. ----
+  double wxx = 0, wyy = 0, wzz = 0, wxy = 0, wxz = 0, wyz = 0;
+  for (int s = tid; s < nlive; s += NT) {
+    const int la = s_atom[s];
+    const int si = s_si[la];
+    const int sa = s_sp[s];
+    const int b0 = s_soff[la], b1 = s_soff[la + 1];
+    const T ra = s_r[s];
+    const T inva = T(1) / ra;
+    const T eax = s_ex[s], eay = s_ey[s], eaz = s_ez[s];
+    const T dza = s_dz[s];
+    T Salpha = T(0), Sc = T(0), Sbx = T(0), Sby = T(0), Sbz = T(0);
+    for (int b = b0; b < b1; ++b) {
+      if (b == s) continue;
+      const T dzb = s_dz[b];
+      const int sb = s_sp[b];
+      const T fcb = s_fc[sa * C + b];   // f_C(r_b) in (i,a,b)
+      const T fca = s_fc[sb * C + s];   // f_C(r_a) in (i,b,a)
+      const bool t1 = (dza != T(0)) && (fcb != T(0));
+      const bool t2 = (dzb != T(0)) && (fca != T(0));
+      if (!(t1 || t2)) continue;
+      const T ebx = s_ex[b], eby = s_ey[b], ebz = s_ez[b];
+      T cost = eax * ebx + eay * eby + eaz * ebz;
+      cost = fmin(T(1), fmax(T(-1), cost));
+      T alpha, beta;
+      if (S == 1 && !LAM3) {
+        const TripP<T> &tp = tab.trip[0];
+        T g, dg;
+        angular(cost, tp, g, dg);
+        const T dfca = s_dfc[s];
+        alpha = dzb * (dfca * g);
+        beta = dg * (dza * fcb + dzb * fca);
+      } else {
+        alpha = T(0);
+        beta = T(0);
+        if (t1) {
+          const TripP<T> &tp = tab.trip[(si * S + sa) * S + sb];
+          T g, dg, ex = T(1), darg = T(0);
+          angular(cost, tp, g, dg);
+          if (LAM3) lam3_term(ra - s_r[b], tp, ex, darg);
+          const T val = fcb * g * ex;
+          alpha += dza * (val * darg);
+          beta += dza * (fcb * dg * ex);
+        }
+        if (t2) {
+          const TripP<T> &tp = tab.trip[(si * S + sb) * S + sa];
+          T g, dg, ex = T(1), darg = T(0);
+          angular(cost, tp, g, dg);
+          if (LAM3) lam3_term(s_r[b] - ra, tp, ex, darg);
+          const T dfca = s_dfc[sb * C + s];
+          const T val = fca * g * ex;
+          alpha += dzb * (dfca * g * ex - val * darg);
+          beta += dzb * (fca * dg * ex);
+        }
+      }
+      Salpha += alpha;
+      Sc += beta * cost;
+      Sbx += beta * ebx;
+      Sby += beta * eby;
+      Sbz += beta * ebz;
+    }
+    // force on a: pair part -dV/dr e_a (kernels.py:300-308) and the zeta part
+    const T ca = s_dvdr[s] + Salpha - Sc * inva;
+    const double fx = -(double)(ca * eax + inva * Sbx);
+    const double fy = -(double)(ca * eay + inva * Sby);
+    const double fz = -(double)(ca * eaz + inva * Sbz);
+    s_fx[s] = fx;
+    s_fy[s] = fy;
+    s_fz[s] = fz;
+    // virial (x_a - x_i) (x) f_a   [derived; not in the reference]
+    const double dxa = (double)ra * (double)eax, dya = (double)ra * (double)eay,
+                 dza_ = (double)ra * (double)eaz;
+    wxx += dxa * fx;
+    wyy += dya * fy;
+    wzz += dza_ * fz;
+    wxy += dxa * fy;
+    wxz += dxa * fz;
+    wyz += dya * fz;
+    const int j = s_j[s];
+    if (MODE == 0) {
+      atomicAdd(a.forces + 3 * (int64_t)j, fx);
+      atomicAdd(a.forces + 3 * (int64_t)j + 1, fy);
+      atomicAdd(a.forces + 3 * (int64_t)j + 2, fz);
+    } else {
+      double *fb = a.fbuf + 3 * (int64_t)s_ent[s];
+      fb[0] = fx;
+      fb[1] = fy;
+      fb[2] = fz;
+    }
+  }
+  __syncthreads();
+
+  // ---- phase 3: per-atom self force (translation invariance: F_i from the
+  //      terms centred on i is minus the sum over its neighbours) and e_i ----
+  double ebl = 0.0;
+  if (tid < na) {
+    const int i = atom0 + tid;
+    double fx = 0.0, fy = 0.0, fz = 0.0, ei = 0.0;
+    for (int s = s_soff[tid]; s < s_soff[tid + 1]; ++s) {
+      fx -= s_fx[s];
+      fy -= s_fy[s];
+      fz -= s_fz[s];
+      ei += (double)s_v[s];
+    }
+    ebl = ei;
+    if (a.per_atom) a.per_atom[i] = ei + 0.0;
+    if (MODE == 0) {
+      atomicAdd(a.forces + 3 * (int64_t)i, fx);
+      atomicAdd(a.forces + 3 * (int64_t)i + 1, fy);
+      atomicAdd(a.forces + 3 * (int64_t)i + 2, fz);
+    } else {
+      a.fself[3 * (int64_t)i] = fx;
+      a.fself[3 * (int64_t)i + 1] = fy;
+      a.fself[3 * (int64_t)i + 2] = fz;
+    }
+  }
+  // ---- block partials: energy (atom order) and virial ----
+  double vals[7] = {ebl, wxx, wyy, wzz, wxy, wxz, wyz};
+  __shared__ double s_red[NW][7];
+#pragma unroll
+  for (int q = 0; q < 7; ++q) {
+    double v = warp_sum(vals[q]);
+    if (lane == 0) s_red[wid][q] = v;
+  }
+  __syncthreads();
+  if (tid < 7) {
+    double v = 0.0;
+#pragma unroll
+    for (int w = 0; w < NW; ++w) v += s_red[w][tid];
+    a.partials[8 * (int64_t)blockIdx.x + tid] = v;
+  }
+}
+
+// deterministic final reduction of block partials -> result[7]
+__global__ void k_reduce_partials(int nblocks, const double *__restrict__ partials,
+                                  double *__restrict__ result) {
+  __shared__ double s[256][7];
+  double acc[7] = {0, 0, 0, 0, 0, 0, 0};
+  for (int b = threadIdx.x; b < nblocks; b += 256)
+#pragma unroll
+    for (int q = 0; q < 7; ++q) acc[q] += partials[8 * (int64_t)b + q];
+#pragma unroll
+  for (int q = 0; q < 7; ++q) s[threadIdx.x][q] = acc[q];
+  __syncthreads();
+  for (int h = 128; h > 0; h >>= 1) {
+    if (threadIdx.x < h)
+#pragma unroll
+      for (int q = 0; q < 7; ++q) s[threadIdx.x][q] += s[threadIdx.x + h][q];
+    __syncthreads();
+  }
+  if (threadIdx.x < 7) result[threadIdx.x] = s[0][threadIdx.x] + 0.0;
+}
+
+// deterministic gather: F_m = self_m + sum over entries (m->i) of fbuf[rev]
+__global__ void k_force_gather(int n, const int *__restrict__ off, const int *__restrict__ rev,
+                               const double *__restrict__ fbuf, const double *__restrict__ fself,
+                               double *__restrict__ forces) {
+  int m = blockIdx.x * blockDim.x + threadIdx.x;
+  if (m >= n) return;
+  double fx = fself[3 * (int64_t)m], fy = fself[3 * (int64_t)m + 1], fz = fself[3 * (int64_t)m + 2];
+  for (int e = off[m]; e < off[m + 1]; ++e) {
+    const double *f = fbuf + 3 * (int64_t)__ldg(rev + e);
+    fx += f[0];
+    fy += f[1];
+    fz += f[2];
+  }
+  forces[3 * (int64_t)m] = fx + 0.0;
+  forces[3 * (int64_t)m + 1] = fy + 0.0;
+  forces[3 * (int64_t)m + 2] = fz + 0.0;
+}
+
+// ---------------------------------------------------------------------------
+// K8: velocity Verlet pieces (system.py:355-380)
+// ---------------------------------------------------------------------------
+
+// v += half F / m ; x += dt v ; wrap periodic axes with np.remainder
+__global__ void k_kick_drift(int n, double *__restrict__ pos, double *__restrict__ vel,
+                             const double *__restrict__ f, const double *__restrict__ mass,
+                             double half, double dt, Box box) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double m = mass[i];
+#pragma unroll
+  for (int ax = 0; ax < 3; ++ax) {
+    int64_t k = 3 * (int64_t)i + ax;
+    double v = __dadd_rn(vel[k], __ddiv_rn(__dmul_rn(half, f[k]), m));
+    vel[k] = v;
+    double x = __dadd_rn(pos[k], __dmul_rn(dt, v));
+    if (box.per[ax]) x = np_remainder(x, box.L[ax]);
+    pos[k] = x;
+  }
+}
+
+__global__ void k_kick(int n, double *__restrict__ vel, const double *__restrict__ f,
+                       const double *__restrict__ mass, double half) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double m = mass[i];
+#pragma unroll
+  for (int ax = 0; ax < 3; ++ax) {
+    int64_t k = 3 * (int64_t)i + ax;
+    vel[k] = __dadd_rn(vel[k], __ddiv_rn(__dmul_rn(half, f[k]), m));
+  }
+}
+
+// ---------------------------------------------------------------------------
+// FMA-pipe peak probe (roofline denominator)
+// ---------------------------------------------------------------------------
+template <class T>
+__global__ void __launch_bounds__(256) k_fma_peak(T *out, int iters, T b, T c) {
+  T a0 = T(threadIdx.x) * T(1e-3), a1 = a0 + T(1), a2 = a0 + T(2), a3 = a0 + T(3);
+  T a4 = a0 + T(4), a5 = a0 + T(5), a6 = a0 + T(6), a7 = a0 + T(7);
+  for (int i = 0; i < iters; ++i) {
+    a0 = fma(a0, b, c); a1 = fma(a1, b, c); a2 = fma(a2, b, c); a3 = fma(a3, b, c);
+    a4 = fma(a4, b, c); a5 = fma(a5, b, c); a6 = fma(a6, b, c); a7 = fma(a7, b, c);
+  }
+  T s = ((a0 + a1) + (a2 + a3)) + ((a4 + a5) + (a6 + a7));
+  if (s == T(-12345)) out[blockIdx.x] = s;  // keep the chains alive
+}
+
+}  // namespace tb

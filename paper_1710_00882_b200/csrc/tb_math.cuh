@@ -1,0 +1,135 @@
+// tb_math.cuh -- Tersoff potential math as sm_100a device functions.
+//
+// Semantics follow reference pkg/src/tersoffmd/potential.py:167-290 and
+// pkg/docs/math_notes.md; the expression trees are re-derived for the GPU:
+//   * f_C taper via sincospi (potential.py:167-175; plateaus inclusive and exact)
+//   * g in the cancellation-free form gamma(1 + c^2 x^2 / (d^2 (d^2 + x^2)))
+//     (potential.py:190-199), written gamma + (gamma c^2/d^2) x^2 / den with one
+//     reciprocal of den shared by g and dg/dcos
+//   * bond order with 2 transcendental calls instead of the reference's 4 pow:
+//       u = (beta zeta)^eta = exp(eta log t),  b = exp(-log1p(u)/(2 eta)),
+//       db/dzeta = -beta/2 * (u/t) * (b/(1+u))          (potential.py:202-215)
+//     and the ZETA_TINY guard: zeta < 1e-30 => db = 0 (b still evaluated).
+#pragma once
+#include <cuda_runtime.h>
+#include <math.h>
+
+namespace tb {
+
+constexpr int SMAX = 4;
+constexpr double ZETA_TINY = 1e-30;
+
+// Per-entry constants derived on the host from the flattened tables (see
+// tb_api.cu make_tables); T = double for fp64, float for the mixed mode.
+template <class T>
+struct TripP {
+  T Rm, Rp, R, halfInvD, nqpInvD;  // plateau bounds, taper scale, -pi/(4D)
+  T gamma, gc2d2, m2gc2, d2, h;   // g(cos) constants
+  T lam3, lam3x3;                 // exp((lam3 (rij-rik))^m) term
+  int m;
+  int pad;
+};
+
+template <class T>
+struct PairP {
+  T Rm, Rp, R, halfInvD, nqpInvD;
+  T A, lam1, B, lam2;
+  T beta, eta, neg_half_inv_eta, neg_half_beta;
+};
+
+template <class T, int S>
+struct Tables {
+  PairP<T> pair[S * S];
+  TripP<T> trip[S * S * S];
+};
+
+// ---- transcendental wrappers (overloads keep the templates readable) ----
+__device__ __forceinline__ double t_exp(double x) { return exp(x); }
+__device__ __forceinline__ float t_exp(float x) { return expf(x); }
+__device__ __forceinline__ double t_log(double x) { return log(x); }
+__device__ __forceinline__ float t_log(float x) { return logf(x); }
+__device__ __forceinline__ double t_log1p(double x) { return log1p(x); }
+__device__ __forceinline__ float t_log1p(float x) { return log1pf(x); }
+__device__ __forceinline__ void t_sincospi(double x, double *s, double *c) { sincospi(x, s, c); }
+__device__ __forceinline__ void t_sincospi(float x, float *s, float *c) { sincospif(x, s, c); }
+__device__ __forceinline__ double t_rcp(double x) { return 1.0 / x; }
+__device__ __forceinline__ float t_rcp(float x) { return __frcp_rn(x); }
+
+// f_C and dF_C/dr with inclusive exact plateaus (potential.py:167-175).
+// Returns false when r >= R + D (exactly zero contribution).
+template <class T, class P>
+__device__ __forceinline__ bool cutoff(T r, const P &p, T &fc, T &dfc) {
+  if (r <= p.Rm) {
+    fc = T(1);
+    dfc = T(0);
+    return true;
+  }
+  if (r >= p.Rp) {
+    fc = T(0);
+    dfc = T(0);
+    return false;
+  }
+  T s, c;
+  t_sincospi((r - p.R) * p.halfInvD, &s, &c);  // sin/cos(pi/2 (r-R)/D)
+  fc = T(0.5) - T(0.5) * s;
+  dfc = p.nqpInvD * c;
+  return true;
+}
+
+// g(cos) and dg/dcos (potential.py:190-199), cancellation-free.
+template <class T>
+__device__ __forceinline__ void angular(T cost, const TripP<T> &p, T &g, T &dg) {
+  T x = p.h - cost;
+  T x2 = x * x;
+  T inv = t_rcp(p.d2 + x2);
+  g = p.gamma + p.gc2d2 * (x2 * inv);
+  dg = (p.m2gc2 * x) * (inv * inv);
+}
+
+// exp((lam3 t)^m) with t = rij - rik and its derivative factor wrt t.
+template <class T>
+__device__ __forceinline__ void lam3_term(T dr, const TripP<T> &p, T &ex, T &darg) {
+  T t = p.lam3 * dr;
+  if (p.m == 3) {
+    ex = t_exp(t * t * t);
+    darg = p.lam3x3 * (t * t);
+  } else {
+    ex = t_exp(t);
+    darg = p.lam3;
+  }
+}
+
+// Pair part of one ordered (i,j) bond at fixed zeta (potential.py:280-290):
+// returns V, dV/dr and delta_zeta = f_C f_A db/dzeta.
+template <class T>
+__device__ __forceinline__ void pair_part(T r, T zeta, const PairP<T> &p, T &v, T &dvdr,
+                                          T &dzeta) {
+  T fc, dfc;
+  if (!cutoff(r, p, fc, dfc)) {
+    v = T(0);
+    dvdr = T(0);
+    dzeta = T(0);
+    return;
+  }
+  T fr = p.A * t_exp(-p.lam1 * r);
+  T fa = -p.B * t_exp(-p.lam2 * r);
+  T t = p.beta * zeta;
+  T b, db;
+  if (zeta < T(ZETA_TINY)) {
+    // (beta zeta)^eta with zeta ~ 0; exact b = 1 at zeta == 0
+    T u = zeta > T(0) ? t_exp(p.eta * t_log(t)) : T(0);
+    b = t_exp(p.neg_half_inv_eta * t_log1p(u));
+    db = T(0);
+  } else {
+    T u = t_exp(p.eta * t_log(t));
+    T opu = T(1) + u;
+    b = t_exp(p.neg_half_inv_eta * t_log1p(u));
+    db = p.neg_half_beta * (u / t) * (b / opu);
+  }
+  T inner = fr + b * fa;
+  v = fc * inner;
+  dvdr = dfc * inner + fc * (-p.lam1 * fr + b * (-p.lam2 * fa));
+  dzeta = fc * fa * db;
+}
+
+}  // namespace tb

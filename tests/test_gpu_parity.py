@@ -1,0 +1,187 @@
+"""GPU parity: the sm_100a path against the reference (golden vectors) and the
+CPU oracle on the same seeded inputs.
+
+Bars (BASELINE north_star): neighbour lists bit-exact; fp64 energy/forces
+within 1e-10 relative (energy: |dE|/|E|; forces: max|dF| / max|F|); mixed
+precision max|dF| <= 1e-5 max|F|.
+"""
+
+import numpy as np
+import pytest
+
+import paper_1710_00882_b200 as B
+from conftest import Frame, golden_clusters, golden_frame, load_golden
+from paper_1710_00882_b200 import structures
+from paper_1710_00882_b200.paramfile import builtin_params, parse_params
+
+pytestmark = pytest.mark.gpu
+
+FP64_TOL = 1e-10
+MIXED_TOL = 1e-5
+SCATTERS = ["atomic", "gather"]
+
+
+def rel_f(a, b):
+    return np.abs(np.asarray(a) - np.asarray(b)).max() / max(np.abs(b).max(), 1e-300)
+
+
+def gpu_eval(fr, table, precision="double", scatter="atomic", skin=0.3):
+    nl = B.build_neighbor_list(fr, table.r_cut, skin)
+    return nl, B.compute(fr, nl, table, B.make_variant("B200", precision=precision,
+                                                       scatter=scatter))
+
+
+@pytest.mark.parametrize("name", ["dimer", "si512", "sic216", "disordered"])
+def test_neighbor_list_bit_exact_vs_reference(name):
+    g = load_golden(name)
+    t = parse_params(str(g["table"]))
+    nl = B.build_neighbor_list(golden_frame(g), t.r_cut, 0.3)
+    assert np.array_equal(nl.offsets, g["offsets"])
+    assert np.array_equal(nl.neighbors, g["neighbors"])
+
+
+@pytest.mark.parametrize("frame", [0, 1, 2])
+def test_neighbor_list_edge_frames(frame):
+    g = load_golden("nl_frames")
+    p = f"f{frame}_"
+    fr = Frame(g[p + "positions"], (9.0, 9.0, 9.0), g[p + "periodic"])
+    nl = B.build_neighbor_list(fr, 2.1, 0.3)
+    assert np.array_equal(nl.offsets, g[p + "offsets"])
+    assert np.array_equal(nl.neighbors, g[p + "neighbors"])
+
+
+@pytest.mark.parametrize("scatter", SCATTERS)
+@pytest.mark.parametrize("name", ["dimer", "si512", "sic216", "disordered"])
+def test_fp64_matches_reference(name, scatter):
+    g = load_golden(name)
+    t = parse_params(str(g["table"]))
+    _, r = gpu_eval(golden_frame(g), t, "double", scatter)
+    e = float(g["energy"])
+    assert abs(r.potential_energy - e) <= FP64_TOL * abs(e)
+    assert rel_f(r.forces, g["forces"]) <= FP64_TOL
+    assert np.abs(r.per_atom_energy - g["per_atom"]).max() <= FP64_TOL * np.abs(g["per_atom"]).max()
+    assert r.stats["zeta_visits"] == int(g["zeta_visits"])
+
+
+@pytest.mark.parametrize("name", ["si512", "sic216", "disordered"])
+def test_mixed_matches_reference_fp64(name):
+    g = load_golden(name)
+    t = parse_params(str(g["table"]))
+    _, r = gpu_eval(golden_frame(g), t, "single")
+    assert rel_f(r.forces, g["forces"]) <= MIXED_TOL
+    e = float(g["energy"])
+    assert abs(r.potential_energy - e) <= 1e-6 * abs(e)
+
+
+def test_dimer_frozen_goldens():
+    g = load_golden("dimer")
+    t = parse_params(str(g["table"]))
+    _, r = gpu_eval(golden_frame(g), t)
+    assert r.potential_energy == pytest.approx(float(g["frozen_energy"]), rel=5e-14)
+    assert r.forces[0, 0] == pytest.approx(float(g["frozen_f0x"]), rel=5e-13)
+    assert np.all(r.forces[:, 1:] == 0.0)
+
+
+def test_clusters_carbon_and_two_species():
+    # free clusters incl. the synthetic table with m=1 and lam3 != 0
+    for fr, table, row in golden_clusters():
+        for scatter in SCATTERS:
+            nl, r = gpu_eval(fr, table, "double", scatter)
+            assert np.array_equal(nl.neighbors, row["neighbors"])
+            e = float(row["energy"])
+            assert abs(r.potential_energy - e) <= FP64_TOL * abs(e)
+            assert rel_f(r.forces, row["forces"]) <= FP64_TOL
+            assert r.stats["zeta_visits"] == int(row["zeta_visits"])
+        _, rs = gpu_eval(fr, table, "single")
+        assert rel_f(rs.forces, row["forces"]) <= MIXED_TOL
+
+
+def test_virial_matches_oracle_and_strain_fd(oracle_mod):
+    g = load_golden("si512")
+    t = parse_params(str(g["table"]))
+    fr = golden_frame(g)
+    _, r = gpu_eval(fr, t)
+    o = oracle_mod.compute(fr.positions, fr.species, fr.box.lengths, fr.box.periodic,
+                           g["offsets"], g["neighbors"], t)
+    assert np.abs(r.virial - o["virial"]).max() <= 1e-10 * np.abs(o["virial"]).max()
+    assert np.allclose(r.virial[:3], g["virial_fd_diag"], rtol=1e-7, atol=1e-6)
+
+
+def _config(idx, small=True):
+    st, tname = structures.config(idx, small=small)
+    return st, builtin_params(tname)
+
+
+@pytest.mark.parametrize("idx", [1, 2, 3, 4, 5])
+@pytest.mark.parametrize("precision", ["double", "single"])
+def test_configs_vs_oracle(oracle_mod, idx, precision):
+    st, t = _config(idx)
+    nl, r = gpu_eval(st, t, precision)
+    off, nb = oracle_mod.build_neighbor_list(st.positions, st.box.lengths, st.box.periodic,
+                                             t.r_cut, 0.3, threads=8)
+    assert np.array_equal(nl.offsets, off) and np.array_equal(nl.neighbors, nb)
+    o = oracle_mod.compute(st.positions, st.species, st.box.lengths, st.box.periodic, off, nb, t,
+                           threads=8)
+    tol = FP64_TOL if precision == "double" else MIXED_TOL
+    assert rel_f(r.forces, o["forces"]) <= tol
+    assert abs(r.potential_energy - o["energy"]) <= (tol if precision == "double" else 1e-6) * abs(o["energy"])
+    assert r.stats["zeta_visits"] == o["zeta_visits"]
+    if precision == "double":
+        assert np.abs(r.virial - o["virial"]).max() <= 1e-9 * np.abs(o["virial"]).max()
+
+
+def test_total_force_vanishes_and_gather_deterministic():
+    st, t = _config(4)
+    nl = B.build_neighbor_list(st, t.r_cut, 0.3)
+    v = B.make_variant("B200", scatter="gather")
+    a = B.compute(st, nl, t, v)
+    b = B.compute(st, nl, t, v)
+    assert a.forces.tobytes() == b.forces.tobytes()
+    assert a.potential_energy == b.potential_energy
+    assert np.abs(a.forces.sum(axis=0)).max() < 1e-12 * st.natoms * max(1, np.abs(a.forces).max())
+
+
+def test_errors_map_to_reference_exceptions():
+    t = builtin_params("C")
+    fr = Frame([[0.0, 0, 0], [1.5, 0, 0]], (10, 10, 10), (False,) * 3)
+    nl = B.build_neighbor_list(fr, t.r_cut, 0.3)
+    fr.positions[1, 0] = np.nan
+    with pytest.raises(B.InputError, match="non-finite"):
+        B.compute(fr, nl, t)
+    fr.positions[1, 0] = 1.5
+    fr.species = np.array([0, 1])
+    with pytest.raises(B.ConfigurationError, match="species index"):
+        B.compute(fr, nl, t)
+    fr2 = Frame([[0.0, 0, 0], [1e-9, 0, 0]], (10, 10, 10), (False,) * 3)
+    nl2 = B.build_neighbor_list(fr2, t.r_cut, 0.3)
+    with pytest.raises(B.InputError, match="coincident"):
+        B.compute(fr2, nl2, t)
+    with pytest.raises(B.ConfigurationError, match="skin"):
+        B.build_neighbor_list(fr2, t.r_cut, -0.1)
+    box = Frame([[0.5, 1.0, 1.0], [2.0, 1.0, 1.0]], (4.0, 9.0, 9.0), (True, True, True))
+    with pytest.raises(B.ConfigurationError, match="twice the build cutoff"):
+        B.build_neighbor_list(box, 2.1, 0.3)
+
+
+def test_lone_and_distant_atoms():
+    t = builtin_params("C")
+    for pos in ([[0.0, 0, 0]], [[0.0, 0, 0], [5.0, 0, 0]]):
+        fr = Frame(pos, (20, 20, 20), (False,) * 3)
+        _, r = gpu_eval(fr, t)
+        assert r.potential_energy == 0.0
+        assert np.all(r.forces == 0.0)
+
+
+def test_needs_rebuild_threshold():
+    t = builtin_params("C")
+    fr = Frame([[0, 0, 0], [1.5, 0, 0], [3.0, 0, 0]], (20, 20, 20), (False,) * 3)
+    nl = B.build_neighbor_list(fr, 2.1, 0.3)
+    assert not B.needs_rebuild(fr, nl)
+    fr.positions[1, 1] += 0.5 * 0.3 - 1e-9
+    assert not B.needs_rebuild(fr, nl)
+    fr.positions[1, 1] += 2e-9
+    assert B.needs_rebuild(fr, nl)
+    p = Frame([[0.2, 5, 5]], (10, 10, 10), (True, False, False))
+    nlp = B.build_neighbor_list(p, 2.1, 0.3)
+    p.positions[0, 0] = 9.95
+    assert B.needs_rebuild(p, nlp)
