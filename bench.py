@@ -52,8 +52,12 @@ FLOPS_TRIP = 32 + 55 + 4 * 15 + 31
 FLOPS_TAPER = 2 + 3 + 15 + 26 + 26                           # per tapered f_C
 
 
+def _jsonable(o):
+    return o.item() if hasattr(o, "item") else str(o)
+
+
 def algorithmic_flops(stats):
-    return (FLOPS_PAIR * stats[2] + FLOPS_TAPER * stats[4]
+    return int(FLOPS_PAIR * stats[2] + FLOPS_TAPER * stats[4]
             + FLOPS_TRIP * stats[3] + FLOPS_TAPER * stats[5])
 
 
@@ -202,7 +206,7 @@ def reference_arm(args):
                                    f"ScalarOpt, OpenMP over {threads} threads"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
-    print(json.dumps(line), flush=True)
+    print(json.dumps(line, default=_jsonable), flush=True)
 
 
 def gpu_arm(args):
@@ -359,7 +363,7 @@ def gpu_arm(args):
                                           f"in {el:.1f} s (NL outside the timer); oracle/ C "
                                           f"restatement of ScalarOpt, OpenMP {cores} threads"}
     if rank == 0:
-        print(json.dumps(line), flush=True)
+        print(json.dumps(line, default=_jsonable), flush=True)
     if ws > 1:
         torch.distributed.barrier()
         torch.distributed.destroy_process_group()

@@ -585,15 +585,15 @@ extern "C" int tb_needs_rebuild(tb_context *ctx, const tb_nlist *nl, const doubl
 template <class T, int S, bool LAM3, int MODE>
 static int launch_tersoff_t(tb_context *ctx, const tb_nlist *nl, KArgs &a, int C) {
   size_t smem = SmemLayout<T, S>::bytes(C);
-  if (smem > 227 * 1024)
+  if (smem > 220 * 1024)
     return fail(ctx, TB_ERR_CONFIG, "neighbour rows of %lld entries exceed the kernel's staging",
                 (long long)nl->max_row);
   auto kern = k_tersoff<T, S, LAM3, MODE>;
-  // opt in to large dynamic shared memory once per instantiation
-  static bool done = false;
-  if (!done) {
-    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-    done = true;
+  // opt in to the dynamic shared memory this launch needs (per instantiation)
+  static size_t opted = 48 * 1024;
+  if (smem > opted) {
+    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    opted = smem;
   }
   int nb = nblk(a.n, a.atoms_per_block);
   Tables<T, S> tab = make_tables<T, S>(ctx);

@@ -576,6 +576,9 @@ __global__ void __launch_bounds__(NT, 3)
     const T inva = T(1) / ra;
     const T eax = s_ex[s], eay = s_ey[s], eaz = s_ez[s];
     const T dza = s_dz[s];
+    // (i,b,a) terms need f_C(r_a) OR its derivative: in the taper f_C can round
+    // to 0 while dF_C/dr does not (r -> R+D), so test both
+    const bool own_k1 = (S == 1) && (s_fc[s] != T(0) || s_dfc[s] != T(0));
     T Salpha = T(0), Sc = T(0), Sbx = T(0), Sby = T(0), Sbz = T(0);
     for (int b = b0; b < b1; ++b) {
       if (b == s) continue;
@@ -584,7 +587,8 @@ __global__ void __launch_bounds__(NT, 3)
       const T fcb = s_fc[sa * C + b];   // f_C(r_b) in (i,a,b)
       const T fca = s_fc[sb * C + s];   // f_C(r_a) in (i,b,a)
       const bool t1 = (dza != T(0)) && (fcb != T(0));
-      const bool t2 = (dzb != T(0)) && (fca != T(0));
+      const bool klive = (S == 1) ? own_k1 : (fca != T(0) || s_dfc[sb * C + s] != T(0));
+      const bool t2 = (dzb != T(0)) && klive;
       if (!(t1 || t2)) continue;
       const T ebx = s_ex[b], eby = s_ey[b], ebz = s_ez[b];
       T cost = eax * ebx + eay * eby + eaz * ebz;
