@@ -224,7 +224,8 @@ def gpu_arm(args):
     state, tname = structures.config(args.config)
     table = builtin_params(tname)
     n = state.natoms
-    stream = torch.cuda.current_stream()
+    stream = torch.cuda.Stream(device=dev)   # one explicit stream for torch and the C ABI
+    torch.cuda.set_stream(stream)
     ctx = _native.default_context(dev)
     ctx.set_stream(stream.cuda_stream)
     ctx.set_table(table)

@@ -64,8 +64,15 @@ int tb_create(int device, tb_context **out);
 void tb_destroy(tb_context *ctx);
 const char *tb_last_error(const tb_context *ctx);
 /* Use an external CUDA stream (cudaStream_t, e.g. torch's current stream);
- * NULL restores the context's own stream. */
+ * NULL selects the legacy default stream.  Until this is called the context
+ * uses its own non-blocking stream. */
 int tb_set_stream(tb_context *ctx, void *stream);
+/* Kernel-selection options.  TB_OPT_TILE_KERNEL = 1 forces the general
+ * shared-memory tile kernel even when the warp-chunk kernel applies (rows of
+ * <= 32 skin-list entries); used to cover both paths in the parity tests. */
+#define TB_OPT_TILE_KERNEL 1
+int tb_set_option(tb_context *ctx, int option, int value);
+
 /* Synchronise the context's stream. */
 int tb_synchronize(tb_context *ctx);
 

@@ -15,13 +15,14 @@ import numpy as np
 from .errors import ConfigurationError, InputError
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libtersoff_b200.so")
+LIB_PATH = os.environ.get("TB_LIB_PATH") or os.path.join(_HERE, "lib", "libtersoff_b200.so")
 HEADER_PATH = os.path.join(os.path.dirname(_HERE), "include", "tersoff_b200.h")
 
 TB_OK, TB_ERR_CONFIG, TB_ERR_INPUT, TB_ERR_CUDA, TB_ERR_ARG = range(5)
 PRECISION = {"double": 0, "single": 1, "mixed": 1}
 SCATTER = {"atomic": 0, "gather": 1}
 NSTATS = 6
+OPT_TILE_KERNEL = 1
 
 # symbol -> (restype, argtypes); the exported surface of the C ABI
 _P = ctypes.c_void_p
@@ -33,6 +34,7 @@ SIGNATURES = {
     "tb_destroy": (None, [_P]),
     "tb_last_error": (ctypes.c_char_p, [_P]),
     "tb_set_stream": (_I, [_P, _P]),
+    "tb_set_option": (_I, [_P, _I, _I]),
     "tb_synchronize": (_I, [_P]),
     "tb_set_params": (_I, [_P, _I, _P, _P, _P]),
     "tb_nlist_create": (_I, [_P, ctypes.POINTER(_P)]),
@@ -133,6 +135,9 @@ class Context:
     def set_stream(self, stream_ptr):
         self.check(self.lib.tb_set_stream(self.handle, ctypes.c_void_p(stream_ptr or 0)),
                    "tb_set_stream")
+
+    def set_option(self, option, value):
+        self.check(self.lib.tb_set_option(self.handle, int(option), int(value)), "tb_set_option")
 
     def synchronize(self):
         self.check(self.lib.tb_synchronize(self.handle), "tb_synchronize")

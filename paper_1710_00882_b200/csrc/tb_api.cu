@@ -13,6 +13,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -21,6 +22,7 @@
 
 #include "../../include/tersoff_b200.h"
 #include "tb_kernels.cuh"
+#include "tb_warp.cuh"
 
 #ifndef TB_VERSION_TAG
 #define TB_VERSION_TAG "dev"
@@ -64,12 +66,16 @@ struct tb_context {
   double r_cut = 0.0;
   std::vector<double> pair_mat, trip_mat;
   // scratch
-  DevBuf pos, species, forces, per_atom, result, stats, partials, fbuf, fself, errf, drift, bounds,
-      cub_tmp;
+  DevBuf pos, species, forces, per_atom, result, stats, partials, fbuf, errf, drift, bounds,
+      cub_tmp, facc, stats_acc;
+  int64_t facc_n = -1;
   ErrFlags *h_err = nullptr;      // pinned
   double *h_small = nullptr;      // pinned scratch (16 doubles)
   // kernel timing (tb_profile)
   bool profile = false;
+  bool force_tile = false;
+  bool warp_per_chunk = getenv("TB_WARP_PER_CHUNK") != nullptr;
+  int last_blocks = 0;  // grid of the last Tersoff launch (partials to reduce)  // tb_set_option(TB_OPT_TILE_KERNEL): general tile kernel only
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_used, ev_free;
 };
 
@@ -82,8 +88,10 @@ struct tb_nlist {
   int64_t entries = 0, max_row = 0;
   bool built = false;
   DevBuf offsets, nbr, rev, ref_pos, atom_cell, cell_count, cell_start, cell_atoms, row_count,
-      maxrow;
+      maxrow, nl_row, sorted_atoms, sort_keys, iota, lanes, hist;
   bool rev_valid = false;
+  int nchunks = 0;  // > 0: warp-chunk fast path available (max_row <= 32)
+  int n_empty = 0;  // atoms with empty rows: sorted_atoms[0, n_empty)
 };
 
 // ---------------------------------------------------------------------------
@@ -215,7 +223,7 @@ extern "C" void tb_destroy(tb_context *ctx) {
   cudaSetDevice(ctx->device);
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   DevBuf *bufs[] = {&ctx->pos, &ctx->species, &ctx->forces, &ctx->per_atom, &ctx->result,
-                    &ctx->stats, &ctx->partials, &ctx->fbuf, &ctx->fself, &ctx->errf,
+                    &ctx->stats, &ctx->partials, &ctx->fbuf, &ctx->facc, &ctx->stats_acc, &ctx->errf,
                     &ctx->drift, &ctx->bounds, &ctx->cub_tmp};
   for (DevBuf *b : bufs) b->release();
   for (auto *v : {&ctx->ev_used, &ctx->ev_free})
@@ -235,8 +243,17 @@ extern "C" const char *tb_last_error(const tb_context *ctx) {
 
 extern "C" int tb_set_stream(tb_context *ctx, void *stream) {
   if (!ctx) return TB_ERR_ARG;
-  ctx->stream = stream ? (cudaStream_t)stream : ctx->own;
+  ctx->stream = (cudaStream_t)stream;
   return TB_OK;
+}
+
+extern "C" int tb_set_option(tb_context *ctx, int option, int value) {
+  if (!ctx) return TB_ERR_ARG;
+  if (option == TB_OPT_TILE_KERNEL) {
+    ctx->force_tile = value != 0;
+    return TB_OK;
+  }
+  return fail(ctx, TB_ERR_ARG, "unknown option %d", option);
 }
 
 extern "C" int tb_synchronize(tb_context *ctx) {
@@ -342,7 +359,8 @@ extern "C" void tb_nlist_destroy(tb_nlist *nl) {
   cudaStreamSynchronize(nl->ctx->stream);
   DevBuf *bufs[] = {&nl->offsets, &nl->nbr, &nl->rev, &nl->ref_pos, &nl->atom_cell,
                     &nl->cell_count, &nl->cell_start, &nl->cell_atoms, &nl->row_count,
-                    &nl->maxrow};
+                    &nl->maxrow, &nl->nl_row, &nl->sorted_atoms, &nl->sort_keys,
+                    &nl->iota, &nl->lanes, &nl->hist};
   for (DevBuf *b : bufs) b->release();
   delete nl;
 }
@@ -481,7 +499,7 @@ extern "C" int tb_build_neighbors(tb_context *ctx, tb_nlist *nl, int64_t n,
     k_nl_scan<false><<<nblk(N, 128), 128, 0, ctx->stream>>>(
         N, d_pos, g, bc * bc, nl->atom_cell.as<int>(), nl->cell_start.as<int>(),
         nl->cell_atoms.as<int>(), nl->row_count.as<int>(), nullptr, nullptr,
-        nl->maxrow.as<int>());
+        nl->maxrow.as<int>(), nullptr);
     CK(cudaGetLastError());
   }
   rc = exclusive_scan(ctx, nl->row_count.as<int>(), nl->offsets.as<int>(), N + 1);
@@ -494,13 +512,62 @@ extern "C" int tb_build_neighbors(tb_context *ctx, tb_nlist *nl, int64_t n,
   nl->entries = tail[0];
   nl->max_row = tail[1];
   CK(nl->nbr.ensure(sizeof(int) * std::max<int64_t>(nl->entries, 1)));
+  CK(nl->nl_row.ensure(sizeof(int) * std::max<int64_t>(nl->entries, 1)));
   if (N) {
     k_nl_scan<true><<<nblk(N, 128), 128, 0, ctx->stream>>>(
         N, d_pos, g, bc * bc, nl->atom_cell.as<int>(), nl->cell_start.as<int>(),
-        nl->cell_atoms.as<int>(), nullptr, nl->offsets.as<int>(), nl->nbr.as<int>(), nullptr);
+        nl->cell_atoms.as<int>(), nullptr, nl->offsets.as<int>(), nl->nbr.as<int>(), nullptr,
+        nl->nl_row.as<int>());
     CK(cudaGetLastError());
     CK(cudaMemcpyAsync(nl->ref_pos.p, d_pos, sizeof(double) * 3 * N, cudaMemcpyDeviceToDevice,
                        ctx->stream));
+  }
+  // warp chunks for the fast kernel (tb_warp.cuh): rows sorted by length
+  // (stable radix sort, deterministic), floor(32/L) rows of length L per warp
+  nl->nchunks = 0;
+  nl->n_empty = 0;
+  if (nl->max_row <= 32 && N > 0) {
+    CK(nl->sorted_atoms.ensure(sizeof(int) * N));
+    CK(nl->sort_keys.ensure(sizeof(int) * N));
+    CK(nl->iota.ensure(sizeof(int) * N));
+    CK(nl->hist.ensure(sizeof(int) * 34));
+    k_iota<<<nblk(N, 256), 256, 0, ctx->stream>>>(N, nl->iota.as<int>());
+    CK(cudaGetLastError());
+    size_t tmp = 0;
+    CK(cub::DeviceRadixSort::SortPairs(nullptr, tmp, nl->row_count.as<int>(),
+                                       nl->sort_keys.as<int>(), nl->iota.as<int>(),
+                                       nl->sorted_atoms.as<int>(), N, 0, 6, ctx->stream));
+    CK(ctx->cub_tmp.ensure(tmp));
+    CK(cub::DeviceRadixSort::SortPairs(ctx->cub_tmp.p, tmp, nl->row_count.as<int>(),
+                                       nl->sort_keys.as<int>(), nl->iota.as<int>(),
+                                       nl->sorted_atoms.as<int>(), N, 0, 6, ctx->stream));
+    CK(cudaMemsetAsync(nl->hist.p, 0, sizeof(int) * 34, ctx->stream));
+    k_len_hist<<<nblk(N, 256), 256, 0, ctx->stream>>>(N, nl->row_count.as<int>(),
+                                                       nl->hist.as<int>());
+    CK(cudaGetLastError());
+    int hist[34];
+    CK(cudaMemcpyAsync(hist, nl->hist.p, sizeof(hist), cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    ChunkPlan plan;
+    memset(&plan, 0, sizeof(plan));
+    int start = hist[0], chunks = 0;
+    for (int L = 1; L <= 32; ++L) {
+      plan.count[L] = hist[L];
+      plan.bucket_start[L] = start;
+      plan.chunk_base[L] = chunks;
+      start += hist[L];
+      chunks += (hist[L] + 32 / L - 1) / (32 / L);
+    }
+    plan.chunk_base[33] = chunks;
+    nl->n_empty = hist[0];
+    if (chunks > 0) {
+      CK(nl->lanes.ensure(sizeof(int4) * 32 * (size_t)chunks));
+      k_fill_lanes<<<chunks, 32, 0, ctx->stream>>>(plan, nl->sorted_atoms.as<int>(),
+                                                    nl->offsets.as<int>(), nl->nbr.as<int>(),
+                                                    nl->lanes.as<int4>());
+      CK(cudaGetLastError());
+    }
+    nl->nchunks = chunks;
   }
   nl->built = true;
   return TB_OK;
@@ -617,6 +684,66 @@ static int launch_tersoff_t(tb_context *ctx, const tb_nlist *nl, KArgs &a, int C
   return TB_OK;
 }
 
+template <class T, int S, bool LAM3, int MODE, bool ST>
+static int launch_warp_t(tb_context *ctx, const tb_nlist *nl, KArgs &a, WArgs &w) {
+  auto kern = k_tersoff_warp<T, S, LAM3, MODE, ST>;
+  static int per_sm = 0;
+  if (!per_sm) {
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, WNT, 0));
+    per_sm = std::max(per_sm, 1);
+  }
+  int sms = 0;
+  CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device));
+  int need = nblk(w.nchunks, WPB);
+  // persistent grid: one resident wave, warps stride over the chunks
+  int nb = std::max(1, ctx->warp_per_chunk ? need : std::min(need, sms * per_sm));
+  CK(ctx->partials.ensure(sizeof(double) * 8 * nb));
+  a.partials = ctx->partials.as<double>();
+  Tables<T, S> tab = make_tables<T, S>(ctx);
+  std::pair<cudaEvent_t, cudaEvent_t> ev{nullptr, nullptr};
+  if (ctx->profile) {
+    if (ctx->ev_free.empty()) {
+      CK(cudaEventCreate(&ev.first));
+      CK(cudaEventCreate(&ev.second));
+    } else {
+      ev = ctx->ev_free.back();
+      ctx->ev_free.pop_back();
+    }
+    CK(cudaEventRecord(ev.first, ctx->stream));
+  }
+  kern<<<nb, WNT, 0, ctx->stream>>>(a, w, tab);
+  ctx->last_blocks = nb;
+  CK(cudaGetLastError());
+  if (ctx->profile) {
+    CK(cudaEventRecord(ev.second, ctx->stream));
+    ctx->ev_used.push_back(ev);
+  }
+  return TB_OK;
+}
+
+template <class T, int S, int MODE>
+static int launch_warp_m(tb_context *ctx, const tb_nlist *nl, KArgs &a, WArgs &w, bool stats) {
+  if (ctx->lam3)
+    return stats ? launch_warp_t<T, S, true, MODE, true>(ctx, nl, a, w)
+                 : launch_warp_t<T, S, true, MODE, false>(ctx, nl, a, w);
+  return stats ? launch_warp_t<T, S, false, MODE, true>(ctx, nl, a, w)
+               : launch_warp_t<T, S, false, MODE, false>(ctx, nl, a, w);
+}
+
+template <class T>
+static int launch_warp_prec(tb_context *ctx, const tb_nlist *nl, KArgs &a, WArgs &w, int mode,
+                            bool stats) {
+  switch (ctx->S) {
+    case 1:
+      return mode ? launch_warp_m<T, 1, 1>(ctx, nl, a, w, stats)
+                  : launch_warp_m<T, 1, 0>(ctx, nl, a, w, stats);
+    case 2:
+      return mode ? launch_warp_m<T, 2, 1>(ctx, nl, a, w, stats)
+                  : launch_warp_m<T, 2, 0>(ctx, nl, a, w, stats);
+  }
+  return fail(ctx, TB_ERR_CONFIG, "warp kernel: unsupported species count %d", ctx->S);
+}
+
 template <class T, int S>
 static int launch_s(tb_context *ctx, const tb_nlist *nl, KArgs &a, int C, int mode) {
   if (ctx->lam3)
@@ -688,13 +815,22 @@ static int enqueue_compute(tb_context *ctx, const tb_nlist *nl, const double *d_
       if (rc) return rc;
     }
     CK(ctx->fbuf.ensure(sizeof(double) * 3 * std::max<int64_t>(nl->entries, 1)));
-    CK(ctx->fself.ensure(sizeof(double) * 3 * std::max(n, 1)));
   }
-  if (d_stats) CK(cudaMemsetAsync(d_stats, 0, sizeof(unsigned long long) * TB_NSTATS, ctx->stream));
-  if (scatter == TB_SCATTER_ATOMIC && n)
-    CK(cudaMemsetAsync(d_forces, 0, sizeof(double) * 3 * n, ctx->stream));
+  // warp-chunk kernel for rows <= 32 entries and <= 2 species; else the tile kernel
+  const bool warp_path = nl->nchunks > 0 && !ctx->force_tile && ctx->S <= 2;
+  // force accumulator and stats counters: zero once, left zeroed by k_finalize
+  if (ctx->facc_n < n) {
+    CK(ctx->facc.ensure(sizeof(double) * 3 * std::max(n, 1)));
+    CK(cudaMemsetAsync(ctx->facc.p, 0, sizeof(double) * 3 * std::max(n, 1), ctx->stream));
+    ctx->facc_n = n;
+  }
+  if (!ctx->stats_acc.p) {
+    CK(ctx->stats_acc.ensure(sizeof(unsigned long long) * TB_NSTATS));
+    CK(cudaMemsetAsync(ctx->stats_acc.p, 0, sizeof(unsigned long long) * TB_NSTATS, ctx->stream));
+  }
   if (n == 0) {
     CK(cudaMemsetAsync(d_result, 0, sizeof(double) * 7, ctx->stream));
+    if (d_stats) CK(cudaMemsetAsync(d_stats, 0, sizeof(unsigned long long) * TB_NSTATS, ctx->stream));
     return TB_OK;
   }
   KArgs a;
@@ -706,26 +842,38 @@ static int enqueue_compute(tb_context *ctx, const tb_nlist *nl, const double *d_
   a.species = d_species;
   a.off = nl->offsets.as<int>();
   a.nbr = nl->nbr.as<int>();
-  a.forces = d_forces;
+  a.forces = ctx->facc.as<double>();
   a.fbuf = ctx->fbuf.as<double>();
-  a.fself = ctx->fself.as<double>();
   a.per_atom = d_per_atom;
   a.partials = ctx->partials.as<double>();
-  a.stats = d_stats;
+  a.stats = ctx->stats_acc.as<unsigned long long>();
   a.err = ctx->errf.as<ErrFlags>();
-  if (!d_stats) {
-    CK(ctx->stats.ensure(sizeof(unsigned long long) * TB_NSTATS));
-    a.stats = ctx->stats.as<unsigned long long>();
+  int rc;
+  int nparts = nb;
+  if (warp_path) {
+    WArgs w;
+    w.lanes = nl->lanes.as<int4>();
+    w.empty_atoms = nl->sorted_atoms.as<int>();
+    w.nchunks = nl->nchunks;
+    w.n_empty = nl->n_empty;
+    w.facc = ctx->facc.as<double>();
+    const bool want_stats = d_stats != nullptr;
+    rc = precision == TB_PREC_DOUBLE ? launch_warp_prec<double>(ctx, nl, a, w, scatter, want_stats)
+                                     : launch_warp_prec<float>(ctx, nl, a, w, scatter, want_stats);
+    nparts = ctx->last_blocks;
+  } else {
+    rc = precision == TB_PREC_DOUBLE ? launch_prec<double>(ctx, nl, a, C, scatter)
+                                     : launch_prec<float>(ctx, nl, a, C, scatter);
   }
-  int rc = precision == TB_PREC_DOUBLE ? launch_prec<double>(ctx, nl, a, C, scatter)
-                                       : launch_prec<float>(ctx, nl, a, C, scatter);
   if (rc) return rc;
-  if (scatter == TB_SCATTER_GATHER) {
-    k_force_gather<<<nblk(n, 256), 256, 0, ctx->stream>>>(n, a.off, nl->rev.as<int>(), a.fbuf,
-                                                           a.fself, d_forces);
-    CK(cudaGetLastError());
-  }
-  k_reduce_partials<<<1, 256, 0, ctx->stream>>>(nb, a.partials, d_result);
+  int fb = std::min(nblk(scatter == TB_SCATTER_GATHER ? n : 3 * (int64_t)n, 256), 4 * 148);
+  if (scatter == TB_SCATTER_GATHER)
+    k_finalize<1><<<fb, 256, 0, ctx->stream>>>(n, nullptr, a.off, nl->rev.as<int>(), a.fbuf,
+                                                d_forces, nparts, a.partials, d_result, a.stats,
+                                                d_stats);
+  else
+    k_finalize<0><<<fb, 256, 0, ctx->stream>>>(n, a.forces, nullptr, nullptr, nullptr, d_forces,
+                                                nparts, a.partials, d_result, a.stats, d_stats);
   CK(cudaGetLastError());
   return TB_OK;
 }

@@ -184,7 +184,7 @@ __global__ void k_nl_scan(int n, const double *__restrict__ pos, Grid g, double 
                           const int *__restrict__ atom_cell, const int *__restrict__ cell_start,
                           const int *__restrict__ cell_atoms, int *__restrict__ row_count,
                           const int *__restrict__ offsets, int *__restrict__ nbr,
-                          int *__restrict__ max_row) {
+                          int *__restrict__ max_row, int *__restrict__ nl_row) {
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   double xi[3];
@@ -215,6 +215,7 @@ __global__ void k_nl_scan(int n, const double *__restrict__ pos, Grid g, double 
         }
       }
   if (FILL) {
+    for (int u = 0; u < cnt; ++u) nl_row[base + u] = i;
     // rows ascending by j (neighbor.py:210-212); rows are short
     int *row = nbr + base;
     for (int u = 1; u < cnt; ++u) {
@@ -248,6 +249,23 @@ __global__ void k_nl_reverse(int n, const int *__restrict__ offsets, const int *
     }
     rev[e] = lo;
   }
+}
+
+// Row-aligned warp chunks: chunk c = the rows whose first entry lies in
+// [c*W, (c+1)*W); with W = 33 - max_row a chunk never exceeds 32 entries.
+// chunk_entry[c] = first entry of chunk c (lower_bound of c*W in offsets).
+__global__ void k_nl_chunks(int n, int nchunks, int W, const int *__restrict__ offsets,
+                            int *__restrict__ chunk_entry) {
+  int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c > nchunks) return;
+  long long key = (long long)c * W;
+  int lo = 0, hi = n;  // first row start >= key (offsets[n] = total)
+  while (lo < hi) {
+    int mid = (lo + hi) >> 1;
+    if (offsets[mid] < key) lo = mid + 1;
+    else hi = mid;
+  }
+  chunk_entry[c] = c == nchunks ? offsets[n] : offsets[lo];
 }
 
 __global__ void k_export_i64(int m, const int *__restrict__ in, int64_t *__restrict__ out) {
@@ -326,7 +344,6 @@ struct KArgs {
   const int *__restrict__ nbr;
   double *__restrict__ forces;    // ATOMIC: (n,3) zero-initialised accumulators
   double *__restrict__ fbuf;      // GATHER: per skin-list entry force (3 doubles)
-  double *__restrict__ fself;     // GATHER: per-atom self force
   double *__restrict__ per_atom;  // may be null
   double *__restrict__ partials;  // per block: [E, W xx yy zz xy xz yz, pad]
   unsigned long long *__restrict__ stats;  // TB_NSTATS counters
@@ -679,10 +696,6 @@ __global__ void __launch_bounds__(NT, 3)
       atomicAdd(a.forces + 3 * (int64_t)i, fx);
       atomicAdd(a.forces + 3 * (int64_t)i + 1, fy);
       atomicAdd(a.forces + 3 * (int64_t)i + 2, fz);
-    } else {
-      a.fself[3 * (int64_t)i] = fx;
-      a.fself[3 * (int64_t)i + 1] = fy;
-      a.fself[3 * (int64_t)i + 2] = fz;
     }
   }
   // ---- block partials: energy (atom order) and virial ----
@@ -722,22 +735,28 @@ __global__ void k_reduce_partials(int nblocks, const double *__restrict__ partia
   if (threadIdx.x < 7) result[threadIdx.x] = s[0][threadIdx.x] + 0.0;
 }
 
-// deterministic gather: F_m = self_m + sum over entries (m->i) of fbuf[rev]
+// deterministic gather from the per-entry buffer: the force on m is the sum
+// of the pieces its neighbours' terms put on it (entries i->m, found through
+// rev) minus the pieces m's own terms put on its neighbours (translation
+// invariance: F_m(self) = -sum over row m).  Row order fixes the summation.
 __global__ void k_force_gather(int n, const int *__restrict__ off, const int *__restrict__ rev,
-                               const double *__restrict__ fbuf, const double *__restrict__ fself,
-                               double *__restrict__ forces) {
+                               const double *__restrict__ fbuf, double *__restrict__ forces) {
   int m = blockIdx.x * blockDim.x + threadIdx.x;
   if (m >= n) return;
-  double fx = fself[3 * (int64_t)m], fy = fself[3 * (int64_t)m + 1], fz = fself[3 * (int64_t)m + 2];
+  double ix = 0.0, iy = 0.0, iz = 0.0, sx = 0.0, sy = 0.0, sz = 0.0;
   for (int e = off[m]; e < off[m + 1]; ++e) {
     const double *f = fbuf + 3 * (int64_t)__ldg(rev + e);
-    fx += f[0];
-    fy += f[1];
-    fz += f[2];
+    ix += f[0];
+    iy += f[1];
+    iz += f[2];
+    const double *g = fbuf + 3 * (int64_t)e;
+    sx += g[0];
+    sy += g[1];
+    sz += g[2];
   }
-  forces[3 * (int64_t)m] = fx + 0.0;
-  forces[3 * (int64_t)m + 1] = fy + 0.0;
-  forces[3 * (int64_t)m + 2] = fz + 0.0;
+  forces[3 * (int64_t)m] = (ix - sx) + 0.0;
+  forces[3 * (int64_t)m + 1] = (iy - sy) + 0.0;
+  forces[3 * (int64_t)m + 2] = (iz - sz) + 0.0;
 }
 
 // ---------------------------------------------------------------------------

@@ -20,6 +20,17 @@ FP64_TOL = 1e-10
 MIXED_TOL = 1e-5
 MIXED_E_TOL = 1e-5
 SCATTERS = ["atomic", "gather"]
+PATHS = ["warp", "tile"]
+
+
+@pytest.fixture(params=PATHS)
+def kernel_path(request):
+    """Run the test on the warp-chunk kernel and on the general tile kernel."""
+    from paper_1710_00882_b200 import _native
+    ctx = _native.default_context(0)
+    ctx.set_option(_native.OPT_TILE_KERNEL, request.param == "tile")
+    yield request.param
+    ctx.set_option(_native.OPT_TILE_KERNEL, 0)
 
 
 def rel_f(a, b):
@@ -53,7 +64,7 @@ def test_neighbor_list_edge_frames(frame):
 
 @pytest.mark.parametrize("scatter", SCATTERS)
 @pytest.mark.parametrize("name", ["dimer", "si512", "sic216", "disordered"])
-def test_fp64_matches_reference(name, scatter):
+def test_fp64_matches_reference(name, scatter, kernel_path):
     g = load_golden(name)
     t = parse_params(str(g["table"]))
     _, r = gpu_eval(golden_frame(g), t, "double", scatter)
@@ -65,7 +76,7 @@ def test_fp64_matches_reference(name, scatter):
 
 
 @pytest.mark.parametrize("name", ["si512", "sic216", "disordered"])
-def test_mixed_matches_reference_fp64(name):
+def test_mixed_matches_reference_fp64(name, kernel_path):
     g = load_golden(name)
     t = parse_params(str(g["table"]))
     _, r = gpu_eval(golden_frame(g), t, "single")
@@ -84,7 +95,7 @@ def test_dimer_frozen_goldens():
     assert np.all(r.forces[:, 1:] == 0.0)
 
 
-def test_clusters_carbon_and_two_species():
+def test_clusters_carbon_and_two_species(kernel_path):
     # free clusters incl. the synthetic table with m=1 and lam3 != 0
     for fr, table, row in golden_clusters():
         for scatter in SCATTERS:
@@ -98,7 +109,7 @@ def test_clusters_carbon_and_two_species():
         assert rel_f(rs.forces, row["forces"]) <= MIXED_TOL
 
 
-def test_virial_matches_oracle_and_strain_fd(oracle_mod):
+def test_virial_matches_oracle_and_strain_fd(oracle_mod, kernel_path):
     g = load_golden("si512")
     t = parse_params(str(g["table"]))
     fr = golden_frame(g)
@@ -116,7 +127,7 @@ def _config(idx, small=True):
 
 @pytest.mark.parametrize("idx", [1, 2, 3, 4, 5])
 @pytest.mark.parametrize("precision", ["double", "single"])
-def test_configs_vs_oracle(oracle_mod, idx, precision):
+def test_configs_vs_oracle(oracle_mod, idx, precision, kernel_path):
     st, t = _config(idx)
     nl, r = gpu_eval(st, t, precision)
     off, nb = oracle_mod.build_neighbor_list(st.positions, st.box.lengths, st.box.periodic,
@@ -133,7 +144,7 @@ def test_configs_vs_oracle(oracle_mod, idx, precision):
         assert np.abs(r.virial - o["virial"]).max() <= 1e-9 * np.abs(o["virial"]).max()
 
 
-def test_total_force_vanishes_and_gather_deterministic():
+def test_total_force_vanishes_and_gather_deterministic(kernel_path):
     st, t = _config(4)
     nl = B.build_neighbor_list(st, t.r_cut, 0.3)
     v = B.make_variant("B200", scatter="gather")
@@ -144,7 +155,7 @@ def test_total_force_vanishes_and_gather_deterministic():
     assert np.abs(a.forces.sum(axis=0)).max() < 1e-12 * st.natoms * max(1, np.abs(a.forces).max())
 
 
-def test_errors_map_to_reference_exceptions():
+def test_errors_map_to_reference_exceptions(kernel_path):
     t = builtin_params("C")
     fr = Frame([[0.0, 0, 0], [1.5, 0, 0]], (10, 10, 10), (False,) * 3)
     nl = B.build_neighbor_list(fr, t.r_cut, 0.3)
@@ -166,7 +177,7 @@ def test_errors_map_to_reference_exceptions():
         B.build_neighbor_list(box, 2.1, 0.3)
 
 
-def test_lone_and_distant_atoms():
+def test_lone_and_distant_atoms(kernel_path):
     t = builtin_params("C")
     for pos in ([[0.0, 0, 0]], [[0.0, 0, 0], [5.0, 0, 0]]):
         fr = Frame(pos, (20, 20, 20), (False,) * 3)
