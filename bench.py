@@ -56,6 +56,17 @@ def _jsonable(o):
     return o.item() if hasattr(o, "item") else str(o)
 
 
+# fp32-weighted counterparts (div 10, sqrt ~5, exp 10, pow 63, sin = cos 20)
+FLOPS32_PAIR = 19 + 25 + 3 * 10 + 2 * 10 + 4 * 63
+FLOPS32_TRIP = 32 + 55 + 4 * 10 + 10
+FLOPS32_TAPER = 2 + 3 + 10 + 20 + 20
+
+
+def algorithmic_flops32(stats):
+    return int(FLOPS32_PAIR * stats[2] + FLOPS32_TAPER * stats[4]
+               + FLOPS32_TRIP * stats[3] + FLOPS32_TAPER * stats[5])
+
+
 def algorithmic_flops(stats):
     return int(FLOPS_PAIR * stats[2] + FLOPS_TAPER * stats[4]
             + FLOPS_TRIP * stats[3] + FLOPS_TAPER * stats[5])
@@ -210,6 +221,7 @@ def reference_arm(args):
 
 
 def gpu_arm(args):
+    import ctypes
     import torch
     ws, rank, local = dist_setup()
     dev = local if ws > 1 else 0
@@ -244,54 +256,71 @@ def gpu_arm(args):
     ds = DevState()
     ds.positions, ds.species, ds.box = pos, species, state.box
     nl = B.build_neighbor_list(ds, table.r_cut, 0.3, device=dev)
-    prec = _native.PRECISION[args.precision]
     scat = _native.SCATTER[args.scatter]
     P = _native.ptr
 
-    def step(precision=prec):
+    def step(precision, with_stats=False):
         rc = lib.tb_compute_device(ctx.handle, nl._nl.handle, P(pos), P(species),
                                    float(table.r_cut), precision, scat, P(forces),
-                                   P(per_atom), P(result), P(stats))
+                                   P(per_atom), P(result), P(stats) if with_stats else None)
         if rc:
             ctx.check(rc, "tb_compute_device")
 
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=pos.device)
 
-    def timed_loop(k, precision=prec, sampler=None):
+    def capture(precision):
+        """The evaluation (Tersoff kernel + finalize) as one CUDA graph."""
+        for _ in range(3):
+            step(precision)
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=stream):
+            step(precision)
+        ctx.set_stream(stream.cuda_stream)
+        torch.cuda.synchronize()
+        return g
+
+    def timed_graph(g, k):
+        """k steps, L2 flushed between steps (outside the event bracket)."""
         starts = [torch.cuda.Event(enable_timing=True) for _ in range(k)]
         ends = [torch.cuda.Event(enable_timing=True) for _ in range(k)]
-        lib.tb_profile(ctx.handle, 1)
         torch.cuda.synchronize()
         if ws > 1:
             torch.distributed.barrier()
-        for s in range(k):
-            flush.zero_()          # L2 flush between timed steps (outside the bracket)
-            starts[s].record(stream)
+        for s_ in range(k):
+            flush.zero_()
+            starts[s_].record(stream)
+            g.replay()
+            ends[s_].record(stream)
+        torch.cuda.synchronize()
+        return sum(a_.elapsed_time(b_) for a_, b_ in zip(starts, ends))
+
+    def kernel_time(precision, k):
+        """Average Tersoff-kernel duration (CUDA events bracketing each launch on
+        the launch stream, tb_profile), same flush protocol."""
+        lib.tb_profile(ctx.handle, 1)
+        for _ in range(k):
+            flush.zero_()
             step(precision)
-            ends[s].record(stream)
         torch.cuda.synchronize()
         lib.tb_profile(ctx.handle, 0)
-        tot_ms = ctypes_double()
-        launches = ctypes_i64()
-        ctx.check(lib.tb_profile_read(ctx.handle, ctypes_ref(tot_ms), ctypes_ref(launches)),
-                  "tb_profile_read")
-        step_ms = sum(a.elapsed_time(b) for a, b in zip(starts, ends))
-        return step_ms, tot_ms.value, launches.value
+        tot, cnt = ctypes.c_double(), ctypes.c_int64()
+        ctx.check(lib.tb_profile_read(ctx.handle, ctypes.byref(tot), ctypes.byref(cnt)))
+        return tot.value / max(cnt.value, 1)
 
-    import ctypes
-    ctypes_double, ctypes_i64, ctypes_ref = ctypes.c_double, ctypes.c_int64, ctypes.byref
-
-    # warm-up (>= 3)
+    prec = _native.PRECISION[args.precision]
     for _ in range(max(3, args.warmup)):
-        step()
+        step(prec)
+    step(prec, with_stats=True)
     torch.cuda.synchronize()
     ctx.check(lib.tb_check_errors(ctx.handle), "warm-up")
     st = stats.cpu().numpy().astype(np.int64)
     energy0 = float(result[0])
+    g = capture(prec)
 
     sampler = ClockSampler(dev)
     with sampler:
-        step_ms, kern_ms, launches = timed_loop(args.steps)
+        step_ms = timed_graph(g, args.steps)
     ctx.check(lib.tb_check_errors(ctx.handle), "timed loop")
     t_local = step_ms / 1e3
     if ws > 1:
@@ -302,11 +331,11 @@ def gpu_arm(args):
         t_max = t_local
     value = ws * n * args.steps / t_max
 
-    # roofline of the Tersoff kernel (dominant launch)
-    kern_avg_s = kern_ms / 1e3 / max(launches, 1)
-    flops = algorithmic_flops(st)
-    peak = measure_fp64_peak(lib, ctx) if rank == 0 else None
-    achieved = flops / kern_avg_s / 1e12
+    # roofline of the Tersoff kernel (the dominant launch of the step)
+    kern_ms = kernel_time(prec, min(args.steps, 200))
+    flops = algorithmic_flops(st) if args.precision == "double" else algorithmic_flops32(st)
+    peak = measure_peak(lib, ctx, prec) if rank == 0 else None
+    achieved = flops / (kern_ms / 1e3) / 1e12
     traffic = None
     prof_json = os.path.join(ROOT, "profiles", "ncu_tersoff_fp64.json")
     if os.path.exists(prof_json):
@@ -315,16 +344,26 @@ def gpu_arm(args):
         except Exception:
             traffic = None
 
-    # mixed-precision mode on the same workload (reported alongside)
     extra = {}
-    if args.extras and rank == 0:
-        k2 = max(10, args.steps // 4)
-        mixed_ms, mixed_kern_ms, mixed_l = timed_loop(k2, precision=1)
-        extra["mixed"] = {"value": n * k2 / (mixed_ms / 1e3), "unit": UNIT,
-                          "kernel_ms": mixed_kern_ms / max(mixed_l, 1),
-                          "achieved_fp32_weighted_tflops": None}
+    if args.extras and rank == 0 and args.precision == "double":
+        # mixed precision on the same workload, against the FP32 pipe
+        gm = capture(1)
+        k2 = max(10, args.steps // 2)
+        mixed_ms = timed_graph(gm, k2)
+        mk = kernel_time(1, min(k2, 200))
+        mflops = algorithmic_flops32(st)
+        mpeak = measure_peak(lib, ctx, 1)
+        extra["mixed"] = {
+            "value": n * k2 / (mixed_ms / 1e3), "unit": UNIT, "steps": k2,
+            "ms_per_step": mixed_ms / k2, "dtype": "f32 math / f64 positions+accumulators",
+            "roofline": {"bound": "fp32", "achieved": mflops / (mk / 1e3) / 1e12,
+                         "peak": mpeak["tflops"] if mpeak else None, "unit": "TFLOP/s",
+                         "frac": (mflops / (mk / 1e3) / 1e12) / mpeak["tflops"] if mpeak else None,
+                         "kernel_ms": mk, "flops_per_launch": mflops,
+                         "peak_source": mpeak["source"] if mpeak else None}}
+        step(prec)  # restore the fp64 result buffers
+        torch.cuda.synchronize()
 
-    # e2e through the public API with pinned host buffers
     e2e = None
     if rank == 0:
         e2e = e2e_arm(args, B, state, table, nl, dev)
@@ -334,21 +373,27 @@ def gpu_arm(args):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_ms / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "f64" if args.precision == "double" else "f32/f64", "data": "synthetic",
-        "config": {"workload": f"BASELINE config {args.config}: {n}-atom Si diamond "
-                               f"(sigma 0.1 A), one E+F+virial evaluation per step, "
-                               f"skin-list repack at r_cut inside the step",
+        "config": {"workload": f"BASELINE config {args.config}: {n}-atom "
+                               f"{'Si diamond' if tname == 'Si' else tname}, one E+F+virial "
+                               f"evaluation per step (skin-list repack at r_cut, Tersoff "
+                               f"terms, force/energy/virial reduction), neighbour list built "
+                               f"outside the timed region",
                    "atoms": n, "precision": args.precision, "scatter": args.scatter,
                    "parallelism": f"replicas x{ws}" if ws > 1 else "single GPU",
-                   "l2": "flushed between timed steps (256 MiB write)"},
+                   "l2": "flushed between timed steps (256 MiB write)",
+                   "launch": "each step is one CUDA-graph replay (Tersoff kernel + finalize)"},
         "e2e": e2e,
-        "gpu_launches": 2 * args.steps + (args.steps if args.scatter == "gather" else 0),
-        "roofline": {"bound": "fp64", "achieved": achieved,
+        "gpu_launches": 2 * args.steps,
+        "roofline": {"bound": "fp64" if args.precision == "double" else "fp32",
+                     "achieved": achieved,
                      "peak": peak["tflops"] if peak else None, "unit": "TFLOP/s",
                      "frac": achieved / peak["tflops"] if peak else None,
                      "traffic": traffic,
-                     "kernel": "k_tersoff<double,1,false,atomic>",
-                     "kernel_ms": kern_avg_s * 1e3,
+                     "kernel": f"k_tersoff_warp<{'double' if prec == 0 else 'float'},S=1,{args.scatter}>",
+                     "kernel_ms": kern_ms,
                      "flops_per_launch": flops,
+                     "flop_convention": "SURVEY 8(d): reference ScalarOpt expression tree "
+                                        "charged once per live pair and live triplet",
                      "peak_source": peak["source"] if peak else None,
                      "counts": {"live_pairs": int(st[2]), "live_triplets": int(st[3]),
                                 "taper_pairs": int(st[4]), "taper_triplets": int(st[5]),
@@ -370,14 +415,16 @@ def gpu_arm(args):
         torch.distributed.destroy_process_group()
 
 
-def measure_fp64_peak(lib, ctx):
-    """FP64 FMA throughput measured on this GPU (MEASURED_PEAKS.json has no
-    fp64 figure): a dependent-chain-free DFMA loop over all SMs."""
+def measure_peak(lib, ctx, precision):
+    """FMA-pipe peak measured on this GPU (MEASURED_PEAKS.json has no fp64/fp32
+    figure): an 8-chain FMA loop over all SMs, best of 5 (tb_measure_peak)."""
     import ctypes
     out = ctypes.c_double()
-    if lib.tb_measure_peak(ctx.handle, 0, ctypes.byref(out)) != 0:
+    if lib.tb_measure_peak(ctx.handle, int(precision), ctypes.byref(out)) != 0:
         return None
-    return {"tflops": out.value, "source": "measured DFMA loop in bench.py (tb_measure_peak)"}
+    return {"tflops": out.value,
+            "source": f"measured {'DFMA' if precision == 0 else 'FFMA'} loop in bench.py "
+                      f"(tb_measure_peak; MEASURED_PEAKS.json has no fp64/fp32 entry)"}
 
 
 def e2e_arm(args, B, state, table, nl, dev):

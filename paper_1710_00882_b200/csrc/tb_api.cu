@@ -689,6 +689,10 @@ static int launch_warp_t(tb_context *ctx, const tb_nlist *nl, KArgs &a, WArgs &w
   auto kern = k_tersoff_warp<T, S, LAM3, MODE, ST>;
   static int per_sm = 0;
   if (!per_sm) {
+    // all of the unified L1/shared array as shared memory: occupancy is set
+    // by registers and the per-warp staging, not by a small default carveout
+    CK(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
+                            cudaSharedmemCarveoutMaxShared));
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, WNT, 0));
     per_sm = std::max(per_sm, 1);
   }

@@ -1,0 +1,131 @@
+// tb_fastmath.h -- branch-free fp64 exp / log / log1p / reciprocal for the
+// Tersoff pair term (potential.py:178-215), written for latency: polynomials
+// are evaluated with Estrin's scheme (dependency depth ~log2(degree) instead of
+// Horner's ~degree), and there are no special-case branches.
+//
+// Domains (all the pair term ever feeds them; documented in DESIGN.md):
+//   tb_exp(x):    finite x in [-708, 709]         (exp(-lam r), exp(eta log t), ...)
+//   tb_log(x):    finite normal x > 0              (log(beta zeta), zeta >= 1e-30)
+//   tb_log1p(u):  finite u >= 0                    (log(1 + (beta zeta)^eta))
+//   tb_rcp(y):    1e-30 < |y| < 1e30 (single-precision seed)
+// Accuracy (checked on the host against libm over the domains by
+// tests/test_fastmath.py): <= 2 ulp.
+//
+// Usable from host C/C++ (gcc, for the accuracy test) and device code (nvcc).
+#pragma once
+#include <math.h>
+#include <stdint.h>
+#include <string.h>
+
+#if defined(__CUDACC__)
+#define TBFM_QUAL __host__ __device__ __forceinline__
+#else
+#define TBFM_QUAL static inline
+#endif
+
+TBFM_QUAL double tbfm_from_bits(uint64_t u) {
+#if defined(__CUDA_ARCH__)
+  return __longlong_as_double((long long)u);
+#else
+  double d;
+  memcpy(&d, &u, 8);
+  return d;
+#endif
+}
+
+TBFM_QUAL uint64_t tbfm_bits(double d) {
+#if defined(__CUDA_ARCH__)
+  return (uint64_t)__double_as_longlong(d);
+#else
+  uint64_t u;
+  memcpy(&u, &d, 8);
+  return u;
+#endif
+}
+
+// exp(x): x = k ln2 + r, |r| <= ln2/2; exp(r) by its degree-12 Taylor
+// polynomial (truncation < 2e-17 relative) in Estrin form; 2^k by exponent bits.
+TBFM_QUAL double tb_exp(double x) {
+  const double L2E = 1.4426950408889634;
+  const double LN2HI = 6.93147180369123816490e-01;
+  const double LN2LO = 1.90821492927058770002e-10;
+  const double SH = 6755399441055744.0;  // 1.5 * 2^52: round-to-nearest integer trick
+  double kd = fma(x, L2E, SH);
+  const int k = (int)(int64_t)(tbfm_bits(kd) & 0xffffffffull);  // low word = rint(x log2e)
+  kd -= SH;
+  double r = fma(kd, -LN2HI, x);
+  r = fma(kd, -LN2LO, r);
+  const double r2 = r * r, r4 = r2 * r2, r8 = r4 * r4;
+  // c_n = 1/n!
+  const double p01 = fma(r, 1.0, 1.0);
+  const double p23 = fma(r, 1.0 / 6.0, 0.5);
+  const double p45 = fma(r, 1.0 / 120.0, 1.0 / 24.0);
+  const double p67 = fma(r, 1.0 / 5040.0, 1.0 / 720.0);
+  const double p89 = fma(r, 1.0 / 362880.0, 1.0 / 40320.0);
+  const double pab = fma(r, 1.0 / 39916800.0, 1.0 / 3628800.0);
+  const double pc = 1.0 / 479001600.0;
+  const double q03 = fma(r2, p23, p01);
+  const double q47 = fma(r2, p67, p45);
+  const double q8b = fma(r2, pab, p89);
+  const double q8c = fma(r4, pc, q8b);
+  const double q07 = fma(r4, q47, q03);
+  const double p = fma(r8, q8c, q07);
+  // 2^k with k in [-1021, 1023] (the domain keeps k >= -1021)
+  const double scale = tbfm_from_bits((uint64_t)(int64_t)(k + 1023) << 52);
+  return p * scale;
+}
+
+// log(x), x > 0 normal: x = 2^e m, m in [sqrt(1/2), sqrt(2)); f = m - 1,
+// s = f / (2 + f), log(m) = f - (hfsq - s (hfsq + R(s^2))) (fdlibm form),
+// R by its degree-7 polynomial in z = s^2 (fdlibm coefficients) in Estrin form.
+TBFM_QUAL double tb_rcp(double y);
+TBFM_QUAL double tb_log(double x) {
+  uint64_t u = tbfm_bits(x);
+  int e = (int)((u >> 52) & 0x7ff) - 1023;
+  // mantissa in [1, 2); move to [sqrt(1/2), sqrt(2)) (compare on the high word)
+  uint64_t mb = (u & 0x000fffffffffffffull) | 0x3ff0000000000000ull;
+  const uint64_t hi = mb >> 32;
+  const int big = hi > 0x3ff6a09eull;  // m > sqrt(2)
+  mb -= (uint64_t)big << 52;           // halve m
+  e += big;
+  const double m = tbfm_from_bits(mb);
+  const double f = m - 1.0;
+  const double s = f * tb_rcp(2.0 + f);
+  const double z = s * s, w = z * z;
+  const double Lg1 = 6.666666666666735130e-01, Lg2 = 3.999999999940941908e-01,
+               Lg3 = 2.857142874366239149e-01, Lg4 = 2.222219843214978396e-01,
+               Lg5 = 1.818357216161805012e-01, Lg6 = 1.531383769920937332e-01,
+               Lg7 = 1.479819860511658591e-01;
+  // R = z (Lg1 + z Lg2 + ... + z^6 Lg7), Estrin in z
+  const double a = fma(z, Lg2, Lg1);
+  const double b = fma(z, Lg4, Lg3);
+  const double c = fma(z, Lg6, Lg5);
+  const double ab = fma(w, b, a);
+  const double cd = fma(w, Lg7, c);
+  const double R = z * fma(w * w, cd, ab);
+  const double hfsq = 0.5 * f * f;
+  const double ed = (double)e;
+  const double LN2HI = 6.93147180369123816490e-01;
+  const double LN2LO = 1.90821492927058770002e-10;
+  return fma(ed, LN2HI, f - (hfsq - (s * (hfsq + R) + ed * LN2LO)));
+}
+
+// 1/y: single-precision seed, two Newton steps (2^-23 -> 2^-46 -> 2^-92).
+TBFM_QUAL double tb_rcp(double y) {
+#if defined(__CUDA_ARCH__)
+  double r = (double)__frcp_rn((float)y);
+#else
+  double r = (double)(1.0f / (float)y);
+#endif
+  double e = fma(-y, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-y, r, 1.0);
+  return fma(r, e, r);
+}
+
+// log1p(u), u >= 0: w = 1 + u rounded; log1p(u) = log(w) + (u - (w - 1)) / w.
+TBFM_QUAL double tb_log1p(double u) {
+  const double w = 1.0 + u;
+  const double c = (u - (w - 1.0)) * tb_rcp(w);
+  return tb_log(w) + c;
+}

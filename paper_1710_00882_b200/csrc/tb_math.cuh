@@ -14,6 +14,8 @@
 #include <cuda_runtime.h>
 #include <math.h>
 
+#include "tb_fastmath.h"
+
 namespace tb {
 
 constexpr int SMAX = 4;
@@ -44,15 +46,15 @@ struct Tables {
 };
 
 // ---- transcendental wrappers (overloads keep the templates readable) ----
-__device__ __forceinline__ double t_exp(double x) { return exp(x); }
+__device__ __forceinline__ double t_exp(double x) { return tb_exp(x); }
 __device__ __forceinline__ float t_exp(float x) { return expf(x); }
-__device__ __forceinline__ double t_log(double x) { return log(x); }
+__device__ __forceinline__ double t_log(double x) { return tb_log(x); }
 __device__ __forceinline__ float t_log(float x) { return logf(x); }
-__device__ __forceinline__ double t_log1p(double x) { return log1p(x); }
+__device__ __forceinline__ double t_log1p(double x) { return tb_log1p(x); }
 __device__ __forceinline__ float t_log1p(float x) { return log1pf(x); }
 __device__ __forceinline__ void t_sincospi(double x, double *s, double *c) { sincospi(x, s, c); }
 __device__ __forceinline__ void t_sincospi(float x, float *s, float *c) { sincospif(x, s, c); }
-__device__ __forceinline__ double t_rcp(double x) { return 1.0 / x; }
+__device__ __forceinline__ double t_rcp(double x) { return tb_rcp(x); }
 __device__ __forceinline__ float t_rcp(float x) { return __frcp_rn(x); }
 
 // f_C and dF_C/dr with inclusive exact plateaus (potential.py:167-175).
@@ -116,15 +118,19 @@ __device__ __forceinline__ void pair_part(T r, T zeta, const PairP<T> &p, T &v, 
   T t = p.beta * zeta;
   T b, db;
   if (zeta < T(ZETA_TINY)) {
-    // (beta zeta)^eta with zeta ~ 0; exact b = 1 at zeta == 0
-    T u = zeta > T(0) ? t_exp(p.eta * t_log(t)) : T(0);
-    b = t_exp(p.neg_half_inv_eta * t_log1p(u));
+    // isolated bond (potential.py:202-215): db = 0; b from the library
+    // functions, which also cover subnormal beta*zeta (exact b = 1 at zeta = 0)
+    T u = zeta > T(0) ? pow(t, p.eta) : T(0);
+    b = pow(T(1) + u, p.neg_half_inv_eta);
     db = T(0);
   } else {
-    T u = t_exp(p.eta * t_log(t));
+    // u = t^eta, b = (1+u)^(-1/2eta); db/dzeta = -beta/2 t^(eta-1) (1+u)^(-1/2eta-1)
+    //   = -beta/2 * exp((eta-1) log t) * b / (1+u)
+    const T lt = t_log(t);
+    T u = t_exp(p.eta * lt);
     T opu = T(1) + u;
     b = t_exp(p.neg_half_inv_eta * t_log1p(u));
-    db = p.neg_half_beta * (u / t) * (b / opu);
+    db = p.neg_half_beta * t_exp((p.eta - T(1)) * lt) * (b * t_rcp(opu));
   }
   T inner = fr + b * fa;
   v = fc * inner;

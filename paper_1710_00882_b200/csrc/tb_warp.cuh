@@ -26,7 +26,7 @@ namespace tb {
 #endif
 constexpr int WNT = 128;  // threads per block of the warp kernel
 constexpr int WPB = WNT / 32;
-constexpr int QCAP = 8;   // k-iterations whose angular values are cached
+constexpr int QCAP = 4;   // k-iterations whose angular values are cached
 
 template <class V>
 __device__ __forceinline__ V shfl(V v, int src) {
@@ -50,17 +50,74 @@ struct WArgs {
 };
 
 struct WAcc {
-  double acc_e = 0, wxx = 0, wyy = 0, wzz = 0, wxy = 0, wxz = 0, wyz = 0;
+  // energy and virial live in the per-lane shared slots (acc[7][32]) to keep
+  // registers for occupancy; only the optional counters stay in registers
+  double *acc;  // &s_acc[wid][0][lane], stride 32
   unsigned long long c_vis = 0, c_pk = 0, c_lp = 0, c_lt = 0, c_tp = 0, c_tt = 0;
 };
+
+// per-warp table of the lanes' neighbour data, read by the other lanes of
+// the same atom row with vector shared loads (2 x LDS.128 for e_b and r_b)
+template <class T> struct Vec2;
+template <> struct Vec2<double> { using t = double2; };
+template <> struct Vec2<float> { using t = float2; };
+
+template <class T>
+struct WTable {
+  using T2 = typename Vec2<T>::t;
+  T2 exy[32];   // e_x, e_y
+  T2 ezr[32];   // e_z, r
+  T2 fc[32];    // f_C(r) with the k-role entry for j-species 0 / 1
+  T dz[32];     // delta_zeta of the (i, lane) pair
+  double v[32]; // V of the (i, lane) pair (row sum -> e_i)
+  int sp[32];   // species of the lane's neighbour
+};
+
+// per-warp double-buffered staging of the gathered operands (cp.async)
+struct WStage {
+  double xi[3][32], xj[3][32];
+  int si[32], sj[32];
+};
+
+__device__ __forceinline__ void cp_async8(void *smem, const void *gmem) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async4(void *smem, const void *gmem) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+// issue the gathers of one chunk's operands into a stage
+template <int S>
+__device__ __forceinline__ void stage_chunk(WStage &st, const int4 rec, const int lane,
+                                            const double *__restrict__ pos,
+                                            const int *__restrict__ species) {
+  if (rec.x >= 0) {
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+      cp_async8(&st.xi[q][lane], pos + 3 * (int64_t)rec.y + q);
+      cp_async8(&st.xj[q][lane], pos + 3 * (int64_t)rec.z + q);
+    }
+    cp_async4(&st.si[lane], species + rec.y);
+    if (S > 1) cp_async4(&st.sj[lane], species + rec.z);
+  }
+}
 
 // One chunk: rows of length L (LC > 0: compile-time, loops fully unrolled so
 // the independent k-iterations interleave; LC == 0: runtime Ldyn).
 template <class T, int S, bool LAM3, int MODE, bool ST, int LC>
 __device__ __forceinline__ void chunk_body(const KArgs &a, const WArgs &w, const Tables<T, S> &tab,
-                                           T (*s_cache)[3][32], const int lane, const int4 cur,
-                                           const double (&cxi)[3], const double (&cxj)[3],
-                                           const int Ldyn, WAcc &A) {
+                                           T (*s_cache)[3][32], WTable<T> &tb, const int lane,
+                                           const int4 cur, const WStage &stg, const int Ldyn,
+                                           WAcc &A) {
+  static_assert(S <= 2, "the warp kernel handles up to two species");
+  using T2 = typename Vec2<T>::t;
   const int e = cur.x, i = cur.y, j = cur.z;
   const int L = LC > 0 ? LC : Ldyn;  // warp-uniform row length
   const bool valid = e >= 0;
@@ -71,9 +128,11 @@ __device__ __forceinline__ void chunk_body(const KArgs &a, const WArgs &w, const
   double d[3] = {0, 0, 0}, r2 = 1.0;
   int si = 0, sj = 0;
   if (valid) {
+    const double cxi[3] = {stg.xi[0][lane], stg.xi[1][lane], stg.xi[2][lane]};
+    const double cxj[3] = {stg.xj[0][lane], stg.xj[1][lane], stg.xj[2][lane]};
     r2 = disp_r2(cxi, cxj, a.box, d);
-    si = __ldg(a.species + i);
-    sj = S > 1 ? __ldg(a.species + j) : 0;
+    si = stg.si[lane];
+    sj = S > 1 ? stg.sj[lane] : 0;
     if (pos == 0) {
       if (!(isfinite(cxi[0]) && isfinite(cxi[1]) && isfinite(cxi[2])))
         atomicMin(&a.err->nonfinite_atom, i);
@@ -96,7 +155,7 @@ __device__ __forceinline__ void chunk_body(const KArgs &a, const WArgs &w, const
     atomicMin(&a.err->coinc_key, key);
   }
   const double rd = live ? sqrt(r2) : 1.0;
-  const double invd = 1.0 / rd;
+  const double invd = tb_rcp(rd);
   const T ex = (T)(d[0] * invd), ey = (T)(d[1] * invd), ez = (T)(d[2] * invd);
   const T ra = (T)rd;
   // f_C(r) of this entry acting as k in (i, q, this) for every species q of j
@@ -109,21 +168,31 @@ __device__ __forceinline__ void chunk_body(const KArgs &a, const WArgs &w, const
   }
   const PairP<T> &pp = tab.pair[si * S + sj];
   const bool pair_live = live && ra < pp.Rp;
+  {
+    T2 a2, b2, c2;
+    a2.x = ex;
+    a2.y = ey;
+    b2.x = ez;
+    b2.y = ra;
+    c2.x = fck[0];
+    c2.y = fck[S > 1 ? 1 : 0];
+    tb.exy[lane] = a2;
+    tb.ezr[lane] = b2;
+    tb.fc[lane] = c2;
+    if (S > 1) tb.sp[lane] = sj;
+  }
+  __syncwarp();
 
   // ---- phase 1: zeta (and the angular cache) ----
   T zeta = T(0);
 #pragma unroll
   for (int q = 1; q < L; ++q) {
     const int src = first + (pos + q >= L ? pos + q - L : pos + q);
-    const T bx = shfl(ex, src), by = shfl(ey, src), bz = shfl(ez, src);
-    T fcb[S];
-#pragma unroll
-    for (int t = 0; t < S; ++t) fcb[t] = shfl(fck[t], src);
-    const int sb = S > 1 ? shfl(sj, src) : 0;
-    const T rb = LAM3 ? shfl(ra, src) : T(0);
     if (!live) continue;
+    const T2 bxy = tb.exy[src], bzr = tb.ezr[src], bfc = tb.fc[src];
+    const int sb = S > 1 ? tb.sp[src] : 0;
     const TripP<T> &tp = tab.trip[(si * S + sj) * S + sb];
-    T cost = ex * bx + ey * by + ez * bz;
+    T cost = ex * bxy.x + ey * bxy.y + ez * bzr.x;
     cost = fmin(T(1), fmax(T(-1), cost));
     T g, dg;
     angular(cost, tp, g, dg);
@@ -132,7 +201,7 @@ __device__ __forceinline__ void chunk_body(const KArgs &a, const WArgs &w, const
       s_cache[q - 1][1][lane] = g;
       s_cache[q - 1][2][lane] = dg;
     }
-    const T f = pick(fcb, sj);  // f_C(r_b) with entry (i, a, b)
+    const T f = (S > 1 && sj == 1) ? bfc.y : bfc.x;  // f_C(r_b) with entry (i, a, b)
     if (pair_live && f != T(0)) {
       if (ST) {
         A.c_lt++;
@@ -141,7 +210,7 @@ __device__ __forceinline__ void chunk_body(const KArgs &a, const WArgs &w, const
       T term = f * g;
       if (LAM3) {
         T exv, darg;
-        lam3_term(ra - rb, tp, exv, darg);
+        lam3_term(ra - bzr.y, tp, exv, darg);
         term *= exv;
       }
       zeta += term;
@@ -159,34 +228,35 @@ __device__ __forceinline__ void chunk_body(const KArgs &a, const WArgs &w, const
     pair_part(ra, zeta, pp, v, dvdr, dz);
 #endif
   }
+  tb.dz[lane] = dz;
+  tb.v[lane] = (double)v;
+  __syncwarp();
 
   // ---- phase 2: force on this neighbour from the terms centred on i ----
   T Sal = T(0), Sc = T(0), Sbx = T(0), Sby = T(0), Sbz = T(0);
 #pragma unroll
   for (int q = 1; q < L; ++q) {
     const int src = first + (pos + q >= L ? pos + q - L : pos + q);
-    const T bx = shfl(ex, src), by = shfl(ey, src), bz = shfl(ez, src);
-    const T dzb = shfl(dz, src);
-    T fcb[S];
-#pragma unroll
-    for (int t = 0; t < S; ++t) fcb[t] = shfl(fck[t], src);
-    const int sb = S > 1 ? shfl(sj, src) : 0;
-    const T rb = LAM3 ? shfl(ra, src) : T(0);
     if (!live) continue;
-    const T f_b = pick(fcb, sj);     // f_C(r_b) in (i,a,b)
-    const T f_a = pick(fck, sb);     // f_C(r_a) in (i,b,a)
+    const T dzb = tb.dz[src];
+    const T2 bfc = tb.fc[src];
+    const int sb = S > 1 ? tb.sp[src] : 0;
+    const T f_b = (S > 1 && sj == 1) ? bfc.y : bfc.x;  // f_C(r_b) in (i,a,b)
+    const T f_a = pick(fck, sb);                        // f_C(r_a) in (i,b,a)
     const T df_a = pick(dfck, sb);
     const bool t1 = (dz != T(0)) && (f_b != T(0));
     // f_C may round to 0 in the taper while dF_C/dr does not: test both
     const bool t2 = (dzb != T(0)) && (f_a != T(0) || df_a != T(0));
     if (!(t1 || t2)) continue;
+    const T2 bxy = tb.exy[src], bzr = tb.ezr[src];
+    const T rb = bzr.y;
     T cost, g, dg;
     if (q <= QCAP) {
       cost = s_cache[q - 1][0][lane];
       g = s_cache[q - 1][1][lane];
       dg = s_cache[q - 1][2][lane];
     } else {
-      cost = ex * bx + ey * by + ez * bz;
+      cost = ex * bxy.x + ey * bxy.y + ez * bzr.x;
       cost = fmin(T(1), fmax(T(-1), cost));
       angular(cost, tab.trip[(si * S + sj) * S + sb], g, dg);
     }
@@ -214,22 +284,22 @@ __device__ __forceinline__ void chunk_body(const KArgs &a, const WArgs &w, const
     }
     Sal += alpha;
     Sc += beta * cost;
-    Sbx += beta * bx;
-    Sby += beta * by;
-    Sbz += beta * bz;
+    Sbx += beta * bxy.x;
+    Sby += beta * bxy.y;
+    Sbz += beta * bzr.x;
   }
   if (live) {
-    const T inva = T(1) / ra;
+    const T inva = t_rcp(ra);
     const T ca = dvdr + Sal - Sc * inva;
     const double fx = -(double)(ca * ex + inva * Sbx);
     const double fy = -(double)(ca * ey + inva * Sby);
     const double fz = -(double)(ca * ez + inva * Sbz);
-    A.wxx += d[0] * fx;
-    A.wyy += d[1] * fy;
-    A.wzz += d[2] * fz;
-    A.wxy += d[0] * fy;
-    A.wxz += d[0] * fz;
-    A.wyz += d[1] * fz;
+    A.acc[32 * 1] += d[0] * fx;
+    A.acc[32 * 2] += d[1] * fy;
+    A.acc[32 * 3] += d[2] * fz;
+    A.acc[32 * 4] += d[0] * fy;
+    A.acc[32 * 5] += d[0] * fz;
+    A.acc[32 * 6] += d[1] * fz;
     if (MODE == 0) {
       double *fj = w.facc + 3 * (int64_t)j, *fi = w.facc + 3 * (int64_t)i;
       atomicAdd(fj, fx);
@@ -250,15 +320,13 @@ __device__ __forceinline__ void chunk_body(const KArgs &a, const WArgs &w, const
     fb[1] = 0.0;
     fb[2] = 0.0;
   }
-  // ---- e_i: segmented reduction over the L lanes of atom i ----
-  double se = (double)v;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const double oe = __shfl_down_sync(0xffffffffu, se, o);
-    if (pos + o < L) se += oe;
-  }
+  // ---- e_i: the first lane of each row sums the row's V (row order) ----
   if (valid && pos == 0) {
-    A.acc_e += se;
+    double se = 0.0;
+#pragma unroll
+    for (int q = 0; q < (LC > 0 ? LC : 1); ++q) se += tb.v[lane + q];
+    for (int q = LC > 0 ? LC : 1; q < L; ++q) se += tb.v[lane + q];
+    A.acc[0] += se;
     if (a.per_atom) a.per_atom[i] = se + 0.0;
   }
 }
@@ -269,6 +337,9 @@ __global__ void __launch_bounds__(WNT, TB_WARP_MINB)
   __shared__ Tables<T, S> s_tab;
   __shared__ double s_red[WPB][8];
   __shared__ T s_cache[WPB][QCAP][3][32];  // cos, g, dg of (i,a,b) from phase 1
+  __shared__ WStage s_stage[WPB][2];         // gathered operands, double-buffered
+  __shared__ double s_acc[WPB][7][32];       // per-lane energy + virial
+  __shared__ WTable<T> s_tb[WPB];            // lanes' neighbour data (per warp)
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   if (S > 1) {
     const int *src = reinterpret_cast<const int *>(&gtab);
@@ -286,53 +357,43 @@ __global__ void __launch_bounds__(WNT, TB_WARP_MINB)
   }
 
   WAcc A;
+#pragma unroll
+  for (int q = 0; q < 7; ++q) s_acc[wid][q][lane] = 0.0;
+  A.acc = &s_acc[wid][0][lane];
 
-  // software pipeline over this warp's chunks: lane records two chunks ahead,
-  // positions one chunk ahead, so the dependent gathers overlap the math
+  // software pipeline over this warp's chunks: lane records in registers two
+  // chunks ahead; the position/species gathers of the next chunk are issued
+  // as cp.async into the other stage while this chunk computes
   const int stride = gridDim.x * WPB;
   int c = blockIdx.x * WPB + wid;
   const int4 idle = make_int4(-1, 0, 0, 1);
   int4 cur = c < w.nchunks ? __ldg(w.lanes + 32 * (int64_t)c + lane) : idle;
   int4 nxt = c + stride < w.nchunks ? __ldg(w.lanes + 32 * (int64_t)(c + stride) + lane) : idle;
-  double cxi[3] = {0, 0, 0}, cxj[3] = {0, 0, 0};
-  if (cur.x >= 0) {
-    load3(a.pos, cur.y, cxi);
-    load3(a.pos, cur.z, cxj);
-  }
+  stage_chunk<S>(s_stage[wid][0], cur, lane, a.pos, a.species);
+  cp_async_commit();
+  int buf = 0;
   for (; c < w.nchunks; c += stride) {
     const int4 nx2 = c + 2 * stride < w.nchunks
                          ? __ldg(w.lanes + 32 * (int64_t)(c + 2 * stride) + lane)
                          : idle;
-#ifndef TB_NO_POS_PREFETCH
-    double nxi[3] = {0, 0, 0}, nxj[3] = {0, 0, 0};
-    if (nxt.x >= 0) {
-      load3(a.pos, nxt.y, nxi);
-      load3(a.pos, nxt.z, nxj);
-    }
-#endif
+    stage_chunk<S>(s_stage[wid][buf ^ 1], nxt, lane, a.pos, a.species);
+    cp_async_commit();
+    cp_async_wait<1>();  // this lane's gathers for the current chunk have landed
+    const WStage &stg = s_stage[wid][buf];
     const int Ldyn = __shfl_sync(0xffffffffu, cur.w, 0);
     switch (Ldyn) {
-      case 4: chunk_body<T, S, LAM3, MODE, ST, 4>(a, w, tab, s_cache[wid], lane, cur, cxi, cxj, Ldyn, A); break;
-      case 5: chunk_body<T, S, LAM3, MODE, ST, 5>(a, w, tab, s_cache[wid], lane, cur, cxi, cxj, Ldyn, A); break;
-      case 3: chunk_body<T, S, LAM3, MODE, ST, 3>(a, w, tab, s_cache[wid], lane, cur, cxi, cxj, Ldyn, A); break;
-      case 6: chunk_body<T, S, LAM3, MODE, ST, 6>(a, w, tab, s_cache[wid], lane, cur, cxi, cxj, Ldyn, A); break;
-      default: chunk_body<T, S, LAM3, MODE, ST, 0>(a, w, tab, s_cache[wid], lane, cur, cxi, cxj, Ldyn, A);
+      case 4: chunk_body<T, S, LAM3, MODE, ST, 4>(a, w, tab, s_cache[wid], s_tb[wid], lane, cur, stg, Ldyn, A); break;
+      case 5: chunk_body<T, S, LAM3, MODE, ST, 5>(a, w, tab, s_cache[wid], s_tb[wid], lane, cur, stg, Ldyn, A); break;
+      case 3: chunk_body<T, S, LAM3, MODE, ST, 3>(a, w, tab, s_cache[wid], s_tb[wid], lane, cur, stg, Ldyn, A); break;
+      case 6: chunk_body<T, S, LAM3, MODE, ST, 6>(a, w, tab, s_cache[wid], s_tb[wid], lane, cur, stg, Ldyn, A); break;
+      default: chunk_body<T, S, LAM3, MODE, ST, 0>(a, w, tab, s_cache[wid], s_tb[wid], lane, cur, stg, Ldyn, A);
     }
+    __syncwarp();  // the stage and the lane table are rewritten next iteration
     cur = nxt;
     nxt = nx2;
-#ifndef TB_NO_POS_PREFETCH
-#pragma unroll
-    for (int q = 0; q < 3; ++q) {
-      cxi[q] = nxi[q];
-      cxj[q] = nxj[q];
-    }
-#else
-    if (cur.x >= 0) {
-      load3(a.pos, cur.y, cxi);
-      load3(a.pos, cur.z, cxj);
-    }
-#endif
+    buf ^= 1;
   }
+  cp_async_wait<0>();
 
   // ---- stats and block partials (reduced by the finalize kernel) ----
   if (ST) {
@@ -343,7 +404,9 @@ __global__ void __launch_bounds__(WNT, TB_WARP_MINB)
       if (lane == 0 && v) atomicAdd(&a.stats[q], v);
     }
   }
-  double vals[7] = {A.acc_e, A.wxx, A.wyy, A.wzz, A.wxy, A.wxz, A.wyz};
+  double vals[7];
+#pragma unroll
+  for (int q = 0; q < 7; ++q) vals[q] = s_acc[wid][q][lane];
 #pragma unroll
   for (int q = 0; q < 7; ++q) {
     double v = warp_sum(vals[q]);

@@ -1,0 +1,39 @@
+/* Host accuracy check of csrc/tb_fastmath.h against glibc libm (test only).
+ * Prints the max ulp error of tb_exp / tb_log / tb_log1p / tb_rcp over
+ * their documented domains. */
+#include <stdio.h>
+#include <stdlib.h>
+#include <math.h>
+#include "../../paper_1710_00882_b200/csrc/tb_fastmath.h"
+
+static double ulp_err(double got, double want) {
+  if (got == want) return 0.0;
+  double sp = nextafter(fabs(want), INFINITY) - fabs(want);
+  return fabs(got - want) / sp;
+}
+static double urand(unsigned long long *s) {
+  *s = *s * 6364136223846793005ULL + 1442695040888963407ULL;
+  return (double)(*s >> 11) * (1.0 / 9007199254740992.0);
+}
+int main(int argc, char **argv) {
+  long n = argc > 1 ? atol(argv[1]) : 2000000;
+  unsigned long long s = 12345;
+  double me = 0, ml = 0, m1 = 0, mr = 0;
+  for (long i = 0; i < n; ++i) {
+    double x = -708.0 + 1417.0 * urand(&s);
+    double e = ulp_err(tb_exp(x), exp(x)); if (e > me) me = e;
+    double xs = -20.0 + 25.0 * urand(&s);  /* the pair-term range */
+    e = ulp_err(tb_exp(xs), exp(xs)); if (e > me) me = e;
+    double y = exp(-700.0 + 1400.0 * urand(&s));
+    e = ulp_err(tb_log(y), log(y)); if (e > ml) ml = e;
+    double y2 = 0.5 + 1.5 * urand(&s);
+    e = ulp_err(tb_log(y2), log(y2)); if (e > ml) ml = e;
+    double u = exp(-80.0 + 90.0 * urand(&s));
+    e = ulp_err(tb_log1p(u), log1p(u)); if (e > m1) m1 = e;
+    double v = exp(-69.0 + 138.0 * urand(&s));  /* float-representable */
+    e = ulp_err(tb_rcp(v), 1.0 / v); if (e > mr) mr = e;
+  }
+  printf("{\"exp_ulp\": %.3f, \"log_ulp\": %.3f, \"log1p_ulp\": %.3f, \"rcp_ulp\": %.3f, \"n\": %ld}\n",
+         me, ml, m1, mr, n);
+  return 0;
+}

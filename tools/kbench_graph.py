@@ -7,7 +7,11 @@ import torch
 import paper_1710_00882_b200 as B
 from paper_1710_00882_b200 import _native, structures
 cfg = int(os.environ.get("KB_CONFIG", "2"))
-st, tn = structures.config(cfg)
+if os.environ.get("KB_CELLS"):
+    st = structures.seed_velocities(structures.displace(structures.gen_diamond(int(os.environ["KB_CELLS"]), 5.431), 0.1, 1002), 1000.0, 2002)
+    tn = "Si"
+else:
+    st, tn = structures.config(cfg)
 t = B.builtin_params(tn)
 n = st.natoms
 s = torch.cuda.Stream(); torch.cuda.set_stream(s)
