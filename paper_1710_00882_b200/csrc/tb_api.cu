@@ -871,6 +871,8 @@ static int enqueue_compute(tb_context *ctx, const tb_nlist *nl, const double *d_
   }
   if (rc) return rc;
   int fb = std::min(nblk(scatter == TB_SCATTER_GATHER ? n : 3 * (int64_t)n, 256), 4 * 148);
+  // (a programmatic-dependent finalize launch, a cooperative grid-barrier
+  //  finalize and a last-block reduction were all measured slower)
   if (scatter == TB_SCATTER_GATHER)
     k_finalize<1><<<fb, 256, 0, ctx->stream>>>(n, nullptr, a.off, nl->rev.as<int>(), a.fbuf,
                                                 d_forces, nparts, a.partials, d_result, a.stats,

@@ -7,7 +7,7 @@
 //   tb_exp(x):    finite x in [-708, 709]         (exp(-lam r), exp(eta log t), ...)
 //   tb_log(x):    finite normal x > 0              (log(beta zeta), zeta >= 1e-30)
 //   tb_log1p(u):  finite u >= 0                    (log(1 + (beta zeta)^eta))
-//   tb_rcp(y):    1e-30 < |y| < 1e30 (single-precision seed)
+//   tb_rcp(y):    1e-30 < |y| < 1e30 (float-representable seed)
 // Accuracy (checked on the host against libm over the domains by
 // tests/test_fastmath.py): <= 2 ulp.
 //
@@ -110,9 +110,11 @@ TBFM_QUAL double tb_log(double x) {
   return fma(ed, LN2HI, f - (hfsq - (s * (hfsq + R) + ed * LN2LO)));
 }
 
-// 1/y: single-precision seed, two Newton steps (2^-23 -> 2^-46 -> 2^-92).
+// 1/y: single-precision reciprocal seed (~2^-24), two Newton steps (-> 2^-48
+// -> 2^-96).
 TBFM_QUAL double tb_rcp(double y) {
 #if defined(__CUDA_ARCH__)
+  // (__frcp_rn measured faster here than rcp.approx.f32 or MUFU.RCP64H seeds)
   double r = (double)__frcp_rn((float)y);
 #else
   double r = (double)(1.0f / (float)y);

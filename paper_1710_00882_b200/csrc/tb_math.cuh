@@ -55,7 +55,11 @@ __device__ __forceinline__ float t_log1p(float x) { return log1pf(x); }
 __device__ __forceinline__ void t_sincospi(double x, double *s, double *c) { sincospi(x, s, c); }
 __device__ __forceinline__ void t_sincospi(float x, float *s, float *c) { sincospif(x, s, c); }
 __device__ __forceinline__ double t_rcp(double x) { return tb_rcp(x); }
-__device__ __forceinline__ float t_rcp(float x) { return __frcp_rn(x); }
+__device__ __forceinline__ float t_rcp(float x) {
+  float r;  // MUFU.RCP (~1 ulp) -- the mixed mode's tolerance is 1e-5
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
 
 // f_C and dF_C/dr with inclusive exact plateaus (potential.py:167-175).
 // Returns false when r >= R + D (exactly zero contribution).

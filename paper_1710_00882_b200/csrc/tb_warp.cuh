@@ -301,7 +301,7 @@ __device__ __forceinline__ void chunk_body(const KArgs &a, const WArgs &w, const
     A.acc[32 * 5] += d[0] * fz;
     A.acc[32 * 6] += d[1] * fz;
     if (MODE == 0) {
-      double *fj = w.facc + 3 * (int64_t)j, *fi = w.facc + 3 * (int64_t)i;
+      double *fj = w.facc + 3 * (int64_t)j, *fi = w.facc + 3 * (int64_t)i;  // facc: accumulator
       atomicAdd(fj, fx);
       atomicAdd(fj + 1, fy);
       atomicAdd(fj + 2, fz);
@@ -328,6 +328,64 @@ __device__ __forceinline__ void chunk_body(const KArgs &a, const WArgs &w, const
     for (int q = LC > 0 ? LC : 1; q < L; ++q) se += tb.v[lane + q];
     A.acc[0] += se;
     if (a.per_atom) a.per_atom[i] = se + 0.0;
+  }
+}
+
+template <int MODE, int NTHR>
+__device__ __forceinline__ void finalize_body(int n, double *__restrict__ facc,
+                                              const int *__restrict__ off,
+                                              const int *__restrict__ rev,
+                                              const double *__restrict__ fbuf,
+                                              double *__restrict__ forces, int nparts,
+                                              const double *__restrict__ partials,
+                                              double *__restrict__ result,
+                                              unsigned long long *__restrict__ stats_acc,
+                                              unsigned long long *__restrict__ stats_out,
+                                              double (*s)[7] /* [NTHR][7] shared scratch */) {
+  if (MODE == 0) {
+    const int64_t m3 = 3 * (int64_t)n;
+    for (int64_t k = blockIdx.x * (int64_t)NTHR + threadIdx.x; k < m3;
+         k += (int64_t)gridDim.x * NTHR) {
+      forces[k] = __ldcg(facc + k) + 0.0;
+      facc[k] = 0.0;
+    }
+  } else {
+    for (int m = blockIdx.x * NTHR + threadIdx.x; m < n; m += gridDim.x * NTHR) {
+      double ix = 0.0, iy = 0.0, iz = 0.0, sx = 0.0, sy = 0.0, sz = 0.0;
+      for (int e = off[m]; e < off[m + 1]; ++e) {
+        const double *f = fbuf + 3 * (int64_t)__ldg(rev + e);
+        ix += __ldcg(f);
+        iy += __ldcg(f + 1);
+        iz += __ldcg(f + 2);
+        const double *g = fbuf + 3 * (int64_t)e;
+        sx += __ldcg(g);
+        sy += __ldcg(g + 1);
+        sz += __ldcg(g + 2);
+      }
+      forces[3 * (int64_t)m] = (ix - sx) + 0.0;
+      forces[3 * (int64_t)m + 1] = (iy - sy) + 0.0;
+      forces[3 * (int64_t)m + 2] = (iz - sz) + 0.0;
+    }
+  }
+  if (blockIdx.x == 0) {
+    double acc[7] = {0, 0, 0, 0, 0, 0, 0};
+    for (int b = threadIdx.x; b < nparts; b += NTHR)
+#pragma unroll
+      for (int q = 0; q < 7; ++q) acc[q] += __ldcg(partials + 8 * (int64_t)b + q);
+#pragma unroll
+    for (int q = 0; q < 7; ++q) s[threadIdx.x][q] = acc[q];
+    __syncthreads();
+    for (int h = NTHR / 2; h > 0; h >>= 1) {
+      if (threadIdx.x < h)
+#pragma unroll
+        for (int q = 0; q < 7; ++q) s[threadIdx.x][q] += s[threadIdx.x + h][q];
+      __syncthreads();
+    }
+    if (threadIdx.x < 7) result[threadIdx.x] = s[0][threadIdx.x] + 0.0;
+    if (threadIdx.x < 6) {
+      if (stats_out) stats_out[threadIdx.x] = __ldcg(stats_acc + threadIdx.x);
+      stats_acc[threadIdx.x] = 0ull;
+    }
   }
 }
 
@@ -465,58 +523,15 @@ __global__ void k_fill_lanes(const ChunkPlan plan, const int *__restrict__ sorte
 // ---------------------------------------------------------------------------
 
 template <int MODE>
-__global__ void k_finalize(int n, double *__restrict__ facc, const int *__restrict__ off,
+__global__ void __launch_bounds__(256) k_finalize(int n, double *__restrict__ facc, const int *__restrict__ off,
                            const int *__restrict__ rev, const double *__restrict__ fbuf,
                            double *__restrict__ forces, int nparts,
                            const double *__restrict__ partials, double *__restrict__ result,
                            unsigned long long *__restrict__ stats_acc,
                            unsigned long long *__restrict__ stats_out) {
-  if (MODE == 0) {
-    const int64_t m3 = 3 * (int64_t)n;
-    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < m3;
-         k += (int64_t)gridDim.x * blockDim.x) {
-      forces[k] = facc[k] + 0.0;
-      facc[k] = 0.0;
-    }
-  } else {
-    for (int m = blockIdx.x * blockDim.x + threadIdx.x; m < n; m += gridDim.x * blockDim.x) {
-      double ix = 0.0, iy = 0.0, iz = 0.0, sx = 0.0, sy = 0.0, sz = 0.0;
-      for (int e = off[m]; e < off[m + 1]; ++e) {
-        const double *f = fbuf + 3 * (int64_t)__ldg(rev + e);
-        ix += f[0];
-        iy += f[1];
-        iz += f[2];
-        const double *g = fbuf + 3 * (int64_t)e;
-        sx += g[0];
-        sy += g[1];
-        sz += g[2];
-      }
-      forces[3 * (int64_t)m] = (ix - sx) + 0.0;
-      forces[3 * (int64_t)m + 1] = (iy - sy) + 0.0;
-      forces[3 * (int64_t)m + 2] = (iz - sz) + 0.0;
-    }
-  }
-  if (blockIdx.x == 0) {
-    __shared__ double s[256][7];
-    double acc[7] = {0, 0, 0, 0, 0, 0, 0};
-    for (int b = threadIdx.x; b < nparts; b += blockDim.x)
-#pragma unroll
-      for (int q = 0; q < 7; ++q) acc[q] += partials[8 * (int64_t)b + q];
-#pragma unroll
-    for (int q = 0; q < 7; ++q) s[threadIdx.x][q] = acc[q];
-    __syncthreads();
-    for (int h = 128; h > 0; h >>= 1) {
-      if (threadIdx.x < h)
-#pragma unroll
-        for (int q = 0; q < 7; ++q) s[threadIdx.x][q] += s[threadIdx.x + h][q];
-      __syncthreads();
-    }
-    if (threadIdx.x < 7) result[threadIdx.x] = s[0][threadIdx.x] + 0.0;
-    if (threadIdx.x < 6) {
-      if (stats_out) stats_out[threadIdx.x] = stats_acc[threadIdx.x];
-      stats_acc[threadIdx.x] = 0ull;
-    }
-  }
+  __shared__ double s[256][7];
+  finalize_body<MODE, 256>(n, facc, off, rev, fbuf, forces, nparts, partials, result, stats_acc,
+                           stats_out, s);
 }
 
 }  // namespace tb
