@@ -443,21 +443,25 @@ def e2e_arm(args, B, state, table, nl, dev):
     hs = HostState()
     hs.positions, hs.species, hs.box = pos_h, sp_h, state.box
     variant = B.make_variant("B200", precision=args.precision, scatter=args.scatter)
+    # caller-owned pinned result buffers (compute(..., out=)): D2H by DMA
+    out = B.ForceEnergyResult(torch.empty((n, 3), dtype=torch.float64).pin_memory().numpy(),
+                              0.0, torch.empty(n, dtype=torch.float64).pin_memory().numpy(), {})
     for _ in range(3):
-        B.compute(hs, nl, table, variant)
+        B.compute(hs, nl, table, variant, out=out)
     k = max(10, min(args.steps, args.e2e_steps))
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     for _ in range(k):
-        res = B.compute(hs, nl, table, variant)
+        res = B.compute(hs, nl, table, variant, out=out)
     torch.cuda.synchronize()
     el = time.perf_counter() - t0
     assert np.isfinite(res.potential_energy)
     return {"value": n * k / el, "unit": UNIT, "steps": k,
             "h2d_bytes_per_step": n * 3 * 8 + n * 4,
             "d2h_bytes_per_step": n * 3 * 8 + n * 8 + 7 * 8 + 6 * 8,
-            "path": "paper_1710_00882_b200.compute(state, nl, params, variant), pinned host "
-                    "positions in, host forces/per-atom energy out"}
+            "path": "paper_1710_00882_b200.compute(state, nl, params, variant, out=pinned), "
+                    "pinned host positions+species in, pinned host forces/per-atom energy out, "
+                    "energy/virial/stats to host, wall clock per call (synchronous)"}
 
 
 def main():

@@ -88,12 +88,15 @@ def _species_i32(state, n):
     return sp
 
 
-def compute(state, nl, params, variant=None, threads=1):
+def compute(state, nl, params, variant=None, threads=1, out=None):
     """One E+F(+virial) evaluation (kernels.py:517-527).
 
     state.positions may be a numpy array (copied to the GPU inside the call)
     or a contiguous float64 CUDA tensor (used in place; forces then come back
-    as a CUDA tensor).  `threads` is accepted for signature compatibility."""
+    as a CUDA tensor).  `threads` is accepted for signature compatibility.
+    `out` (extension): a ForceEnergyResult whose forces / per_atom_energy
+    arrays are overwritten instead of allocating new ones (e.g. pinned host
+    buffers for a streaming driver); it is returned updated."""
     variant = variant or KernelVariant()
     ctx = nl.context
     r_cut = ctx.set_table(params)
@@ -104,7 +107,11 @@ def compute(state, nl, params, variant=None, threads=1):
         raise ConfigurationError(f"state has {n} atoms but the neighbor list {nl.natoms}")
     sp = _species_i32(state, n)
     on_device = not isinstance(pos, np.ndarray)
-    if on_device:
+    if out is not None:
+        forces, per_atom = out.forces, out.per_atom_energy
+        if tuple(forces.shape) != (n, 3) or tuple(per_atom.shape) != (n,):
+            raise ConfigurationError("out buffers do not match the number of atoms")
+    elif on_device:
         import torch
         forces = torch.empty((n, 3), dtype=torch.float64, device=pos.device)
         per_atom = torch.empty(n, dtype=torch.float64, device=pos.device)
@@ -124,6 +131,9 @@ def compute(state, nl, params, variant=None, threads=1):
           "packed_pairs": int(stats[1]), "live_pairs": int(stats[2]),
           "live_triplets": int(stats[3]), "taper_pairs": int(stats[4]),
           "taper_triplets": int(stats[5])}
+    if out is not None:
+        out.potential_energy, out.stats, out.virial = float(energy[0]), st, virial
+        return out
     return ForceEnergyResult(forces, float(energy[0]), per_atom, st, virial)
 
 
