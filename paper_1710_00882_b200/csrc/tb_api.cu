@@ -70,7 +70,7 @@ struct tb_context {
       cub_tmp, facc, stats_acc;
   int64_t facc_n = -1;
   ErrFlags *h_err = nullptr;      // pinned
-  double *h_small = nullptr;      // pinned scratch (16 doubles)
+  double *h_small = nullptr;      // pinned scratch (64 doubles)
   // kernel timing (tb_profile)
   bool profile = false;
   bool force_tile = false;
@@ -88,7 +88,7 @@ struct tb_nlist {
   int64_t entries = 0, max_row = 0;
   bool built = false;
   DevBuf offsets, nbr, rev, ref_pos, atom_cell, cell_count, cell_start, cell_atoms, row_count,
-      maxrow, nl_row, sorted_atoms, sort_keys, iota, lanes, hist;
+      maxrow, nl_row, sorted_atoms, sort_keys, iota, lanes, hist, cpos;
   bool rev_valid = false;
   int nchunks = 0;  // > 0: warp-chunk fast path available (max_row <= 32)
   int n_empty = 0;  // atoms with empty rows: sorted_atoms[0, n_empty)
@@ -209,7 +209,7 @@ extern "C" int tb_create(int device, tb_context **out) {
   }
   if (cudaStreamCreateWithFlags(&ctx->own, cudaStreamNonBlocking) != cudaSuccess ||
       cudaMallocHost(&ctx->h_err, sizeof(ErrFlags)) != cudaSuccess ||
-      cudaMallocHost(&ctx->h_small, 16 * sizeof(double)) != cudaSuccess) {
+      cudaMallocHost(&ctx->h_small, 64 * sizeof(double)) != cudaSuccess) {
     delete ctx;
     return TB_ERR_CUDA;
   }
@@ -360,7 +360,7 @@ extern "C" void tb_nlist_destroy(tb_nlist *nl) {
   DevBuf *bufs[] = {&nl->offsets, &nl->nbr, &nl->rev, &nl->ref_pos, &nl->atom_cell,
                     &nl->cell_count, &nl->cell_start, &nl->cell_atoms, &nl->row_count,
                     &nl->maxrow, &nl->nl_row, &nl->sorted_atoms, &nl->sort_keys,
-                    &nl->iota, &nl->lanes, &nl->hist};
+                    &nl->iota, &nl->lanes, &nl->hist, &nl->cpos};
   for (DevBuf *b : bufs) b->release();
   delete nl;
 }
@@ -496,26 +496,42 @@ extern "C" int tb_build_neighbors(tb_context *ctx, tb_nlist *nl, int64_t n,
                                                         nl->cell_count.as<int>(),
                                                         nl->cell_atoms.as<int>());
     CK(cudaGetLastError());
+    CK(nl->cpos.ensure(sizeof(double4) * N));
+    k_cell_gather<<<nblk(N, 256), 256, 0, ctx->stream>>>(N, d_pos, nl->cell_atoms.as<int>(),
+                                                          nl->cpos.as<double4>());
+    CK(cudaGetLastError());
     k_nl_scan<false><<<nblk(N, 128), 128, 0, ctx->stream>>>(
-        N, d_pos, g, bc * bc, nl->atom_cell.as<int>(), nl->cell_start.as<int>(),
+        N, nl->cpos.as<double4>(), g, bc * bc, nl->atom_cell.as<int>(), nl->cell_start.as<int>(),
         nl->cell_atoms.as<int>(), nl->row_count.as<int>(), nullptr, nullptr,
         nl->maxrow.as<int>(), nullptr);
     CK(cudaGetLastError());
   }
   rc = exclusive_scan(ctx, nl->row_count.as<int>(), nl->offsets.as<int>(), N + 1);
   if (rc) return rc;
-  int tail[2];
-  CK(cudaMemcpyAsync(&tail[0], nl->offsets.as<int>() + N, sizeof(int), cudaMemcpyDeviceToHost,
+  // row-length histogram for the warp chunks, read back with the totals in
+  // the build's single host synchronisation
+  CK(nl->hist.ensure(sizeof(int) * 34));
+  CK(cudaMemsetAsync(nl->hist.p, 0, sizeof(int) * 34, ctx->stream));
+  if (N) {
+    k_len_hist<<<std::min(nblk(N, 256), 296), 256, 0, ctx->stream>>>(N, nl->row_count.as<int>(),
+                                                                      nl->hist.as<int>());
+    CK(cudaGetLastError());
+  }
+  int *hm = reinterpret_cast<int *>(ctx->h_small);  // pinned: [entries, max_row, hist[34]]
+  CK(cudaMemcpyAsync(&hm[0], nl->offsets.as<int>() + N, sizeof(int), cudaMemcpyDeviceToHost,
                      ctx->stream));
-  CK(cudaMemcpyAsync(&tail[1], nl->maxrow.p, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaMemcpyAsync(&hm[1], nl->maxrow.p, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaMemcpyAsync(&hm[2], nl->hist.p, sizeof(int) * 34, cudaMemcpyDeviceToHost, ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
-  nl->entries = tail[0];
-  nl->max_row = tail[1];
+  nl->entries = hm[0];
+  nl->max_row = hm[1];
+  int hist[34];
+  memcpy(hist, hm + 2, sizeof(hist));
   CK(nl->nbr.ensure(sizeof(int) * std::max<int64_t>(nl->entries, 1)));
   CK(nl->nl_row.ensure(sizeof(int) * std::max<int64_t>(nl->entries, 1)));
   if (N) {
     k_nl_scan<true><<<nblk(N, 128), 128, 0, ctx->stream>>>(
-        N, d_pos, g, bc * bc, nl->atom_cell.as<int>(), nl->cell_start.as<int>(),
+        N, nl->cpos.as<double4>(), g, bc * bc, nl->atom_cell.as<int>(), nl->cell_start.as<int>(),
         nl->cell_atoms.as<int>(), nullptr, nl->offsets.as<int>(), nl->nbr.as<int>(), nullptr,
         nl->nl_row.as<int>());
     CK(cudaGetLastError());
@@ -530,7 +546,6 @@ extern "C" int tb_build_neighbors(tb_context *ctx, tb_nlist *nl, int64_t n,
     CK(nl->sorted_atoms.ensure(sizeof(int) * N));
     CK(nl->sort_keys.ensure(sizeof(int) * N));
     CK(nl->iota.ensure(sizeof(int) * N));
-    CK(nl->hist.ensure(sizeof(int) * 34));
     k_iota<<<nblk(N, 256), 256, 0, ctx->stream>>>(N, nl->iota.as<int>());
     CK(cudaGetLastError());
     size_t tmp = 0;
@@ -541,13 +556,6 @@ extern "C" int tb_build_neighbors(tb_context *ctx, tb_nlist *nl, int64_t n,
     CK(cub::DeviceRadixSort::SortPairs(ctx->cub_tmp.p, tmp, nl->row_count.as<int>(),
                                        nl->sort_keys.as<int>(), nl->iota.as<int>(),
                                        nl->sorted_atoms.as<int>(), N, 0, 6, ctx->stream));
-    CK(cudaMemsetAsync(nl->hist.p, 0, sizeof(int) * 34, ctx->stream));
-    k_len_hist<<<nblk(N, 256), 256, 0, ctx->stream>>>(N, nl->row_count.as<int>(),
-                                                       nl->hist.as<int>());
-    CK(cudaGetLastError());
-    int hist[34];
-    CK(cudaMemcpyAsync(hist, nl->hist.p, sizeof(hist), cudaMemcpyDeviceToHost, ctx->stream));
-    CK(cudaStreamSynchronize(ctx->stream));
     ChunkPlan plan;
     memset(&plan, 0, sizeof(plan));
     int start = hist[0], chunks = 0;

@@ -56,10 +56,14 @@ __device__ __forceinline__ double np_remainder(double a, double b) {
 // min_image on one axis (neighbor.py:36-43): d - L * rint(d / L).  d*invL
 // selects the same integer as the correctly rounded d/L except within a few
 // ulp of a half-integer; there the exact quotient is taken.
+__device__ __noinline__ double rint_quotient_exact(double d, double L) {
+  return rint(__ddiv_rn(d, L));  // out of line: never speculated into the hot path
+}
+
 __device__ __forceinline__ double min_image(double d, double L, double invL) {
   double y = __dmul_rn(d, invL);
   double q = rint(y);
-  if (0.5 - fabs(y - q) < 1e-9) q = rint(__ddiv_rn(d, L));
+  if (__builtin_expect(0.5 - fabs(y - q) < 1e-9, 0)) q = rint_quotient_exact(d, L);
   return __dsub_rn(d, __dmul_rn(L, q));
 }
 
@@ -179,57 +183,118 @@ __device__ __forceinline__ int stencil_axis(int c, int nc, int per, int out[3]) 
   return k;
 }
 
+// cell-sorted copy of the positions: slot -> {x, y, z, -} (one 32-byte load
+// per candidate in the stencil scan, contiguous within a cell)
+__global__ void k_cell_gather(int n, const double *__restrict__ pos,
+                              const int *__restrict__ cell_atoms, double4 *__restrict__ cpos) {
+  int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n) return;
+  const int i = cell_atoms[t];
+  cpos[t] = make_double4(__ldg(pos + 3 * (int64_t)i), __ldg(pos + 3 * (int64_t)i + 1),
+                         __ldg(pos + 3 * (int64_t)i + 2), 0.0);
+}
+
+// Threads walk atoms in cell order (neighbouring threads share stencil cells,
+// so candidate loads hit L1); for every (x,y) stencil pair the distinct z cells
+// are merged into contiguous runs of the cell-sorted arrays.
 template <bool FILL>
-__global__ void k_nl_scan(int n, const double *__restrict__ pos, Grid g, double bc2,
-                          const int *__restrict__ atom_cell, const int *__restrict__ cell_start,
-                          const int *__restrict__ cell_atoms, int *__restrict__ row_count,
-                          const int *__restrict__ offsets, int *__restrict__ nbr,
-                          int *__restrict__ max_row, int *__restrict__ nl_row) {
-  int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  double xi[3];
-  load3(pos, i, xi);
-  int id = atom_cell[i];
-  int c[3] = {id / (g.nc[1] * g.nc[2]), (id / g.nc[2]) % g.nc[1], id % g.nc[2]};
-  int sx[3], sy[3], sz[3];
-  int nx = stencil_axis(c[0], g.nc[0], g.box.per[0], sx);
-  int ny = stencil_axis(c[1], g.nc[1], g.box.per[1], sy);
-  int nz = stencil_axis(c[2], g.nc[2], g.box.per[2], sz);
+__global__ void __launch_bounds__(128) k_nl_scan(int n, const double4 *__restrict__ cpos, Grid g,
+                                                 double bc2, const int *__restrict__ atom_cell,
+                                                 const int *__restrict__ cell_start,
+                                                 const int *__restrict__ cell_atoms,
+                                                 int *__restrict__ row_count,
+                                                 const int *__restrict__ offsets,
+                                                 int *__restrict__ nbr, int *__restrict__ max_row,
+                                                 int *__restrict__ nl_row) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
   int cnt = 0;
-  int base = FILL ? offsets[i] : 0;
-  for (int a = 0; a < nx; ++a)
-    for (int b = 0; b < ny; ++b)
-      for (int q = 0; q < nz; ++q) {
-        int cid = (sx[a] * g.nc[1] + sy[b]) * g.nc[2] + sz[q];
-        int s1 = cell_start[cid + 1];
-        for (int s = cell_start[cid]; s < s1; ++s) {
-          int j = cell_atoms[s];
-          if (j == i) continue;
-          double xj[3], d[3];
-          load3(pos, j, xj);
-          double r2 = disp_r2(xi, xj, g.box, d);
-          if (r2 < bc2) {
-            if (FILL) nbr[base + cnt] = j;
-            cnt++;
+  if (t < n) {
+    const int i = cell_atoms[t];
+    const double4 pi = cpos[t];
+    const double xi[3] = {pi.x, pi.y, pi.z};
+    const int id = atom_cell[i];
+    const int c[3] = {id / (g.nc[1] * g.nc[2]), (id / g.nc[2]) % g.nc[1], id % g.nc[2]};
+    int sx[3], sy[3], sz[3], nx, ny, nz;
+    // distinct stencil cells per axis; periodic axes with >= 3 cells (the
+    // common case) without the generic de-duplication
+#pragma unroll
+    for (int ax = 0; ax < 3; ++ax) {
+      int *o = ax == 0 ? sx : (ax == 1 ? sy : sz);
+      int &k = ax == 0 ? nx : (ax == 1 ? ny : nz);
+      const int nc = g.nc[ax], cc = c[ax];
+      if (g.box.per[ax] && nc >= 3) {
+        o[0] = cc == 0 ? nc - 1 : cc - 1;
+        o[1] = cc;
+        o[2] = cc == nc - 1 ? 0 : cc + 1;
+        k = 3;
+      } else {
+        k = stencil_axis(cc, nc, g.box.per[ax], o);
+      }
+    }
+    // merge the distinct z cells into runs of consecutive ids
+    int zlo[3], zhi[3], nr = 0;
+    {
+      int zs[3] = {sz[0], nz > 1 ? sz[1] : 0, nz > 2 ? sz[2] : 0};
+#pragma unroll
+      for (int u = 1; u < 3; ++u)  // sort (<= 3 values)
+#pragma unroll
+        for (int v = 2; v > 0; --v)
+          if (v <= u && v < nz && zs[v - 1] > zs[v]) {
+            int tmp = zs[v];
+            zs[v] = zs[v - 1];
+            zs[v - 1] = tmp;
+          }
+#pragma unroll
+      for (int u = 0; u < 3; ++u) {
+        if (u >= nz) break;
+        if (nr > 0 && zs[u] == zhi[nr - 1] + 1) {
+          zhi[nr - 1] = zs[u];
+        } else {
+          zlo[nr] = zs[u];
+          zhi[nr] = zs[u];
+          ++nr;
+        }
+      }
+    }
+    const int base = FILL ? offsets[i] : 0;
+    for (int a = 0; a < nx; ++a)
+      for (int b = 0; b < ny; ++b) {
+        const int row = (sx[a] * g.nc[1] + sy[b]) * g.nc[2];
+        for (int r = 0; r < nr; ++r) {
+          const int s0 = cell_start[row + zlo[r]], s1 = cell_start[row + zhi[r] + 1];
+          for (int s = s0; s < s1; ++s) {
+            if (s == t) continue;
+            const double4 pj = cpos[s];
+            const double xj[3] = {pj.x, pj.y, pj.z};
+            double d[3];
+            const double r2 = disp_r2(xi, xj, g.box, d);
+            if (r2 < bc2) {
+              if (FILL) nbr[base + cnt] = cell_atoms[s];
+              cnt++;
+            }
           }
         }
       }
-  if (FILL) {
-    for (int u = 0; u < cnt; ++u) nl_row[base + u] = i;
-    // rows ascending by j (neighbor.py:210-212); rows are short
-    int *row = nbr + base;
-    for (int u = 1; u < cnt; ++u) {
-      int v = row[u];
-      int w = u - 1;
-      while (w >= 0 && row[w] > v) {
-        row[w + 1] = row[w];
-        --w;
+    if (FILL) {
+      for (int u = 0; u < cnt; ++u) nl_row[base + u] = i;
+      // rows ascending by j (neighbor.py:210-212); rows are short
+      int *rowp = nbr + base;
+      for (int u = 1; u < cnt; ++u) {
+        int v = rowp[u];
+        int w = u - 1;
+        while (w >= 0 && rowp[w] > v) {
+          rowp[w + 1] = rowp[w];
+          --w;
+        }
+        rowp[w + 1] = v;
       }
-      row[w + 1] = v;
+    } else {
+      row_count[i] = cnt;
     }
-  } else {
-    row_count[i] = cnt;
-    atomicMax(max_row, cnt);
+  }
+  if (!FILL) {
+    int m = __reduce_max_sync(0xffffffffu, cnt);
+    if ((threadIdx.x & 31) == 0 && m) atomicMax(max_row, m);
   }
 }
 

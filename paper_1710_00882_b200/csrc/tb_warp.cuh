@@ -494,9 +494,15 @@ __global__ void k_iota(int n, int *__restrict__ out) {
   if (i < n) out[i] = i;
 }
 
+// histogram of row lengths (block-private bins, one global atomic per bin)
 __global__ void k_len_hist(int n, const int *__restrict__ len, int *__restrict__ hist) {
-  int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n) atomicAdd(hist + min(len[i], 33), 1);
+  __shared__ int h[34];
+  if (threadIdx.x < 34) h[threadIdx.x] = 0;
+  __syncthreads();
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    atomicAdd(h + min(len[i], 33), 1);
+  __syncthreads();
+  if (threadIdx.x < 34 && h[threadIdx.x]) atomicAdd(hist + threadIdx.x, h[threadIdx.x]);
 }
 
 // one warp per chunk: lane -> {entry, i, j, L} (entry -1: idle lane)
