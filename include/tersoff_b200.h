@@ -146,7 +146,8 @@ int tb_profile_read(tb_context *ctx, double *total_ms, int64_t *launches);
 /* One velocity-Verlet step on device buffers (positions, velocities, forces
  * updated in place; mass per atom in amu, v += 0.5 dt accel F / m).  Rebuilds the list on the skin/2
  * trigger or when `force_rebuild` is set; *rebuilt (host, may be NULL)
- * reports it.  d_result as in tb_compute_device. */
+ * reports it.  d_result (8 doubles) as in tb_compute_device plus the kinetic
+ * energy 0.5 sum m v^2 / accel in d_result[7] (system.py:129-134). */
 int tb_md_step(tb_context *ctx, tb_nlist *nl, int64_t n, double *d_positions,
                double *d_velocities, double *d_forces, const double *d_mass,
                const int32_t *d_species, const double *box, const int32_t *periodic,

@@ -67,7 +67,7 @@ struct tb_context {
   std::vector<double> pair_mat, trip_mat;
   // scratch
   DevBuf pos, species, forces, per_atom, result, stats, partials, fbuf, errf, drift, bounds,
-      cub_tmp, facc, stats_acc;
+      cub_tmp, facc, stats_acc, ke_part;
   int64_t facc_n = -1;
   ErrFlags *h_err = nullptr;      // pinned
   double *h_small = nullptr;      // pinned scratch (64 doubles)
@@ -223,7 +223,7 @@ extern "C" void tb_destroy(tb_context *ctx) {
   cudaSetDevice(ctx->device);
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   DevBuf *bufs[] = {&ctx->pos, &ctx->species, &ctx->forces, &ctx->per_atom, &ctx->result,
-                    &ctx->stats, &ctx->partials, &ctx->fbuf, &ctx->facc, &ctx->stats_acc, &ctx->errf,
+                    &ctx->stats, &ctx->partials, &ctx->fbuf, &ctx->facc, &ctx->stats_acc, &ctx->ke_part, &ctx->errf,
                     &ctx->drift, &ctx->bounds, &ctx->cub_tmp};
   for (DevBuf *b : bufs) b->release();
   for (auto *v : {&ctx->ev_used, &ctx->ev_free})
@@ -1080,5 +1080,12 @@ extern "C" int tb_md_step(tb_context *ctx, tb_nlist *nl, int64_t n, double *d_po
     k_kick<<<nblk(n, 256), 256, 0, ctx->stream>>>((int)n, d_velocities, d_forces, d_mass, half);
     CK(cudaGetLastError());
   }
+  // kinetic energy 0.5 sum m v^2 / accel (system.py:129-134) -> d_result[7]
+  const int kb = std::max(1, std::min(nblk(n, 256), 4 * 148));
+  CK(ctx->ke_part.ensure(sizeof(double) * kb));
+  k_kinetic<<<kb, 256, 0, ctx->stream>>>((int)n, d_velocities, d_mass, ctx->ke_part.as<double>());
+  k_kinetic_sum<<<1, 256, 0, ctx->stream>>>(kb, ctx->ke_part.as<double>(), 0.5 / accel,
+                                            d_result + 7);
+  CK(cudaGetLastError());
   return TB_OK;
 }

@@ -873,4 +873,37 @@ __global__ void __launch_bounds__(256) k_fma_peak(T *out, int iters, T b, T c) {
   if (s == T(-12345)) out[blockIdx.x] = s;  // keep the chains alive
 }
 
+// per-block partial sums of m v^2 (fixed grid: deterministic)
+__global__ void k_kinetic(int n, const double *__restrict__ vel, const double *__restrict__ mass,
+                          double *__restrict__ part) {
+  __shared__ double s[8];
+  double acc = 0.0;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const double vx = vel[3 * (int64_t)i], vy = vel[3 * (int64_t)i + 1], vz = vel[3 * (int64_t)i + 2];
+    acc += mass[i] * ((vx * vx + vy * vy) + vz * vz);
+  }
+  acc = warp_sum(acc);
+  if ((threadIdx.x & 31) == 0) s[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += s[w];
+    part[blockIdx.x] = t;
+  }
+}
+
+__global__ void k_kinetic_sum(int nb, const double *__restrict__ part, double scale,
+                              double *__restrict__ out) {
+  __shared__ double s[256];
+  double acc = 0.0;
+  for (int b = threadIdx.x; b < nb; b += 256) acc += part[b];
+  s[threadIdx.x] = acc;
+  __syncthreads();
+  for (int h = 128; h > 0; h >>= 1) {
+    if (threadIdx.x < h) s[threadIdx.x] += s[threadIdx.x + h];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *out = scale * s[0];
+}
+
 }  // namespace tb
