@@ -95,6 +95,14 @@ void tb_nlist_destroy(tb_nlist *nl);
 int tb_build_neighbors(tb_context *ctx, tb_nlist *nl, int64_t n, const double *positions,
                        const double *box, const int32_t *periodic, double r_cut,
                        double skin);
+/* Domain-decomposed variant: atoms [0, n_owned) are owned, [n_owned, n) are
+ * ghosts (halo copies, unshifted coordinates).  Only owned atoms get rows, so
+ * only their energy terms are evaluated; ghosts appear as neighbours j, k.
+ * The pair set of every owned row equals the single-domain list's. */
+int tb_build_neighbors_owned(tb_context *ctx, tb_nlist *nl, int64_t n, int64_t n_owned,
+                             const double *positions, const double *box,
+                             const int32_t *periodic, double r_cut, double skin);
+
 /* number of list entries (sum of row lengths) and the longest row */
 int tb_nlist_info(const tb_nlist *nl, int64_t *n_atoms, int64_t *n_entries,
                   int64_t *max_row);

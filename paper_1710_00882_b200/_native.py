@@ -40,6 +40,7 @@ SIGNATURES = {
     "tb_nlist_create": (_I, [_P, ctypes.POINTER(_P)]),
     "tb_nlist_destroy": (None, [_P]),
     "tb_build_neighbors": (_I, [_P, _P, _I64, _P, _P, _P, _D, _D]),
+    "tb_build_neighbors_owned": (_I, [_P, _P, _I64, _I64, _P, _P, _P, _D, _D]),
     "tb_nlist_info": (_I, [_P, _P, _P, _P]),
     "tb_nlist_export": (_I, [_P, _P, _P, _P]),
     "tb_needs_rebuild": (_I, [_P, _P, _P, _P]),

@@ -386,6 +386,14 @@ static int build_rev(tb_context *ctx, tb_nlist *nl) {
 extern "C" int tb_build_neighbors(tb_context *ctx, tb_nlist *nl, int64_t n,
                                   const double *positions, const double *box,
                                   const int32_t *periodic, double r_cut, double skin) {
+  return tb_build_neighbors_owned(ctx, nl, n, n, positions, box, periodic, r_cut, skin);
+}
+
+extern "C" int tb_build_neighbors_owned(tb_context *ctx, tb_nlist *nl, int64_t n,
+                                        int64_t n_owned, const double *positions,
+                                        const double *box, const int32_t *periodic,
+                                        double r_cut, double skin) {
+  if (n_owned < 0 || n_owned > n) return fail(ctx, TB_ERR_ARG, "n_owned outside [0, n]");
   if (!ctx || !nl || !box || !periodic || (n && !positions))
     return fail(ctx, TB_ERR_ARG, "null argument");
   if (n > INT_MAX / 2) return fail(ctx, TB_ERR_ARG, "too many atoms (%lld)", (long long)n);
@@ -501,7 +509,7 @@ extern "C" int tb_build_neighbors(tb_context *ctx, tb_nlist *nl, int64_t n,
                                                           nl->cpos.as<double4>());
     CK(cudaGetLastError());
     k_nl_scan<false><<<nblk(N, 128), 128, 0, ctx->stream>>>(
-        N, nl->cpos.as<double4>(), g, bc * bc, nl->atom_cell.as<int>(), nl->cell_start.as<int>(),
+        N, (int)n_owned, nl->cpos.as<double4>(), g, bc * bc, nl->atom_cell.as<int>(), nl->cell_start.as<int>(),
         nl->cell_atoms.as<int>(), nl->row_count.as<int>(), nullptr, nullptr,
         nl->maxrow.as<int>(), nullptr);
     CK(cudaGetLastError());
@@ -531,7 +539,7 @@ extern "C" int tb_build_neighbors(tb_context *ctx, tb_nlist *nl, int64_t n,
   CK(nl->nl_row.ensure(sizeof(int) * std::max<int64_t>(nl->entries, 1)));
   if (N) {
     k_nl_scan<true><<<nblk(N, 128), 128, 0, ctx->stream>>>(
-        N, nl->cpos.as<double4>(), g, bc * bc, nl->atom_cell.as<int>(), nl->cell_start.as<int>(),
+        N, (int)n_owned, nl->cpos.as<double4>(), g, bc * bc, nl->atom_cell.as<int>(), nl->cell_start.as<int>(),
         nl->cell_atoms.as<int>(), nullptr, nl->offsets.as<int>(), nl->nbr.as<int>(), nullptr,
         nl->nl_row.as<int>());
     CK(cudaGetLastError());

@@ -198,7 +198,7 @@ __global__ void k_cell_gather(int n, const double *__restrict__ pos,
 // so candidate loads hit L1); for every (x,y) stencil pair the distinct z cells
 // are merged into contiguous runs of the cell-sorted arrays.
 template <bool FILL>
-__global__ void __launch_bounds__(128) k_nl_scan(int n, const double4 *__restrict__ cpos, Grid g,
+__global__ void __launch_bounds__(128) k_nl_scan(int n, int n_owned, const double4 *__restrict__ cpos, Grid g,
                                                  double bc2, const int *__restrict__ atom_cell,
                                                  const int *__restrict__ cell_start,
                                                  const int *__restrict__ cell_atoms,
@@ -208,7 +208,7 @@ __global__ void __launch_bounds__(128) k_nl_scan(int n, const double4 *__restric
                                                  int *__restrict__ nl_row) {
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
   int cnt = 0;
-  if (t < n) {
+  if (t < n && cell_atoms[t] < n_owned) {  // ghosts (i >= n_owned) get empty rows
     const int i = cell_atoms[t];
     const double4 pi = cpos[t];
     const double xi[3] = {pi.x, pi.y, pi.z};
@@ -291,6 +291,8 @@ __global__ void __launch_bounds__(128) k_nl_scan(int n, const double4 *__restric
     } else {
       row_count[i] = cnt;
     }
+  } else if (!FILL && t < n) {
+    row_count[cell_atoms[t]] = 0;
   }
   if (!FILL) {
     int m = __reduce_max_sync(0xffffffffu, cnt);
