@@ -26,8 +26,6 @@ The per-rank force engine is pluggable (`engine.rebuild`, `engine.compute`):
 B200Engine drives the CUDA kernels; the CPU tests plug in the oracle.
 """
 
-import math
-
 import numpy as np
 import torch
 import torch.distributed as dist
@@ -111,11 +109,19 @@ def _padded(shape):
     return (max(shape[0], 1),) + tuple(shape[1:])
 
 
+_COMM_DEVICE = {}  # process-wide override: exchange through this device (e.g. "cpu" for gloo)
+
+
 def _exchange(sends, recv_shapes, dtype, device, left, right):
     """Two-way P2P with the left and right ranks.  sends: (to_left, to_right)
     tensors; recv_shapes: (from_left, from_right) row counts x width.  Message
     order per peer is fixed (to_left before to_right), which also resolves the
     two-rank ring where left == right.  Returns (from_left, from_right)."""
+    comm = _COMM_DEVICE.get("device")
+    if comm is not None and str(comm) != str(device):
+        fl, fr = _exchange(tuple(t.to(comm) for t in sends), recv_shapes, dtype, comm, left,
+                           right)
+        return fl.to(device), fr.to(device)
     bufs = []
     for t in sends:
         t = t.contiguous()
@@ -257,7 +263,13 @@ class DecomposedForceField:
             # from_left carries forces on my left-column atoms (rank-1's right ghosts)
             f.index_add_(0, dom._idl, back_from_left)
             f.index_add_(0, dom._idr, back_from_right)
-            dist.all_reduce(result)
+            comm = _COMM_DEVICE.get("device")
+            if comm is not None and str(comm) != str(self.device):
+                r = result.to(comm)
+                dist.all_reduce(r)
+                result = r.to(self.device)
+            else:
+                dist.all_reduce(result)
         return f, result
 
 
@@ -296,9 +308,16 @@ class B200Engine:
         return forces, result[:7]
 
 
+def set_comm_device(device):
+    """Route the P2P/all-reduce traffic through `device` (e.g. "cpu" when the
+    process group is gloo but the domain lives on a GPU)."""
+    _COMM_DEVICE["device"] = device
+
+
 def gather_global(dom, forces_owned, n_global, device):
     """All-gather owned forces into the global atom order (tests/diagnostics)."""
-    out = torch.zeros((n_global, 3), dtype=torch.float64, device=device)
-    out[torch.as_tensor(dom.ids, dtype=torch.long, device=device)] = forces_owned
+    comm = _COMM_DEVICE.get("device") or device
+    out = torch.zeros((n_global, 3), dtype=torch.float64, device=comm)
+    out[torch.as_tensor(dom.ids, dtype=torch.long, device=comm)] = forces_owned.to(comm)
     dist.all_reduce(out)
-    return out
+    return out.to(device)
