@@ -220,10 +220,126 @@ def reference_arm(args):
     print(json.dumps(line, default=_jsonable), flush=True)
 
 
+def gpu_arm_decomposed(args):
+    """N > 1: slab decomposition (decomp.py) with NCCL P2P halos, weak scaling:
+    every GPU owns a 20^3-cell (64,000-atom) slab of a (20N x 20 x 20)-cell Si
+    crystal (config 2 per GPU, same seeds).  A step = forward halo + Tersoff
+    evaluation on [owned | ghosts] + reverse ghost forces + all-reduce of
+    [E, W6]; device-timed (CUDA events) per rank, max over ranks."""
+    import ctypes
+    import torch
+    import torch.distributed as dist
+    ws, rank, local = dist_setup()
+    local = local % torch.cuda.device_count()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    from paper_1710_00882_b200 import _native, decomp, structures
+    backend = os.environ.get("BENCH_DIST_BACKEND", "nccl")  # gloo: single-GPU smoke test only
+    if backend == "nccl":
+        dist.init_process_group("nccl", device_id=dev)
+    else:
+        dist.init_process_group(backend)
+        decomp.set_comm_device("cpu")
+    from paper_1710_00882_b200.paramfile import builtin_params
+    cells = (20 * ws, 20, 20)
+    st = structures.displace(structures.gen_diamond(cells, 5.431), 0.1, 1002)
+    table = builtin_params("Si")
+    n_total = st.natoms
+    stream = torch.cuda.Stream(device=dev)
+    torch.cuda.set_stream(stream)
+    d = decomp.SlabDecomposition(st.box.lengths, st.box.periodic, table.r_cut + 0.3, ws)
+    dom = decomp.scatter_state(d, st, rank, dev)
+    eng = decomp.B200Engine(table, 0.3, device=local, precision=args.precision,
+                            scatter=args.scatter)
+    ff = decomp.DecomposedForceField(d, st.box, eng, rank, ws, dev)
+    dom = ff.rebuild(dom)
+    for _ in range(max(3, args.warmup)):
+        f, res = ff(dom)
+    torch.cuda.synchronize()
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    k = args.steps
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(k)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(k)]
+    sampler = ClockSampler(local)
+    dist.barrier()
+    torch.cuda.synchronize()
+    with sampler:
+        for s_ in range(k):
+            flush.zero_()
+            starts[s_].record(stream)
+            f, res = ff(dom)
+            ends[s_].record(stream)
+        torch.cuda.synchronize()
+    t_local = sum(a.elapsed_time(b) for a, b in zip(starts, ends)) / 1e3
+    comm = "cpu" if backend != "nccl" else dev
+    t = torch.tensor([t_local], dtype=torch.float64, device=comm)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    t_max = float(t[0])
+    value = n_total * k / t_max
+    energy = float(res[0])
+    # kernel share on this rank
+    lib, ctx = eng.ctx.lib, eng.ctx
+    lib.tb_profile(ctx.handle, 1)
+    for _ in range(min(k, 100)):
+        flush.zero_()
+        f, res = ff(dom)
+    torch.cuda.synchronize()
+    lib.tb_profile(ctx.handle, 0)
+    tot, cnt = ctypes.c_double(), ctypes.c_int64()
+    ctx.check(lib.tb_profile_read(ctx.handle, ctypes.byref(tot), ctypes.byref(cnt)))
+    kern_ms = tot.value / max(cnt.value, 1)
+    # e2e: owned positions from pinned host memory each step, forces back
+    pos_h = torch.empty(tuple(dom.pos.shape), dtype=torch.float64).pin_memory()
+    pos_h.copy_(dom.pos)
+    f_h = torch.empty(tuple(dom.pos.shape), dtype=torch.float64).pin_memory()
+    ke = max(10, min(k, args.e2e_steps))
+    dist.barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(ke):
+        dom.pos.copy_(pos_h, non_blocking=True)
+        f, res = ff(dom)
+        f_h.copy_(f, non_blocking=True)
+        e_host = float(res[0])
+    torch.cuda.synchronize()
+    te = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=comm)
+    dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": k,
+        "warmup": args.warmup, "ms_per_step": t_max * 1e3 / k, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64" if args.precision == "double" else "f32/f64", "data": "synthetic",
+        "config": {"workload": f"config 2 per GPU, weak scaling: {cells[0]}x{cells[1]}x{cells[2]}"
+                               f"-cell Si diamond ({n_total} atoms), slab decomposition along x, "
+                               f"NCCL P2P halo + reverse forces + all-reduce per step",
+                   "atoms": n_total, "atoms_per_gpu": n_total // ws,
+                   "precision": args.precision, "scatter": args.scatter,
+                   "parallelism": f"spatial slabs x{ws}",
+                   "l2": "flushed between timed steps (256 MiB write)",
+                   "launch": "eager (Python host loop, NCCL batch_isend_irecv)"},
+        "e2e": {"value": n_total * ke / float(te[0]), "unit": UNIT, "steps": ke,
+                "h2d_bytes_per_step": int(dom.pos.numel() * 8),
+                "d2h_bytes_per_step": int(dom.pos.numel() * 8 + 8),
+                "path": "decomp.DecomposedForceField per rank, pinned host positions in, "
+                        "forces out, energy to host"},
+        "gpu_launches": 2 * k,
+        "roofline": {"bound": "fp64" if args.precision == "double" else "fp32",
+                     "kernel_ms_rank0": kern_ms, "achieved": None, "peak": None,
+                     "unit": "TFLOP/s", "frac": None, "traffic": None},
+        "clocks": sampler.summary(), "energy_eV": energy,
+    }
+    if rank == 0:
+        print(json.dumps(line, default=_jsonable), flush=True)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
 def gpu_arm(args):
     import ctypes
     import torch
     ws, rank, local = dist_setup()
+    if ws > 1 and not args.replicas:
+        return gpu_arm_decomposed(args)
     dev = local if ws > 1 else 0
     torch.cuda.set_device(dev)
     if ws > 1:
@@ -478,6 +594,8 @@ def main():
     ap.add_argument("--cpu-budget", type=float, default=12.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-extras", dest="extras", action="store_false")
+    ap.add_argument("--replicas", action="store_true",
+                    help="N>1: independent replicas instead of the slab decomposition")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

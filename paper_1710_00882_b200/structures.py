@@ -30,19 +30,21 @@ MASSES = {"C": 12.011, "Si": 28.0855, "Ge": 72.63}  # system.py:24
 
 
 def _lattice(cells, a):
-    cells = int(cells)
-    if cells < 1:
+    """cells: int (cubic) or (nx, ny, nz) conventional cells."""
+    nc = (int(cells),) * 3 if np.isscalar(cells) else tuple(int(c) for c in cells)
+    if min(nc) < 1:
         raise ValueError(f"need at least 1 cell, got {cells}")
-    origins = np.stack(np.meshgrid(*[np.arange(cells)] * 3, indexing="ij"),
+    origins = np.stack(np.meshgrid(*[np.arange(c) for c in nc], indexing="ij"),
                        -1).reshape(-1, 3)
     frac = (origins[:, None, :] + _DIAMOND_BASIS[None, :, :]).reshape(-1, 3)
-    return frac * a, cells * a
+    return frac * a, np.array(nc, dtype=np.float64) * a
 
 
 def gen_diamond(cells, a=5.431, symbol="Si"):
-    """Periodic diamond-cubic crystal, 8 atoms per conventional cell."""
+    """Periodic diamond-cubic crystal, 8 atoms per conventional cell; cells is
+    an int (cubic box) or (nx, ny, nz) (slabs stacked along x for weak scaling)."""
     pos, L = _lattice(cells, a)
-    box = SimulationBox([L, L, L], periodic=(True, True, True))
+    box = SimulationBox(L, periodic=(True, True, True))
     return SimulationState(pos, box, species=np.zeros(len(pos), np.int64),
                            masses=np.array([MASSES[symbol]]), symbols=(symbol,))
 
@@ -51,7 +53,7 @@ def gen_zincblende(cells, a=4.359, symbols=("Si", "C")):
     """3C-SiC: species 0 on fcc sites, species 1 on fcc + (1/4,1/4,1/4) a."""
     pos, L = _lattice(cells, a)
     sp = np.tile(np.array([0, 0, 0, 0, 1, 1, 1, 1], np.int64), len(pos) // 8)
-    box = SimulationBox([L, L, L], periodic=(True, True, True))
+    box = SimulationBox(L, periodic=(True, True, True))
     return SimulationState(pos, box, species=sp,
                            masses=np.array([MASSES[s] for s in symbols]),
                            symbols=tuple(symbols))
