@@ -185,10 +185,24 @@ __device__ __forceinline__ void chunk_body(const KArgs &a, const WArgs &w, const
 
   // ---- phase 1: zeta (and the angular cache) ----
   T zeta = T(0);
+  // only live partners of the row contribute (a dead b has f_C = dzeta = 0);
+  // lanes iterate their own row's live mask (the table is in shared memory,
+  // so no warp-uniform trip count is needed)
+  // (LC > 0: the partners are the fixed rotation pos+1..pos+L-1 and the loops
+  // unroll; a dead partner has f_C = dzeta = 0 and contributes exactly 0)
+  const unsigned rowmask = (L >= 32 ? 0xffffffffu : ((1u << L) - 1u)) << first;
+  const unsigned partners = live ? (lmask & rowmask & ~(1u << lane)) : 0u;
+  unsigned m = partners;
+  int q = 0;
 #pragma unroll
-  for (int q = 1; q < L; ++q) {
-    const int src = first + (pos + q >= L ? pos + q - L : pos + q);
-    if (!live) continue;
+  for (int it = 1; LC > 0 ? (live && it < LC) : m != 0; ++it, ++q) {
+    int src;
+    if (LC > 0) {
+      src = first + (pos + it >= L ? pos + it - L : pos + it);
+    } else {
+      src = __ffs(m) - 1;
+      m &= m - 1;
+    }
     const T2 bxy = tb.exy[src], bzr = tb.ezr[src], bfc = tb.fc[src];
     const int sb = S > 1 ? tb.sp[src] : 0;
     const TripP<T> &tp = tab.trip[(si * S + sj) * S + sb];
@@ -196,10 +210,10 @@ __device__ __forceinline__ void chunk_body(const KArgs &a, const WArgs &w, const
     cost = fmin(T(1), fmax(T(-1), cost));
     T g, dg;
     angular(cost, tp, g, dg);
-    if (q <= QCAP) {
-      s_cache[q - 1][0][lane] = cost;
-      s_cache[q - 1][1][lane] = g;
-      s_cache[q - 1][2][lane] = dg;
+    if (q < QCAP) {
+      s_cache[q][0][lane] = cost;
+      s_cache[q][1][lane] = g;
+      s_cache[q][2][lane] = dg;
     }
     const T f = (S > 1 && sj == 1) ? bfc.y : bfc.x;  // f_C(r_b) with entry (i, a, b)
     if (pair_live && f != T(0)) {
@@ -234,10 +248,17 @@ __device__ __forceinline__ void chunk_body(const KArgs &a, const WArgs &w, const
 
   // ---- phase 2: force on this neighbour from the terms centred on i ----
   T Sal = T(0), Sc = T(0), Sbx = T(0), Sby = T(0), Sbz = T(0);
+  m = partners;
+  q = 0;
 #pragma unroll
-  for (int q = 1; q < L; ++q) {
-    const int src = first + (pos + q >= L ? pos + q - L : pos + q);
-    if (!live) continue;
+  for (int it = 1; LC > 0 ? (live && it < LC) : m != 0; ++it, ++q) {
+    int src;
+    if (LC > 0) {
+      src = first + (pos + it >= L ? pos + it - L : pos + it);
+    } else {
+      src = __ffs(m) - 1;
+      m &= m - 1;
+    }
     const T dzb = tb.dz[src];
     const T2 bfc = tb.fc[src];
     const int sb = S > 1 ? tb.sp[src] : 0;
@@ -251,10 +272,10 @@ __device__ __forceinline__ void chunk_body(const KArgs &a, const WArgs &w, const
     const T2 bxy = tb.exy[src], bzr = tb.ezr[src];
     const T rb = bzr.y;
     T cost, g, dg;
-    if (q <= QCAP) {
-      cost = s_cache[q - 1][0][lane];
-      g = s_cache[q - 1][1][lane];
-      dg = s_cache[q - 1][2][lane];
+    if (q < QCAP) {
+      cost = s_cache[q][0][lane];
+      g = s_cache[q][1][lane];
+      dg = s_cache[q][2][lane];
     } else {
       cost = ex * bxy.x + ey * bxy.y + ez * bzr.x;
       cost = fmin(T(1), fmax(T(-1), cost));
@@ -439,11 +460,10 @@ __global__ void __launch_bounds__(WNT, TB_WARP_MINB)
     cp_async_wait<1>();  // this lane's gathers for the current chunk have landed
     const WStage &stg = s_stage[wid][buf];
     const int Ldyn = __shfl_sync(0xffffffffu, cur.w, 0);
+    // short rows (diamond: 4): fixed rotation, unrolled; longer rows: live masks
     switch (Ldyn) {
       case 4: chunk_body<T, S, LAM3, MODE, ST, 4>(a, w, tab, s_cache[wid], s_tb[wid], lane, cur, stg, Ldyn, A); break;
       case 5: chunk_body<T, S, LAM3, MODE, ST, 5>(a, w, tab, s_cache[wid], s_tb[wid], lane, cur, stg, Ldyn, A); break;
-      case 3: chunk_body<T, S, LAM3, MODE, ST, 3>(a, w, tab, s_cache[wid], s_tb[wid], lane, cur, stg, Ldyn, A); break;
-      case 6: chunk_body<T, S, LAM3, MODE, ST, 6>(a, w, tab, s_cache[wid], s_tb[wid], lane, cur, stg, Ldyn, A); break;
       default: chunk_body<T, S, LAM3, MODE, ST, 0>(a, w, tab, s_cache[wid], s_tb[wid], lane, cur, stg, Ldyn, A);
     }
     __syncwarp();  // the stage and the lane table are rewritten next iteration
