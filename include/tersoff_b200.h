@@ -135,7 +135,10 @@ int tb_compute(tb_context *ctx, const tb_nlist *nl, const double *positions,
  * graph capture: all pointers are DEVICE pointers; `result` receives
  * [energy, virial(6)] as 7 doubles; `dstats` TB_NSTATS uint64 (may be NULL).
  * Does not synchronise; validation errors are latched on the device and
- * reported by the next tb_check_errors(). */
+ * reported by the next tb_check_errors().  With two or more species the
+ * first call after a build derives a species-pair compute filter from
+ * d_species (one host synchronisation); the species array must not change
+ * in place while the list is in use (pass a different pointer instead). */
 int tb_compute_device(tb_context *ctx, const tb_nlist *nl, const double *d_positions,
                       const int32_t *d_species, double r_cut, int precision, int scatter,
                       double *d_forces, double *d_per_atom, double *d_result,

@@ -66,7 +66,7 @@ struct tb_context {
   double r_cut = 0.0;
   std::vector<double> pair_mat, trip_mat;
   // scratch
-  DevBuf pos, species, forces, per_atom, result, stats, partials, fbuf, errf, drift, bounds,
+  DevBuf pos, species, forces, per_atom, result, stats, partials, errf, drift, bounds,
       cub_tmp, facc, stats_acc, ke_part;
   int64_t facc_n = -1;
   ErrFlags *h_err = nullptr;      // pinned
@@ -75,6 +75,8 @@ struct tb_context {
   bool profile = false;
   bool force_tile = false;
   bool warp_per_chunk = getenv("TB_WARP_PER_CHUNK") != nullptr;
+  bool no_filter = getenv("TB_NO_FILTER") != nullptr;  // disable the species-pair compute filter
+  std::vector<int> last_species;  // host species of the last tb_compute (filter validity)
   int last_blocks = 0;  // grid of the last Tersoff launch (partials to reduce)  // tb_set_option(TB_OPT_TILE_KERNEL): general tile kernel only
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_used, ev_free;
 };
@@ -88,7 +90,11 @@ struct tb_nlist {
   int64_t entries = 0, max_row = 0;
   bool built = false;
   DevBuf offsets, nbr, rev, ref_pos, atom_cell, cell_count, cell_start, cell_atoms, row_count,
-      maxrow, nl_row, sorted_atoms, sort_keys, iota, lanes, hist, cpos;
+      maxrow, nl_row, sorted_atoms, sort_keys, iota, lanes, hist, cpos, crow, coff, centry;
+  bool filtered = false;                 // chunks built from the species-pair filter
+  DevBuf fbuf;                           // gather mode: per-entry force pieces
+  bool fbuf_zero = false;                // entries without lanes hold zeros
+  const int *filter_species = nullptr;   // species array the filter was built for
   bool rev_valid = false;
   int nchunks = 0;  // > 0: warp-chunk fast path available (max_row <= 32)
   int n_empty = 0;  // atoms with empty rows: sorted_atoms[0, n_empty)
@@ -223,7 +229,7 @@ extern "C" void tb_destroy(tb_context *ctx) {
   cudaSetDevice(ctx->device);
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   DevBuf *bufs[] = {&ctx->pos, &ctx->species, &ctx->forces, &ctx->per_atom, &ctx->result,
-                    &ctx->stats, &ctx->partials, &ctx->fbuf, &ctx->facc, &ctx->stats_acc, &ctx->ke_part, &ctx->errf,
+                    &ctx->stats, &ctx->partials, &ctx->facc, &ctx->stats_acc, &ctx->ke_part, &ctx->errf,
                     &ctx->drift, &ctx->bounds, &ctx->cub_tmp};
   for (DevBuf *b : bufs) b->release();
   for (auto *v : {&ctx->ev_used, &ctx->ev_free})
@@ -360,7 +366,8 @@ extern "C" void tb_nlist_destroy(tb_nlist *nl) {
   DevBuf *bufs[] = {&nl->offsets, &nl->nbr, &nl->rev, &nl->ref_pos, &nl->atom_cell,
                     &nl->cell_count, &nl->cell_start, &nl->cell_atoms, &nl->row_count,
                     &nl->maxrow, &nl->nl_row, &nl->sorted_atoms, &nl->sort_keys,
-                    &nl->iota, &nl->lanes, &nl->hist, &nl->cpos};
+                    &nl->iota, &nl->lanes, &nl->hist, &nl->cpos, &nl->crow, &nl->coff,
+                    &nl->centry, &nl->fbuf};
   for (DevBuf *b : bufs) b->release();
   delete nl;
 }
@@ -380,6 +387,102 @@ static int build_rev(tb_context *ctx, tb_nlist *nl) {
         (int)nl->n, nl->offsets.as<int>(), nl->nbr.as<int>(), nl->rev.as<int>());
   CK(cudaGetLastError());
   nl->rev_valid = true;
+  return TB_OK;
+}
+
+// Warp chunks: rows sorted by length (stable radix sort -> deterministic),
+// floor(32/L) rows of length L per warp.  row_len[i] = lanes of atom i; lane
+// k of row i maps to entry coff[i] + k of centry (or offsets[i] + k when
+// centry == nullptr).  hist = row-length histogram (hist[0] = empty rows).
+static int build_chunks(tb_context *ctx, tb_nlist *nl, const int *row_len, const int *coff,
+                        const int *centry, const int *hist) {
+  const int N = (int)nl->n;
+  CK(nl->sorted_atoms.ensure(sizeof(int) * N));
+  CK(nl->sort_keys.ensure(sizeof(int) * N));
+  CK(nl->iota.ensure(sizeof(int) * N));
+  k_iota<<<nblk(N, 256), 256, 0, ctx->stream>>>(N, nl->iota.as<int>());
+  CK(cudaGetLastError());
+  size_t tmp = 0;
+  CK(cub::DeviceRadixSort::SortPairs(nullptr, tmp, row_len, nl->sort_keys.as<int>(),
+                                     nl->iota.as<int>(), nl->sorted_atoms.as<int>(), N, 0, 6,
+                                     ctx->stream));
+  CK(ctx->cub_tmp.ensure(tmp));
+  CK(cub::DeviceRadixSort::SortPairs(ctx->cub_tmp.p, tmp, row_len, nl->sort_keys.as<int>(),
+                                     nl->iota.as<int>(), nl->sorted_atoms.as<int>(), N, 0, 6,
+                                     ctx->stream));
+  ChunkPlan plan;
+  memset(&plan, 0, sizeof(plan));
+  int start = hist[0], chunks = 0;
+  for (int L = 1; L <= 32; ++L) {
+    plan.count[L] = hist[L];
+    plan.bucket_start[L] = start;
+    plan.chunk_base[L] = chunks;
+    start += hist[L];
+    chunks += (hist[L] + 32 / L - 1) / (32 / L);
+  }
+  plan.chunk_base[33] = chunks;
+  nl->n_empty = hist[0];
+  if (chunks > 0) {
+    CK(nl->lanes.ensure(sizeof(int4) * 32 * (size_t)chunks));
+    k_fill_lanes<<<chunks, 32, 0, ctx->stream>>>(plan, nl->sorted_atoms.as<int>(),
+                                                  coff ? coff : nl->offsets.as<int>(), centry,
+                                                  nl->nbr.as<int>(), nl->lanes.as<int4>());
+    CK(cudaGetLastError());
+  }
+  nl->nchunks = chunks;
+  return TB_OK;
+}
+
+// Species-pair compute filter (S > 1): an entry (i,j) whose build-time
+// distance exceeds need(si,sj) + skin can never become live before the next
+// rebuild, need(si,sj) = max(R+D of pair (si,sj,sj), R+D of every (si,q,sj))
+// -- it is exactly zero as a pair and as a k.  Such entries stay in the
+// exported list (bit-exact pair set, zeta_visits) but get no warp lanes.
+// Computed at the first evaluation after a build (species are known then).
+static int build_filter(tb_context *ctx, tb_nlist *nl, const int *d_species) {
+  const int N = (int)nl->n, S = ctx->S;
+  float need2[16];
+  for (int a = 0; a < S; ++a)
+    for (int b = 0; b < S; ++b) {
+      double nd = ctx->pair_mat[8 * (a * S + b)] + ctx->pair_mat[8 * (a * S + b) + 1];
+      for (int q = 0; q < S; ++q) {
+        const double *t = &ctx->trip_mat[8 * ((a * S + q) * S + b)];
+        nd = std::max(nd, t[0] + t[1]);
+      }
+      const double c = nd + nl->skin;
+      need2[a * 4 + b] = (float)(c * c * (1.0 + 1e-6));  // conservative (float table)
+    }
+  CK(nl->crow.ensure(sizeof(int) * (N + 1)));
+  CK(nl->coff.ensure(sizeof(int) * (N + 1)));
+  CK(nl->centry.ensure(sizeof(int) * std::max<int64_t>(nl->entries, 1)));
+  CK(cudaMemsetAsync(nl->crow.p, 0, sizeof(int) * (N + 1), ctx->stream));
+  Box b = make_box(nl->L, nl->per);
+  NeedTable nt;
+  memcpy(nt.need2, need2, sizeof(need2));
+  k_filter_rows<false><<<nblk(N, 128), 128, 0, ctx->stream>>>(
+      N, nl->ref_pos.as<double>(), d_species, S, nt, b, nl->offsets.as<int>(), nl->nbr.as<int>(),
+      nl->crow.as<int>(), nullptr, nullptr);
+  CK(cudaGetLastError());
+  int rc = exclusive_scan(ctx, nl->crow.as<int>(), nl->coff.as<int>(), N + 1);
+  if (rc) return rc;
+  k_filter_rows<true><<<nblk(N, 128), 128, 0, ctx->stream>>>(
+      N, nl->ref_pos.as<double>(), d_species, S, nt, b, nl->offsets.as<int>(), nl->nbr.as<int>(),
+      nullptr, nl->coff.as<int>(), nl->centry.as<int>());
+  CK(cudaGetLastError());
+  CK(cudaMemsetAsync(nl->hist.p, 0, sizeof(int) * 34, ctx->stream));
+  k_len_hist<<<std::min(nblk(N, 256), 296), 256, 0, ctx->stream>>>(N, nl->crow.as<int>(),
+                                                                    nl->hist.as<int>());
+  CK(cudaGetLastError());
+  int *hm = reinterpret_cast<int *>(ctx->h_small);
+  CK(cudaMemcpyAsync(hm, nl->hist.p, sizeof(int) * 34, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  int hist[34];
+  memcpy(hist, hm, sizeof(hist));
+  rc = build_chunks(ctx, nl, nl->crow.as<int>(), nl->coff.as<int>(), nl->centry.as<int>(), hist);
+  if (rc) return rc;
+  nl->filtered = true;
+  nl->filter_species = d_species;
+  nl->fbuf_zero = false;
   return TB_OK;
 }
 
@@ -546,44 +649,17 @@ extern "C" int tb_build_neighbors_owned(tb_context *ctx, tb_nlist *nl, int64_t n
     CK(cudaMemcpyAsync(nl->ref_pos.p, d_pos, sizeof(double) * 3 * N, cudaMemcpyDeviceToDevice,
                        ctx->stream));
   }
-  // warp chunks for the fast kernel (tb_warp.cuh): rows sorted by length
-  // (stable radix sort, deterministic), floor(32/L) rows of length L per warp
-  nl->nchunks = 0;
-  nl->n_empty = 0;
+  // warp chunks for the fast kernel (tb_warp.cuh) over the full rows; a
+  // species-pair compute filter may replace them at the first evaluation
+  nl->filter_species = nullptr;
+  nl->filtered = false;
+  nl->fbuf_zero = false;
   if (nl->max_row <= 32 && N > 0) {
-    CK(nl->sorted_atoms.ensure(sizeof(int) * N));
-    CK(nl->sort_keys.ensure(sizeof(int) * N));
-    CK(nl->iota.ensure(sizeof(int) * N));
-    k_iota<<<nblk(N, 256), 256, 0, ctx->stream>>>(N, nl->iota.as<int>());
-    CK(cudaGetLastError());
-    size_t tmp = 0;
-    CK(cub::DeviceRadixSort::SortPairs(nullptr, tmp, nl->row_count.as<int>(),
-                                       nl->sort_keys.as<int>(), nl->iota.as<int>(),
-                                       nl->sorted_atoms.as<int>(), N, 0, 6, ctx->stream));
-    CK(ctx->cub_tmp.ensure(tmp));
-    CK(cub::DeviceRadixSort::SortPairs(ctx->cub_tmp.p, tmp, nl->row_count.as<int>(),
-                                       nl->sort_keys.as<int>(), nl->iota.as<int>(),
-                                       nl->sorted_atoms.as<int>(), N, 0, 6, ctx->stream));
-    ChunkPlan plan;
-    memset(&plan, 0, sizeof(plan));
-    int start = hist[0], chunks = 0;
-    for (int L = 1; L <= 32; ++L) {
-      plan.count[L] = hist[L];
-      plan.bucket_start[L] = start;
-      plan.chunk_base[L] = chunks;
-      start += hist[L];
-      chunks += (hist[L] + 32 / L - 1) / (32 / L);
-    }
-    plan.chunk_base[33] = chunks;
-    nl->n_empty = hist[0];
-    if (chunks > 0) {
-      CK(nl->lanes.ensure(sizeof(int4) * 32 * (size_t)chunks));
-      k_fill_lanes<<<chunks, 32, 0, ctx->stream>>>(plan, nl->sorted_atoms.as<int>(),
-                                                    nl->offsets.as<int>(), nl->nbr.as<int>(),
-                                                    nl->lanes.as<int4>());
-      CK(cudaGetLastError());
-    }
-    nl->nchunks = chunks;
+    int rc2 = build_chunks(ctx, nl, nl->row_count.as<int>(), nullptr, nullptr, hist);
+    if (rc2) return rc2;
+  } else {
+    nl->nchunks = 0;
+    nl->n_empty = 0;
   }
   nl->built = true;
   return TB_OK;
@@ -834,10 +910,23 @@ static int enqueue_compute(tb_context *ctx, const tb_nlist *nl, const double *d_
       int rc = build_rev(ctx, const_cast<tb_nlist *>(nl));
       if (rc) return rc;
     }
-    CK(ctx->fbuf.ensure(sizeof(double) * 3 * std::max<int64_t>(nl->entries, 1)));
+    tb_nlist *nlm = const_cast<tb_nlist *>(nl);
+    CK(nlm->fbuf.ensure(sizeof(double) * 3 * std::max<int64_t>(nl->entries, 1)));
   }
   // warp-chunk kernel for rows <= 32 entries and <= 2 species; else the tile kernel
   const bool warp_path = nl->nchunks > 0 && !ctx->force_tile && ctx->S <= 2;
+  if (warp_path && ctx->S > 1 && !ctx->no_filter &&
+      (!nl->filtered || nl->filter_species != d_species)) {
+    int rc = build_filter(ctx, const_cast<tb_nlist *>(nl), d_species);
+    if (rc) return rc;
+  }
+  const bool filtered = warp_path && nl->filtered;
+  if (scatter == TB_SCATTER_GATHER && filtered && !nl->fbuf_zero) {
+    // entries the filter gave no lane are never written: zero them once per build
+    CK(cudaMemsetAsync(nl->fbuf.p, 0, sizeof(double) * 3 * std::max<int64_t>(nl->entries, 1),
+                       ctx->stream));
+    const_cast<tb_nlist *>(nl)->fbuf_zero = true;
+  }
   // force accumulator and stats counters: zero once, left zeroed by k_finalize
   if (ctx->facc_n < n) {
     CK(ctx->facc.ensure(sizeof(double) * 3 * std::max(n, 1)));
@@ -863,7 +952,7 @@ static int enqueue_compute(tb_context *ctx, const tb_nlist *nl, const double *d_
   a.off = nl->offsets.as<int>();
   a.nbr = nl->nbr.as<int>();
   a.forces = ctx->facc.as<double>();
-  a.fbuf = ctx->fbuf.as<double>();
+  a.fbuf = nl->fbuf.as<double>();
   a.per_atom = d_per_atom;
   a.partials = ctx->partials.as<double>();
   a.stats = ctx->stats_acc.as<unsigned long long>();
@@ -877,10 +966,16 @@ static int enqueue_compute(tb_context *ctx, const tb_nlist *nl, const double *d_
     w.nchunks = nl->nchunks;
     w.n_empty = nl->n_empty;
     w.facc = ctx->facc.as<double>();
+    w.count_packed = filtered ? 0 : 1;
     const bool want_stats = d_stats != nullptr;
     rc = precision == TB_PREC_DOUBLE ? launch_warp_prec<double>(ctx, nl, a, w, scatter, want_stats)
                                      : launch_warp_prec<float>(ctx, nl, a, w, scatter, want_stats);
     nparts = ctx->last_blocks;
+    if (!rc && filtered && want_stats) {
+      k_pack_stats<<<nblk(n, 256), 256, 0, ctx->stream>>>(n, d_pos, a.box, a.rc2, a.off, a.nbr,
+                                                           a.stats);
+      CK(cudaGetLastError());
+    }
   } else {
     rc = precision == TB_PREC_DOUBLE ? launch_prec<double>(ctx, nl, a, C, scatter)
                                      : launch_prec<float>(ctx, nl, a, C, scatter);
@@ -958,8 +1053,18 @@ extern "C" int tb_compute(tb_context *ctx, const tb_nlist *nl, const double *pos
   if (rc) return rc;
   const double *d_pos = stage_in(ctx, positions, 3 * (size_t)n, ctx->pos, rc);
   if (rc) return rc;
+  const bool sp_host = !is_device_ptr(species);
   const int *d_sp = stage_in(ctx, species, (size_t)n, ctx->species, rc);
   if (rc) return rc;
+  if (sp_host && ctx->S > 1) {
+    // host species go through one staging buffer: a content change must
+    // invalidate the species-pair compute filter built for the old values
+    if (ctx->last_species.size() != (size_t)n ||
+        memcmp(ctx->last_species.data(), species, sizeof(int) * n) != 0) {
+      ctx->last_species.assign(species, species + n);
+      const_cast<tb_nlist *>(nl)->filtered = false;
+    }
+  }
   bool f_dev = is_device_ptr(forces);
   double *d_f = forces;
   if (!f_dev) {

@@ -46,6 +46,7 @@ struct WArgs {
   const int4 *__restrict__ lanes;      // [nchunks*32] {entry, i, j, L}; entry -1 = idle lane
   const int *__restrict__ empty_atoms; // atoms with empty rows (per_atom = 0)
   int nchunks, n_empty;
+  int count_packed;                    // rows are the full skin rows: count zeta_visits here
   double *__restrict__ facc;           // ATOMIC: zeroed force accumulator (n,3)
 };
 
@@ -143,7 +144,7 @@ __device__ __forceinline__ void chunk_body(const KArgs &a, const WArgs &w, const
   }
   const bool live = valid && r2 < a.rc2;
   const unsigned lmask = __ballot_sync(0xffffffffu, live);
-  if (ST && valid && pos == 0) {
+  if (ST && w.count_packed && valid && pos == 0) {
     const unsigned seg = (L >= 32 ? 0xffffffffu : ((1u << L) - 1u)) << first;
     const unsigned long long nl = __popc(lmask & seg);
     A.c_vis += nl * nl;  // zeta_visits = sum_i n_i^2 (kernels.py:537-544)
@@ -527,8 +528,8 @@ __global__ void k_len_hist(int n, const int *__restrict__ len, int *__restrict__
 
 // one warp per chunk: lane -> {entry, i, j, L} (entry -1: idle lane)
 __global__ void k_fill_lanes(const ChunkPlan plan, const int *__restrict__ sorted_atoms,
-                             const int *__restrict__ offsets, const int *__restrict__ nbr,
-                             int4 *__restrict__ lanes) {
+                             const int *__restrict__ offsets, const int *__restrict__ centry,
+                             const int *__restrict__ nbr, int4 *__restrict__ lanes) {
   const int c = blockIdx.x, lane = threadIdx.x;
   int L = 1;
   while (L < 32 && plan.chunk_base[L + 1] <= c) ++L;
@@ -537,10 +538,66 @@ __global__ void k_fill_lanes(const ChunkPlan plan, const int *__restrict__ sorte
   int4 v = make_int4(-1, 0, 0, L);
   if (lane < rpc * L && row < plan.count[L]) {
     const int atom = sorted_atoms[plan.bucket_start[L] + row];
-    const int e = offsets[atom] + lane % L;
+    const int k = offsets[atom] + lane % L;
+    const int e = centry ? centry[k] : k;
     v = make_int4(e, atom, nbr[e], L);
   }
   lanes[32 * (int64_t)c + lane] = v;
+}
+
+struct NeedTable {
+  float need2[16];  // (need(si,sj) + skin)^2, [si*4 + sj]
+};
+
+// species-pair compute filter over the full rows at the build positions
+template <bool FILL>
+__global__ void k_filter_rows(int n, const double *__restrict__ ref, const int *__restrict__ species,
+                              int S, NeedTable nt, Box box, const int *__restrict__ offsets,
+                              const int *__restrict__ nbr, int *__restrict__ crow,
+                              const int *__restrict__ coff, int *__restrict__ centry) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  int si = species[i];
+  si = (si < 0 || si >= S) ? 0 : si;
+  double xi[3];
+  load3(ref, i, xi);
+  int cnt = 0;
+  const int base = FILL ? coff[i] : 0;
+  for (int e = offsets[i]; e < offsets[i + 1]; ++e) {
+    const int j = nbr[e];
+    int sj = species[j];
+    sj = (sj < 0 || sj >= S) ? 0 : sj;
+    double xj[3], d[3];
+    load3(ref, j, xj);
+    if (disp_r2(xi, xj, box, d) < (double)nt.need2[si * 4 + sj]) {
+      if (FILL) centry[base + cnt] = e;
+      ++cnt;
+    }
+  }
+  if (!FILL) crow[i] = cnt;
+}
+
+// zeta_visits / packed pairs over the FULL skin rows (needed when the warp
+// chunks only hold the filtered entries): sum_i n_i^2 with n_i = #(r < r_cut)
+__global__ void k_pack_stats(int n, const double *__restrict__ pos, Box box, double rc2,
+                             const int *__restrict__ offsets, const int *__restrict__ nbr,
+                             unsigned long long *__restrict__ stats) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  unsigned long long c = 0;
+  if (i < n) {
+    double xi[3];
+    load3(pos, i, xi);
+    for (int e = offsets[i]; e < offsets[i + 1]; ++e) {
+      double xj[3], d[3];
+      load3(pos, nbr[e], xj);
+      c += disp_r2(xi, xj, box, d) < rc2;
+    }
+  }
+  unsigned long long sq = warp_sum(c * c), pk = warp_sum(c);
+  if ((threadIdx.x & 31) == 0 && pk) {
+    atomicAdd(stats, sq);
+    atomicAdd(stats + 1, pk);
+  }
 }
 
 // ---------------------------------------------------------------------------
