@@ -37,6 +37,7 @@ extern "C" {
 #define TB_ERR_INPUT 2  /* -> InputError */
 #define TB_ERR_CUDA 3   /* CUDA runtime failure */
 #define TB_ERR_ARG 4    /* bad argument (null pointer, size) */
+#define TB_ERR_UNSUPPORTED 5 /* tb_md_run cannot take this system: use tb_md_step */
 
 #define TB_PREC_DOUBLE 0 /* fp64 everywhere ("double", kernels.py:154-165) */
 #define TB_PREC_MIXED 1  /* fp64 positions/displacements/accumulators, fp32 potential math ("single") */
@@ -71,6 +72,10 @@ int tb_set_stream(tb_context *ctx, void *stream);
  * shared-memory tile kernel even when the warp-chunk kernel applies (rows of
  * <= 32 skin-list entries); used to cover both paths in the parity tests. */
 #define TB_OPT_TILE_KERNEL 1
+/* TB_OPT_LIST_MARGIN = p: neighbour lists built from now on reserve p percent
+ * (default 25) of extra entries and warp chunks, the room tb_md_run's device
+ * rebuild grows into before it has to replay from its entry state. */
+#define TB_OPT_LIST_MARGIN 2
 int tb_set_option(tb_context *ctx, int option, int value);
 
 /* Synchronise the context's stream. */
@@ -165,6 +170,36 @@ int tb_md_step(tb_context *ctx, tb_nlist *nl, int64_t n, double *d_positions,
                double dt, double accel, double r_cut, double skin, int precision,
                int scatter, int force_rebuild, double *d_per_atom, double *d_result,
                int32_t *rebuilt);
+
+/* Rebuild nl in place at d_positions with the device-side builder of
+ * tb_md_run (sizes kept in device memory, no host round trip between its
+ * kernels; one synchronisation at the end to refresh the host-side counts).
+ * Same pair set and row order as tb_build_neighbors (neighbor.py:157-212);
+ * falls back to it when the list outgrows its capacity.  Requires a list
+ * built by tb_build_neighbors for a periodic box with rows <= 32 entries
+ * (else TB_ERR_UNSUPPORTED). */
+int tb_nlist_rebuild_device(tb_context *ctx, tb_nlist *nl, const double *d_positions,
+                            const int32_t *d_species, int scatter);
+
+/* Device-resident NVE run: `steps` velocity-Verlet steps (same semantics as
+ * tb_md_step: skin/2 trigger plus a fixed cadence when rebuild_every > 0,
+ * system.py:355-380, 427-460) as ONE CUDA-graph launch with no host
+ * synchronisation inside -- the neighbour-list rebuild runs on the device in
+ * a conditional graph node, its sizes kept in device memory.  On entry nl must
+ * be built (tb_build_neighbors) for periodic boxes, d_forces / d_result[0] hold
+ * F and E of the current positions.  Every `record_every` steps (step s =
+ * 1..steps) [E_pot, E_kin] is written to d_series[2*(s/record_every)] (row 0 is
+ * the caller's).  On return d_result holds E, W6 and E_kin (d_result[7]) of the
+ * last step; *rebuilds = rebuilds done.  Capacity overflows are replayed from
+ * the entry state internally.  Returns TB_ERR_UNSUPPORTED (state untouched)
+ * when the system needs the general path (free axes, rows > 32 entries, > 2
+ * species, tile kernel forced): call tb_md_step per step instead.  Replaces
+ * the step loop of run_nve (system.py:427-460). */
+int tb_md_run(tb_context *ctx, tb_nlist *nl, int64_t n, double *d_positions,
+              double *d_velocities, double *d_forces, const double *d_mass,
+              const int32_t *d_species, double dt, double accel, double r_cut, double skin,
+              int rebuild_every, int precision, int scatter, int64_t steps, int record_every,
+              double *d_series, double *d_result, int64_t *rebuilds);
 
 /* Diagnostic: measured FMA throughput of this GPU in TFLOP/s (2 flops per
  * FMA), precision TB_PREC_DOUBLE -> DFMA, TB_PREC_MIXED -> FFMA; the roofline

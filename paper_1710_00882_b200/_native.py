@@ -18,11 +18,12 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("TB_LIB_PATH") or os.path.join(_HERE, "lib", "libtersoff_b200.so")
 HEADER_PATH = os.path.join(os.path.dirname(_HERE), "include", "tersoff_b200.h")
 
-TB_OK, TB_ERR_CONFIG, TB_ERR_INPUT, TB_ERR_CUDA, TB_ERR_ARG = range(5)
+TB_OK, TB_ERR_CONFIG, TB_ERR_INPUT, TB_ERR_CUDA, TB_ERR_ARG, TB_ERR_UNSUPPORTED = range(6)
 PRECISION = {"double": 0, "single": 1, "mixed": 1}
 SCATTER = {"atomic": 0, "gather": 1}
 NSTATS = 6
 OPT_TILE_KERNEL = 1
+OPT_LIST_MARGIN = 2  # percent of spare list entries / warp chunks (tb_md_run)
 
 # symbol -> (restype, argtypes); the exported surface of the C ABI
 _P = ctypes.c_void_p
@@ -49,6 +50,9 @@ SIGNATURES = {
     "tb_check_errors": (_I, [_P]),
     "tb_md_step": (_I, [_P, _P, _I64, _P, _P, _P, _P, _P, _P, _P, _D, _D, _D, _D, _I, _I,
                         _I, _P, _P, _P]),
+    "tb_md_run": (_I, [_P, _P, _I64, _P, _P, _P, _P, _P, _D, _D, _D, _D, _I, _I, _I, _I64, _I,
+                       _P, _P, _P]),
+    "tb_nlist_rebuild_device": (_I, [_P, _P, _P, _P, _I]),
     "tb_profile": (_I, [_P, _I]),
     "tb_profile_read": (_I, [_P, _P, _P]),
     "tb_measure_peak": (_I, [_P, _I, ctypes.POINTER(_D)]),

@@ -23,6 +23,7 @@
 #include "../../include/tersoff_b200.h"
 #include "tb_kernels.cuh"
 #include "tb_warp.cuh"
+#include "tb_dnl.cuh"
 
 #ifndef TB_VERSION_TAG
 #define TB_VERSION_TAG "dev"
@@ -62,21 +63,25 @@ struct tb_context {
   std::string err;
   // parameters
   int S = 0;
+  int param_version = 0;  // bumped by tb_set_params (captured MD graphs hold the tables)
   bool lam3 = false;
   double r_cut = 0.0;
   std::vector<double> pair_mat, trip_mat;
   // scratch
   DevBuf pos, species, forces, per_atom, result, stats, partials, errf, drift, bounds,
-      cub_tmp, facc, stats_acc, ke_part;
+      cub_tmp, facc, stats_acc, ke_part, snap;
+  cudaStream_t cap[2] = {nullptr, nullptr};  // tb_md_run graph capture
   int64_t facc_n = -1;
   ErrFlags *h_err = nullptr;      // pinned
   double *h_small = nullptr;      // pinned scratch (64 doubles)
   // kernel timing (tb_profile)
   bool profile = false;
   bool force_tile = false;
+  double list_margin = 0.25;  // TB_OPT_LIST_MARGIN
   bool warp_per_chunk = getenv("TB_WARP_PER_CHUNK") != nullptr;
   bool no_filter = getenv("TB_NO_FILTER") != nullptr;  // disable the species-pair compute filter
   std::vector<int> last_species;  // host species of the last tb_compute (filter validity)
+  const int *dplan = nullptr;  // tb_md_run capture: device {nchunks, n_empty}
   int last_blocks = 0;  // grid of the last Tersoff launch (partials to reduce)  // tb_set_option(TB_OPT_TILE_KERNEL): general tile kernel only
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_used, ev_free;
 };
@@ -90,7 +95,8 @@ struct tb_nlist {
   int64_t entries = 0, max_row = 0;
   bool built = false;
   DevBuf offsets, nbr, rev, ref_pos, atom_cell, cell_count, cell_start, cell_atoms, row_count,
-      maxrow, nl_row, sorted_atoms, sort_keys, iota, lanes, hist, cpos, crow, coff, centry;
+      maxrow, nl_row, sorted_atoms, sort_keys, iota, lanes, hist, cpos, crow, coff, centry,
+      scratch;  // TMPW-wide per-atom rows of the single-pass scan
   bool filtered = false;                 // chunks built from the species-pair filter
   DevBuf fbuf;                           // gather mode: per-entry force pieces
   bool fbuf_zero = false;                // entries without lanes hold zeros
@@ -98,7 +104,37 @@ struct tb_nlist {
   bool rev_valid = false;
   int nchunks = 0;  // > 0: warp-chunk fast path available (max_row <= 32)
   int n_empty = 0;  // atoms with empty rows: sorted_atoms[0, n_empty)
+  // capacities for the device-resident rebuild (tb_md_run): entry-sized
+  // buffers hold ecap entries, the lane table ccap warp chunks
+  double margin = -1.0;  // < 0: the context's list margin at the next build
+  int64_t ecap = 0, ccap = 0;
+  Grid grid;
+  int64_t ncell = 0;
+  DevBuf plan;      // DevPlan
+  struct MdGraph *md = nullptr;
 };
+
+// captured device-resident NVE loop (tb_md_run), reused while its key holds
+struct MdKey {
+  const void *ptr[40];
+  int64_t n, ecap, ccap, ncell;
+  double dt, accel, skin, r_cut;
+  int rebuild_every, precision, scatter, record_every, param_version, filtered, S, tile;
+};
+
+struct MdGraph {
+  MdKey key;
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+};
+
+static void md_graph_release(tb_nlist *nl) {
+  if (!nl->md) return;
+  if (nl->md->exec) cudaGraphExecDestroy(nl->md->exec);
+  if (nl->md->graph) cudaGraphDestroy(nl->md->graph);
+  delete nl->md;
+  nl->md = nullptr;
+}
 
 // ---------------------------------------------------------------------------
 // error helpers
@@ -149,6 +185,8 @@ static Box make_box(const double *L, const int *per) {
 }
 
 static inline int nblk(int64_t n, int t) { return (int)((n + t - 1) / t); }
+
+constexpr int SCAN_G = 8;  // lanes per atom in the list scan
 
 // ---------------------------------------------------------------------------
 // parameter tables (potential.py:127-155 column order)
@@ -230,7 +268,7 @@ extern "C" void tb_destroy(tb_context *ctx) {
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   DevBuf *bufs[] = {&ctx->pos, &ctx->species, &ctx->forces, &ctx->per_atom, &ctx->result,
                     &ctx->stats, &ctx->partials, &ctx->facc, &ctx->stats_acc, &ctx->ke_part, &ctx->errf,
-                    &ctx->drift, &ctx->bounds, &ctx->cub_tmp};
+                    &ctx->drift, &ctx->bounds, &ctx->cub_tmp, &ctx->snap};
   for (DevBuf *b : bufs) b->release();
   for (auto *v : {&ctx->ev_used, &ctx->ev_free})
     for (auto &ev : *v) {
@@ -240,6 +278,8 @@ extern "C" void tb_destroy(tb_context *ctx) {
   if (ctx->h_err) cudaFreeHost(ctx->h_err);
   if (ctx->h_small) cudaFreeHost(ctx->h_small);
   if (ctx->own) cudaStreamDestroy(ctx->own);
+  for (cudaStream_t c : ctx->cap)
+    if (c) cudaStreamDestroy(c);
   delete ctx;
 }
 
@@ -257,6 +297,11 @@ extern "C" int tb_set_option(tb_context *ctx, int option, int value) {
   if (!ctx) return TB_ERR_ARG;
   if (option == TB_OPT_TILE_KERNEL) {
     ctx->force_tile = value != 0;
+    return TB_OK;
+  }
+  if (option == TB_OPT_LIST_MARGIN) {
+    if (value < 0 || value > 1000) return fail(ctx, TB_ERR_ARG, "list margin %d%% out of range", value);
+    ctx->list_margin = value / 100.0;
     return TB_OK;
   }
   return fail(ctx, TB_ERR_ARG, "unknown option %d", option);
@@ -289,6 +334,7 @@ extern "C" int tb_set_params(tb_context *ctx, int nspecies, const double *pair_m
   }
   ctx->lam3 = lam3;
   ctx->r_cut = rc;
+  ctx->param_version += 1;
   if (r_cut_out) *r_cut_out = rc;
   return TB_OK;
 }
@@ -367,8 +413,9 @@ extern "C" void tb_nlist_destroy(tb_nlist *nl) {
                     &nl->cell_count, &nl->cell_start, &nl->cell_atoms, &nl->row_count,
                     &nl->maxrow, &nl->nl_row, &nl->sorted_atoms, &nl->sort_keys,
                     &nl->iota, &nl->lanes, &nl->hist, &nl->cpos, &nl->crow, &nl->coff,
-                    &nl->centry, &nl->fbuf};
+                    &nl->centry, &nl->fbuf, &nl->plan, &nl->scratch};
   for (DevBuf *b : bufs) b->release();
+  md_graph_release(nl);
   delete nl;
 }
 
@@ -381,7 +428,7 @@ static int exclusive_scan(tb_context *ctx, const int *in, int *out, int64_t coun
 }
 
 static int build_rev(tb_context *ctx, tb_nlist *nl) {
-  CK(nl->rev.ensure(sizeof(int) * std::max<int64_t>(nl->entries, 1)));
+  CK(nl->rev.ensure(sizeof(int) * std::max<int64_t>(nl->ecap, 1)));
   if (nl->n)
     k_nl_reverse<<<nblk(nl->n, 256), 256, 0, ctx->stream>>>(
         (int)nl->n, nl->offsets.as<int>(), nl->nbr.as<int>(), nl->rev.as<int>());
@@ -422,8 +469,9 @@ static int build_chunks(tb_context *ctx, tb_nlist *nl, const int *row_len, const
   }
   plan.chunk_base[33] = chunks;
   nl->n_empty = hist[0];
+  nl->ccap = chunks + (int64_t)(nl->margin * (double)chunks) + (nl->margin > 0 ? 64 : 0);
   if (chunks > 0) {
-    CK(nl->lanes.ensure(sizeof(int4) * 32 * (size_t)chunks));
+    CK(nl->lanes.ensure(sizeof(int4) * 32 * (size_t)nl->ccap));
     k_fill_lanes<<<chunks, 32, 0, ctx->stream>>>(plan, nl->sorted_atoms.as<int>(),
                                                   coff ? coff : nl->offsets.as<int>(), centry,
                                                   nl->nbr.as<int>(), nl->lanes.as<int4>());
@@ -439,9 +487,10 @@ static int build_chunks(tb_context *ctx, tb_nlist *nl, const int *row_len, const
 // -- it is exactly zero as a pair and as a k.  Such entries stay in the
 // exported list (bit-exact pair set, zeta_visits) but get no warp lanes.
 // Computed at the first evaluation after a build (species are known then).
-static int build_filter(tb_context *ctx, tb_nlist *nl, const int *d_species) {
-  const int N = (int)nl->n, S = ctx->S;
-  float need2[16];
+static NeedTable need_table(const tb_context *ctx, const tb_nlist *nl) {
+  const int S = ctx->S;
+  NeedTable nt;
+  float *need2 = nt.need2;
   for (int a = 0; a < S; ++a)
     for (int b = 0; b < S; ++b) {
       double nd = ctx->pair_mat[8 * (a * S + b)] + ctx->pair_mat[8 * (a * S + b) + 1];
@@ -452,13 +501,17 @@ static int build_filter(tb_context *ctx, tb_nlist *nl, const int *d_species) {
       const double c = nd + nl->skin;
       need2[a * 4 + b] = (float)(c * c * (1.0 + 1e-6));  // conservative (float table)
     }
+  return nt;
+}
+
+static int build_filter(tb_context *ctx, tb_nlist *nl, const int *d_species) {
+  const int N = (int)nl->n, S = ctx->S;
   CK(nl->crow.ensure(sizeof(int) * (N + 1)));
   CK(nl->coff.ensure(sizeof(int) * (N + 1)));
-  CK(nl->centry.ensure(sizeof(int) * std::max<int64_t>(nl->entries, 1)));
+  CK(nl->centry.ensure(sizeof(int) * std::max<int64_t>(nl->ecap, 1)));
   CK(cudaMemsetAsync(nl->crow.p, 0, sizeof(int) * (N + 1), ctx->stream));
   Box b = make_box(nl->L, nl->per);
-  NeedTable nt;
-  memcpy(nt.need2, need2, sizeof(need2));
+  const NeedTable nt = need_table(ctx, nl);
   k_filter_rows<false><<<nblk(N, 128), 128, 0, ctx->stream>>>(
       N, nl->ref_pos.as<double>(), d_species, S, nt, b, nl->offsets.as<int>(), nl->nbr.as<int>(),
       nl->crow.as<int>(), nullptr, nullptr);
@@ -589,8 +642,11 @@ extern "C" int tb_build_neighbors_owned(tb_context *ctx, tb_nlist *nl, int64_t n
   CK(nl->maxrow.ensure(sizeof(int)));
   CK(nl->ref_pos.ensure(sizeof(double) * 3 * std::max(N, 1)));
 
+  CK(nl->hist.ensure(sizeof(int) * 34));
+  CK(nl->scratch.ensure(sizeof(int) * TMPW * (size_t)std::max(N, 1)));
   CK(cudaMemsetAsync(nl->cell_count.p, 0, sizeof(int) * (ncell + 1), ctx->stream));
   CK(cudaMemsetAsync(nl->maxrow.p, 0, sizeof(int), ctx->stream));
+  CK(cudaMemsetAsync(nl->hist.p, 0, sizeof(int) * 34, ctx->stream));
   CK(cudaMemsetAsync(nl->row_count.p, 0, sizeof(int) * (N + 1), ctx->stream));
   if (N) {
     k_cell_index<<<nblk(N, 256), 256, 0, ctx->stream>>>(N, d_pos, g, nl->atom_cell.as<int>(),
@@ -611,23 +667,16 @@ extern "C" int tb_build_neighbors_owned(tb_context *ctx, tb_nlist *nl, int64_t n
     k_cell_gather<<<nblk(N, 256), 256, 0, ctx->stream>>>(N, d_pos, nl->cell_atoms.as<int>(),
                                                           nl->cpos.as<double4>());
     CK(cudaGetLastError());
-    k_nl_scan<false><<<nblk(N, 128), 128, 0, ctx->stream>>>(
-        N, (int)n_owned, nl->cpos.as<double4>(), g, bc * bc, nl->atom_cell.as<int>(), nl->cell_start.as<int>(),
-        nl->cell_atoms.as<int>(), nl->row_count.as<int>(), nullptr, nullptr,
-        nl->maxrow.as<int>(), nullptr);
+    // single pass: rows of <= TMPW entries land in the scratch rows, counts,
+    // max row and the row-length histogram (for the warp chunks) come along
+    k_nl_scan_tmp<SCAN_G><<<nblk((int64_t)N * SCAN_G, 256), 256, 0, ctx->stream>>>(
+        N, (int)n_owned, nl->cpos.as<double4>(), g, bc * bc, nl->atom_cell.as<int>(),
+        nl->cell_start.as<int>(), nl->cell_atoms.as<int>(), nl->row_count.as<int>(),
+        nl->scratch.as<int>(), nl->maxrow.as<int>(), nl->hist.as<int>());
     CK(cudaGetLastError());
   }
   rc = exclusive_scan(ctx, nl->row_count.as<int>(), nl->offsets.as<int>(), N + 1);
   if (rc) return rc;
-  // row-length histogram for the warp chunks, read back with the totals in
-  // the build's single host synchronisation
-  CK(nl->hist.ensure(sizeof(int) * 34));
-  CK(cudaMemsetAsync(nl->hist.p, 0, sizeof(int) * 34, ctx->stream));
-  if (N) {
-    k_len_hist<<<std::min(nblk(N, 256), 296), 256, 0, ctx->stream>>>(N, nl->row_count.as<int>(),
-                                                                      nl->hist.as<int>());
-    CK(cudaGetLastError());
-  }
   int *hm = reinterpret_cast<int *>(ctx->h_small);  // pinned: [entries, max_row, hist[34]]
   CK(cudaMemcpyAsync(&hm[0], nl->offsets.as<int>() + N, sizeof(int), cudaMemcpyDeviceToHost,
                      ctx->stream));
@@ -638,14 +687,28 @@ extern "C" int tb_build_neighbors_owned(tb_context *ctx, tb_nlist *nl, int64_t n
   nl->max_row = hm[1];
   int hist[34];
   memcpy(hist, hm + 2, sizeof(hist));
-  CK(nl->nbr.ensure(sizeof(int) * std::max<int64_t>(nl->entries, 1)));
-  CK(nl->nl_row.ensure(sizeof(int) * std::max<int64_t>(nl->entries, 1)));
-  if (N) {
+  // entry-sized buffers carry a margin so that the device-resident rebuild
+  // (tb_md_run) can regrow the list in place
+  if (nl->margin < 0) nl->margin = ctx->list_margin;
+  nl->ecap = nl->entries + (int64_t)(nl->margin * (double)nl->entries) + (nl->margin > 0 ? 256 : 0);
+  nl->grid = g;
+  nl->ncell = ncell;
+  CK(nl->nbr.ensure(sizeof(int) * nl->ecap));
+  CK(nl->nl_row.ensure(sizeof(int) * nl->ecap));
+  if (N && nl->max_row <= TMPW) {
+    k_nl_compact<SCAN_G><<<nblk((int64_t)N * SCAN_G, 256), 256, 0, ctx->stream>>>(
+        N, nl->scratch.as<int>(), nl->row_count.as<int>(), nl->offsets.as<int>(),
+        nl->nbr.as<int>(), nl->nl_row.as<int>(), nullptr);
+    CK(cudaGetLastError());
+  } else if (N) {
+    // rows longer than the scratch rows: second full scan straight into CSR
     k_nl_scan<true><<<nblk(N, 128), 128, 0, ctx->stream>>>(
         N, (int)n_owned, nl->cpos.as<double4>(), g, bc * bc, nl->atom_cell.as<int>(), nl->cell_start.as<int>(),
         nl->cell_atoms.as<int>(), nullptr, nl->offsets.as<int>(), nl->nbr.as<int>(), nullptr,
         nl->nl_row.as<int>());
     CK(cudaGetLastError());
+  }
+  if (N) {
     CK(cudaMemcpyAsync(nl->ref_pos.p, d_pos, sizeof(double) * 3 * N, cudaMemcpyDeviceToDevice,
                        ctx->stream));
   }
@@ -911,7 +974,7 @@ static int enqueue_compute(tb_context *ctx, const tb_nlist *nl, const double *d_
       if (rc) return rc;
     }
     tb_nlist *nlm = const_cast<tb_nlist *>(nl);
-    CK(nlm->fbuf.ensure(sizeof(double) * 3 * std::max<int64_t>(nl->entries, 1)));
+    CK(nlm->fbuf.ensure(sizeof(double) * 3 * std::max<int64_t>(nl->ecap, 1)));
   }
   // warp-chunk kernel for rows <= 32 entries and <= 2 species; else the tile kernel
   const bool warp_path = nl->nchunks > 0 && !ctx->force_tile && ctx->S <= 2;
@@ -965,6 +1028,11 @@ static int enqueue_compute(tb_context *ctx, const tb_nlist *nl, const double *d_
     w.empty_atoms = nl->sorted_atoms.as<int>();
     w.nchunks = nl->nchunks;
     w.n_empty = nl->n_empty;
+    w.dinfo = nullptr;
+    if (ctx->dplan) {  // tb_md_run capture: chunk counts live in the device plan
+      w.dinfo = ctx->dplan;
+      w.nchunks = (int)nl->ccap;  // grid sizing only
+    }
     w.facc = ctx->facc.as<double>();
     w.count_packed = filtered ? 0 : 1;
     const bool want_stats = d_stats != nullptr;
@@ -1200,5 +1268,405 @@ extern "C" int tb_md_step(tb_context *ctx, tb_nlist *nl, int64_t n, double *d_po
   k_kinetic_sum<<<1, 256, 0, ctx->stream>>>(kb, ctx->ke_part.as<double>(), 0.5 / accel,
                                             d_result + 7);
   CK(cudaGetLastError());
+  return TB_OK;
+}
+
+// ---------------------------------------------------------------------------
+// device-resident NVE loop: one graph launch for a whole run (tb_dnl.cuh)
+// ---------------------------------------------------------------------------
+
+static int radix_sort_rows(tb_context *ctx, tb_nlist *nl, const int *row_len) {
+  size_t tmp = ctx->cub_tmp.cap;
+  CK(cub::DeviceRadixSort::SortPairs(ctx->cub_tmp.p, tmp, row_len, nl->sort_keys.as<int>(),
+                                     nl->iota.as<int>(), nl->sorted_atoms.as<int>(), (int)nl->n,
+                                     0, 6, ctx->stream));
+  return TB_OK;
+}
+
+// The complete neighbour-list rebuild with every size taken from the device
+// plan: cell binning, count pass, offsets, fill pass, snapshot, species-pair
+// filter, warp chunks, reverse index.  No host synchronisation; capacities
+// were fixed by the last host build (tb_build_neighbors_owned).
+static int enqueue_rebuild_device(tb_context *ctx, tb_nlist *nl, const double *d_pos,
+                                  const int *d_species, int scatter, bool filter, DevPlan *plan) {
+  const int N = (int)nl->n;
+  const Grid &g = nl->grid;
+  cudaStream_t st = ctx->stream;
+  const int ecap = (int)nl->ecap, ccap = (int)nl->ccap;
+  k_plan_reset<<<1, 64, 0, st>>>(plan, 1);
+  CK(cudaMemsetAsync(nl->cell_count.p, 0, sizeof(int) * (nl->ncell + 1), st));
+  k_cell_index<<<nblk(N, 256), 256, 0, st>>>(N, d_pos, g, nl->atom_cell.as<int>(),
+                                               nl->cell_count.as<int>());
+  int rc = exclusive_scan(ctx, nl->cell_count.as<int>(), nl->cell_start.as<int>(), nl->ncell + 1);
+  if (rc) return rc;
+  CK(cudaMemcpyAsync(nl->cell_count.p, nl->cell_start.p, sizeof(int) * (nl->ncell + 1),
+                     cudaMemcpyDeviceToDevice, st));
+  k_cell_fill<<<nblk(N, 256), 256, 0, st>>>(N, nl->atom_cell.as<int>(), nl->cell_count.as<int>(),
+                                              nl->cell_atoms.as<int>());
+  k_cell_gather<<<nblk(N, 256), 256, 0, st>>>(N, d_pos, nl->cell_atoms.as<int>(),
+                                                nl->cpos.as<double4>());
+  const double bc2 = nl->bc * nl->bc;
+  k_nl_scan_tmp<SCAN_G><<<nblk((int64_t)N * SCAN_G, 256), 256, 0, st>>>(
+      N, N, nl->cpos.as<double4>(), g, bc2, nl->atom_cell.as<int>(), nl->cell_start.as<int>(),
+      nl->cell_atoms.as<int>(), nl->row_count.as<int>(), nl->scratch.as<int>(), &plan->max_row,
+      plan->hist);
+  CK(cudaGetLastError());
+  rc = exclusive_scan(ctx, nl->row_count.as<int>(), nl->offsets.as<int>(), N + 1);
+  if (rc) return rc;
+  const int hb = std::min(nblk(N, 256), 296);
+  // with the species-pair filter the chunks come from the filtered rows (below)
+  k_plan<<<1, 32, 0, st>>>(plan, nl->offsets.as<int>(), N, ecap, filter ? INT_MAX : ccap);
+  k_guard_offsets<<<nblk(N + 1, 256), 256, 0, st>>>(N, plan, nl->offsets.as<int>());
+  k_nl_compact<SCAN_G><<<nblk((int64_t)N * SCAN_G, 256), 256, 0, st>>>(
+      N, nl->scratch.as<int>(), nl->row_count.as<int>(), nl->offsets.as<int>(), nl->nbr.as<int>(),
+      nl->nl_row.as<int>(), &plan->list_overflow);
+  CK(cudaGetLastError());
+  CK(cudaMemcpyAsync(nl->ref_pos.p, d_pos, sizeof(double) * 3 * N, cudaMemcpyDeviceToDevice, st));
+  const int *row_len = nl->row_count.as<int>(), *loff = nl->offsets.as<int>();
+  const int *cent = nullptr;
+  if (filter) {
+    const NeedTable nt = need_table(ctx, nl);
+    const Box b = make_box(nl->L, nl->per);
+    CK(cudaMemsetAsync(nl->crow.p, 0, sizeof(int) * (N + 1), st));
+    k_filter_rows<false><<<nblk(N, 128), 128, 0, st>>>(
+        N, nl->ref_pos.as<double>(), d_species, ctx->S, nt, b, nl->offsets.as<int>(),
+        nl->nbr.as<int>(), nl->crow.as<int>(), nullptr, nullptr);
+    rc = exclusive_scan(ctx, nl->crow.as<int>(), nl->coff.as<int>(), N + 1);
+    if (rc) return rc;
+    k_filter_rows<true><<<nblk(N, 128), 128, 0, st>>>(
+        N, nl->ref_pos.as<double>(), d_species, ctx->S, nt, b, nl->offsets.as<int>(),
+        nl->nbr.as<int>(), nullptr, nl->coff.as<int>(), nl->centry.as<int>());
+    k_plan_reset<<<1, 64, 0, st>>>(plan, 0);
+    k_len_hist_plan<<<hb, 256, 0, st>>>(N, nl->crow.as<int>(), plan);
+    k_plan<<<1, 32, 0, st>>>(plan, nullptr, N, ecap, ccap);
+    CK(cudaGetLastError());
+    row_len = nl->crow.as<int>();
+    loff = nl->coff.as<int>();
+    cent = nl->centry.as<int>();
+    if (scatter == TB_SCATTER_GATHER)
+      CK(cudaMemsetAsync(nl->fbuf.p, 0, sizeof(double) * 3 * (size_t)ecap, st));
+  }
+  rc = radix_sort_rows(ctx, nl, row_len);
+  if (rc) return rc;
+  k_fill_lanes_dev<<<ccap, 32, 0, st>>>(plan, nl->sorted_atoms.as<int>(), loff, cent,
+                                          nl->nbr.as<int>(), nl->lanes.as<int4>());
+  if (scatter == TB_SCATTER_GATHER)
+    k_nl_reverse<<<nblk(N, 256), 256, 0, st>>>(N, nl->offsets.as<int>(), nl->nbr.as<int>(),
+                                                 nl->rev.as<int>());
+  CK(cudaGetLastError());
+  return TB_OK;
+}
+
+namespace {
+struct MdArgs {
+  int64_t n;
+  double *pos, *vel, *forces;
+  const double *mass;
+  const int *species;
+  double dt, accel, r_cut, skin;
+  int rebuild_every, precision, scatter, record_every;
+  double *series, *result;
+};
+}  // namespace
+
+static MdKey md_key(const tb_context *ctx, const tb_nlist *nl, const MdArgs &m) {
+  MdKey k;
+  memset(&k, 0, sizeof(k));
+  const void *p[] = {m.pos, m.vel, m.forces, m.mass, m.species, m.series, m.result,
+                     nl->plan.p, nl->offsets.p, nl->nbr.p, nl->rev.p, nl->ref_pos.p,
+                     nl->atom_cell.p, nl->cell_count.p, nl->cell_start.p, nl->cell_atoms.p,
+                     nl->row_count.p, nl->nl_row.p, nl->sorted_atoms.p, nl->sort_keys.p,
+                     nl->iota.p, nl->lanes.p, nl->cpos.p, nl->crow.p, nl->coff.p, nl->centry.p,
+                     nl->fbuf.p, ctx->facc.p, ctx->partials.p, ctx->ke_part.p, ctx->errf.p,
+                     ctx->cub_tmp.p, nl->scratch.p};
+  static_assert(sizeof(p) / sizeof(p[0]) <= 40, "MdKey::ptr too small");
+  memcpy(k.ptr, p, sizeof(p));
+  k.n = m.n;
+  k.ecap = nl->ecap;
+  k.ccap = nl->ccap;
+  k.ncell = nl->ncell;
+  k.dt = m.dt;
+  k.accel = m.accel;
+  k.skin = m.skin;
+  k.r_cut = m.r_cut;
+  k.rebuild_every = m.rebuild_every;
+  k.precision = m.precision;
+  k.scatter = m.scatter;
+  k.record_every = m.record_every;
+  k.param_version = ctx->param_version;
+  k.filtered = nl->filtered ? 1 : 0;
+  k.S = ctx->S;
+  k.tile = ctx->force_tile ? 1 : 0;
+  return k;
+}
+
+// capture: WHILE(steps) { kick+drift ; decide ; IF(rebuild) { rebuild } ;
+//                         Tersoff ; finalize ; kick+KE ; tail }
+static int md_capture(tb_context *ctx, tb_nlist *nl, const MdArgs &m, MdGraph *G) {
+  for (cudaStream_t &c : ctx->cap)
+    if (!c) CK(cudaStreamCreateWithFlags(&c, cudaStreamNonBlocking));
+  DevPlan *plan = nl->plan.as<DevPlan>();
+  const int n = (int)m.n;
+  const Box box = make_box(nl->L, nl->per);
+  const double half = 0.5 * m.dt * m.accel;
+  const double hs = 0.5 * m.skin;
+  const int kb = std::max(1, std::min(nblk(n, 256), 4 * 148));
+  const bool filter = ctx->S > 1 && nl->filtered;
+
+  CK(cudaGraphCreate(&G->graph, 0));
+  cudaGraphConditionalHandle h_loop, h_reb;
+  CK(cudaGraphConditionalHandleCreate(&h_loop, G->graph, 1, cudaGraphCondAssignDefault));
+  CK(cudaGraphConditionalHandleCreate(&h_reb, G->graph, 0, 0));
+  cudaGraphNodeParams wp = {cudaGraphNodeTypeConditional};
+  wp.conditional.handle = h_loop;
+  wp.conditional.type = cudaGraphCondTypeWhile;
+  wp.conditional.size = 1;
+  cudaGraphNode_t wnode;
+  CK(cudaGraphAddNode(&wnode, G->graph, nullptr, 0, &wp));
+  cudaGraph_t body = wp.conditional.phGraph_out[0];
+
+  cudaStream_t saved = ctx->stream;
+  const bool saved_prof = ctx->profile;
+  ctx->profile = false;  // event nodes are not allowed in conditional bodies
+  auto restore = [&]() {
+    ctx->stream = saved;
+    ctx->profile = saved_prof;
+    ctx->dplan = nullptr;
+  };
+  cudaStream_t s0 = ctx->cap[0], s1 = ctx->cap[1];
+  CK(cudaStreamBeginCaptureToGraph(s0, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
+  ctx->stream = s0;
+  int rc = TB_OK;
+  do {
+    k_md_kick_drift<<<nblk(n, 256), 256, 0, s0>>>(n, m.pos, m.vel, m.forces, m.mass,
+                                                   nl->ref_pos.as<double>(), half, m.dt, box,
+                                                   plan);
+    k_md_decide<<<1, 1, 0, s0>>>(plan, hs * hs, m.rebuild_every, h_reb);
+    if (cudaGetLastError() != cudaSuccess) {
+      rc = fail(ctx, TB_ERR_CUDA, "md capture: launch failed");
+      break;
+    }
+    cudaStreamCaptureStatus cs;
+    cudaGraph_t cg;
+    const cudaGraphNode_t *deps = nullptr;
+    size_t ndeps = 0;
+    if (cudaStreamGetCaptureInfo(s0, &cs, nullptr, &cg, &deps, &ndeps) != cudaSuccess) {
+      rc = fail(ctx, TB_ERR_CUDA, "md capture: capture info failed");
+      break;
+    }
+    cudaGraphNodeParams ip = {cudaGraphNodeTypeConditional};
+    ip.conditional.handle = h_reb;
+    ip.conditional.type = cudaGraphCondTypeIf;
+    ip.conditional.size = 1;
+    cudaGraphNode_t inode;
+    cudaError_t e = cudaGraphAddNode(&inode, cg, deps, ndeps, &ip);
+    if (e == cudaSuccess) e = cudaStreamUpdateCaptureDependencies(s0, &inode, 1,
+                                                                  cudaStreamSetCaptureDependencies);
+    if (e == cudaSuccess)
+      e = cudaStreamBeginCaptureToGraph(s1, ip.conditional.phGraph_out[0], nullptr, nullptr, 0,
+                                        cudaStreamCaptureModeRelaxed);
+    if (e != cudaSuccess) {
+      rc = fail(ctx, TB_ERR_CUDA, "md capture: conditional node: %s", cudaGetErrorString(e));
+      break;
+    }
+    ctx->stream = s1;
+    rc = enqueue_rebuild_device(ctx, nl, m.pos, m.species, m.scatter, filter, plan);
+    cudaGraph_t tmp;
+    e = cudaStreamEndCapture(s1, &tmp);
+    ctx->stream = s0;
+    if (!rc && e != cudaSuccess)
+      rc = fail(ctx, TB_ERR_CUDA, "md capture: rebuild body: %s", cudaGetErrorString(e));
+    if (rc) break;
+    ctx->dplan = &plan->nchunks;
+    rc = enqueue_compute(ctx, nl, m.pos, m.species, m.r_cut, m.precision, m.scatter, m.forces,
+                         nullptr, m.result, nullptr);
+    ctx->dplan = nullptr;
+    if (rc) break;
+    k_md_kick_ke<<<kb, 256, 0, s0>>>(n, m.vel, m.forces, m.mass, half, ctx->ke_part.as<double>());
+    k_md_tail<<<1, 256, 0, s0>>>(kb, ctx->ke_part.as<double>(), 0.5 / m.accel, m.result, plan,
+                                 m.series, m.record_every, h_loop);
+    if (cudaGetLastError() != cudaSuccess) rc = fail(ctx, TB_ERR_CUDA, "md capture: launch failed");
+  } while (false);
+  cudaGraph_t tmp;
+  cudaError_t e = cudaStreamEndCapture(s0, &tmp);
+  restore();
+  if (rc) return rc;
+  if (e != cudaSuccess)
+    return fail(ctx, TB_ERR_CUDA, "md capture: step body: %s", cudaGetErrorString(e));
+  CK(cudaGraphInstantiate(&G->exec, G->graph, 0));
+  return TB_OK;
+}
+
+// capacities and every lazily sized buffer of the device rebuild and the
+// Tersoff launch, fixed before a capture (nothing may allocate inside one)
+static int md_prepare(tb_context *ctx, tb_nlist *nl, const int *d_species, int scatter) {
+  const int N = (int)nl->n;
+  const bool filter_wanted = ctx->S > 1 && !ctx->no_filter;
+  if (filter_wanted && (!nl->filtered || nl->filter_species != d_species)) {
+    int rc = build_filter(ctx, nl, d_species);
+    if (rc) return rc;
+  }
+  CK(nl->plan.ensure(sizeof(DevPlan)));
+  CK(nl->centry.ensure(sizeof(int) * nl->ecap));
+  CK(nl->crow.ensure(sizeof(int) * (N + 1)));
+  CK(nl->coff.ensure(sizeof(int) * (N + 1)));
+  CK(nl->lanes.ensure(sizeof(int4) * 32 * (size_t)nl->ccap));
+  if (scatter == TB_SCATTER_GATHER) {
+    CK(nl->fbuf.ensure(sizeof(double) * 3 * (size_t)nl->ecap));
+    CK(cudaMemsetAsync(nl->fbuf.p, 0, sizeof(double) * 3 * (size_t)nl->ecap, ctx->stream));
+    nl->fbuf_zero = true;
+    int rc = build_rev(ctx, nl);
+    if (rc) return rc;
+  }
+  {
+    size_t t1 = 0, t2 = 0, t3 = 0;
+    CK(cub::DeviceScan::ExclusiveSum(nullptr, t1, nl->cell_count.as<int>(),
+                                     nl->cell_start.as<int>(), (int)(nl->ncell + 1), ctx->stream));
+    CK(cub::DeviceScan::ExclusiveSum(nullptr, t2, nl->row_count.as<int>(), nl->offsets.as<int>(),
+                                     N + 1, ctx->stream));
+    CK(cub::DeviceRadixSort::SortPairs(nullptr, t3, nl->row_count.as<int>(),
+                                       nl->sort_keys.as<int>(), nl->iota.as<int>(),
+                                       nl->sorted_atoms.as<int>(), N, 0, 6, ctx->stream));
+    CK(ctx->cub_tmp.ensure(std::max(t1, std::max(t2, t3))));
+  }
+  int sms = 0;
+  CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device));
+  CK(ctx->partials.ensure(sizeof(double) * 8 * (size_t)sms * 64));
+  CK(ctx->ke_part.ensure(sizeof(double) * 4 * 148));
+  if (!ctx->errf.p) {
+    int rc = reset_errors(ctx);
+    if (rc) return rc;
+  }
+  if (ctx->facc_n < N) {
+    CK(ctx->facc.ensure(sizeof(double) * 3 * N));
+    CK(cudaMemsetAsync(ctx->facc.p, 0, sizeof(double) * 3 * N, ctx->stream));
+    ctx->facc_n = N;
+  }
+  if (!ctx->stats_acc.p) {
+    CK(ctx->stats_acc.ensure(sizeof(unsigned long long) * TB_NSTATS));
+    CK(cudaMemsetAsync(ctx->stats_acc.p, 0, sizeof(unsigned long long) * TB_NSTATS, ctx->stream));
+  }
+  return TB_OK;
+}
+
+extern "C" int tb_md_run(tb_context *ctx, tb_nlist *nl, int64_t n, double *d_positions,
+                         double *d_velocities, double *d_forces, const double *d_mass,
+                         const int32_t *d_species, double dt, double accel, double r_cut,
+                         double skin, int rebuild_every, int precision, int scatter,
+                         int64_t steps, int record_every, double *d_series, double *d_result,
+                         int64_t *rebuilds) {
+  if (!ctx || !nl || !d_result || (n && (!d_positions || !d_velocities || !d_forces || !d_mass ||
+                                         !d_species)))
+    return fail(ctx, TB_ERR_ARG, "null argument");
+  if (!(dt > 0)) return fail(ctx, TB_ERR_CONFIG, "dt must be positive, got %s", fmt_g(dt).c_str());
+  if (steps < 0 || steps > INT_MAX - 1) return fail(ctx, TB_ERR_ARG, "bad step count");
+  if (record_every < 0) return fail(ctx, TB_ERR_ARG, "bad record interval");
+  if (rebuilds) *rebuilds = 0;
+  if (steps == 0) return TB_OK;
+  CK(cudaSetDevice(ctx->device));
+  // the loop keeps the list geometry and the warp-chunk kernel: anything else
+  // goes through the per-step path (tb_md_step)
+  if (!nl->built || nl->n != n || n == 0 || !(nl->per[0] && nl->per[1] && nl->per[2]) ||
+      nl->nchunks <= 0 || ctx->force_tile || ctx->S > 2 || r_cut != nl->r_cut || skin != nl->skin)
+    return fail(ctx, TB_ERR_UNSUPPORTED,
+                "device-resident loop needs a built periodic list with rows <= 32 entries");
+  MdArgs m{n, d_positions, d_velocities, d_forces, d_mass, d_species, dt, accel, r_cut, skin,
+           rebuild_every, precision, scatter, record_every, d_series, d_result};
+  const int N = (int)n;
+  int64_t extra = 0;
+  CK(ctx->snap.ensure(sizeof(double) * 9 * (size_t)N + sizeof(double)));
+  double *snap = ctx->snap.as<double>();
+  CK(cudaMemcpyAsync(snap, d_positions, sizeof(double) * 3 * N, cudaMemcpyDeviceToDevice, ctx->stream));
+  CK(cudaMemcpyAsync(snap + 3 * N, d_velocities, sizeof(double) * 3 * N, cudaMemcpyDeviceToDevice, ctx->stream));
+  CK(cudaMemcpyAsync(snap + 6 * N, d_forces, sizeof(double) * 3 * N, cudaMemcpyDeviceToDevice, ctx->stream));
+  CK(cudaMemcpyAsync(snap + 9 * N, d_result, sizeof(double), cudaMemcpyDeviceToDevice, ctx->stream));
+  for (int attempt = 0;; ++attempt) {
+    int rc0 = md_prepare(ctx, nl, d_species, scatter);
+    if (rc0) return rc0;
+    const bool filter_wanted = ctx->S > 1 && !ctx->no_filter;
+    // ---- graph (re)capture when anything it holds changed ----
+    const MdKey key = md_key(ctx, nl, m);
+    if (!nl->md || memcmp(&nl->md->key, &key, sizeof(key)) != 0) {
+      md_graph_release(nl);
+      nl->md = new MdGraph();
+      nl->md->key = key;
+      int rc = md_capture(ctx, nl, m, nl->md);
+      if (rc) {
+        md_graph_release(nl);
+        return rc;
+      }
+    }
+    // ---- run ----
+    DevPlan hp;
+    memset(&hp, 0, sizeof(hp));
+    hp.nchunks = nl->nchunks;
+    hp.n_empty = nl->n_empty;
+    hp.entries = (int)nl->entries;
+    hp.max_row = (int)nl->max_row;
+    hp.target = (int)steps;
+    CK(cudaMemcpyAsync(nl->plan.p, &hp, sizeof(hp), cudaMemcpyHostToDevice, ctx->stream));
+    CK(cudaGraphLaunch(nl->md->exec, ctx->stream));
+    CK(cudaMemcpyAsync(&hp, nl->plan.p, sizeof(hp), cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    if (hp.overflow == 0) {
+      nl->entries = hp.entries;
+      nl->max_row = hp.max_row;
+      nl->nchunks = hp.nchunks;
+      nl->n_empty = hp.n_empty;
+      if (hp.rebuilds > 0 && scatter != TB_SCATTER_GATHER) nl->rev_valid = false;
+      if (hp.rebuilds > 0 && filter_wanted) nl->fbuf_zero = scatter == TB_SCATTER_GATHER;
+      if (rebuilds) *rebuilds = hp.rebuilds + extra;
+      return tb_check_errors(ctx);
+    }
+    // ---- capacity overflow: back to the entry state, regrow, replay ----
+    CK(cudaMemcpyAsync(d_positions, snap, sizeof(double) * 3 * N, cudaMemcpyDeviceToDevice, ctx->stream));
+    CK(cudaMemcpyAsync(d_velocities, snap + 3 * N, sizeof(double) * 3 * N, cudaMemcpyDeviceToDevice, ctx->stream));
+    CK(cudaMemcpyAsync(d_forces, snap + 6 * N, sizeof(double) * 3 * N, cudaMemcpyDeviceToDevice, ctx->stream));
+    CK(cudaMemcpyAsync(d_result, snap + 9 * N, sizeof(double), cudaMemcpyDeviceToDevice, ctx->stream));
+    if ((hp.overflow & OVF_ROW) || attempt >= 3)
+      return fail(ctx, TB_ERR_UNSUPPORTED,
+                  "device-resident loop: neighbour rows outgrew the warp kernel (overflow %d)",
+                  hp.overflow);
+    nl->margin = std::max(2.0 * nl->margin, 0.25);
+    int rc = tb_build_neighbors(ctx, nl, n, d_positions, nl->L, nl->per, r_cut, skin);
+    if (rc) return rc;
+    nl->filtered = false;
+    extra += 1;
+    if (nl->nchunks <= 0)
+      return fail(ctx, TB_ERR_UNSUPPORTED, "device-resident loop: rows exceed 32 entries");
+  }
+}
+
+extern "C" int tb_nlist_rebuild_device(tb_context *ctx, tb_nlist *nl, const double *d_positions,
+                                       const int32_t *d_species, int scatter) {
+  if (!ctx || !nl || !d_positions || !d_species) return fail(ctx, TB_ERR_ARG, "null argument");
+  CK(cudaSetDevice(ctx->device));
+  if (!nl->built || nl->n == 0 || !(nl->per[0] && nl->per[1] && nl->per[2]) ||
+      nl->nchunks <= 0 || ctx->force_tile || ctx->S > 2)
+    return fail(ctx, TB_ERR_UNSUPPORTED,
+                "device rebuild needs a built periodic list with rows <= 32 entries");
+  int rc = md_prepare(ctx, nl, d_species, scatter);
+  if (rc) return rc;
+  DevPlan hp;
+  memset(&hp, 0, sizeof(hp));
+  CK(cudaMemcpyAsync(nl->plan.p, &hp, sizeof(hp), cudaMemcpyHostToDevice, ctx->stream));
+  const bool filter = ctx->S > 1 && nl->filtered;
+  rc = enqueue_rebuild_device(ctx, nl, d_positions, d_species, scatter, filter,
+                              nl->plan.as<DevPlan>());
+  if (rc) return rc;
+  CK(cudaMemcpyAsync(&hp, nl->plan.p, sizeof(hp), cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  if (hp.overflow) {
+    // regrow through the host-synchronised build (same list, new capacities)
+    nl->margin = std::max(2.0 * nl->margin, 0.25);
+    return tb_build_neighbors(ctx, nl, nl->n, d_positions, nl->L, nl->per, nl->r_cut, nl->skin);
+  }
+  nl->entries = hp.entries;
+  nl->max_row = hp.max_row;
+  nl->nchunks = hp.nchunks;
+  nl->n_empty = hp.n_empty;
+  nl->rev_valid = scatter == TB_SCATTER_GATHER;
+  nl->fbuf_zero = filter && scatter == TB_SCATTER_GATHER;
+  if (filter) nl->filter_species = d_species;
   return TB_OK;
 }

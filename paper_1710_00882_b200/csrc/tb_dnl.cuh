@@ -1,0 +1,222 @@
+// tb_dnl.cuh -- kernels of the device-resident NVE loop (tb_md_run).
+//
+// The whole run is ONE CUDA-graph launch: a WHILE node over the steps whose
+// body is kick+drift (+ the skin/2 drift reduction), the rebuild decision, an
+// IF node holding the complete neighbour-list rebuild, the Tersoff kernel and
+// its finalize, and kick + kinetic energy.  Every size the rebuild needs
+// (list entries, row-length histogram, warp-chunk plan) lives in device memory
+// (DevPlan) and every buffer has a capacity fixed before capture, so there is
+// no host synchronisation inside the loop.  Capacity overflows are latched in
+// DevPlan and end the loop; the host then restores the run's entry snapshot,
+// regrows the capacities and replays it (tb_api.cu, tb_md_run).
+//
+// Semantics follow run_nve / velocity_verlet_step (system.py:355-380, 427-460)
+// and needs_rebuild (neighbor.py:220-229) exactly as tb_md_step does.
+#pragma once
+#include "tb_warp.cuh"
+
+namespace tb {
+
+enum : int {
+  OVF_ENTRIES = 1,  // more list entries than the capacity
+  OVF_ROW = 2,      // a row longer than 32 entries (warp kernel not applicable)
+  OVF_CHUNKS = 4,   // more warp chunks than the capacity
+};
+
+struct DevPlan {
+  int nchunks, n_empty;   // read by the Tersoff kernel (WArgs::dinfo)
+  int entries;            // offsets[n] of the last build
+  int max_row;
+  int overflow;           // OVF_* bits (sticky for the run)
+  int list_overflow;      // OVF_ENTRIES: the fill pass must not write
+  int step, target;       // steps taken / to take in this launch
+  int rebuilds;
+  int pad;
+  unsigned long long drift_bits;  // max |x - x_ref|^2 of this step (bits; r^2 >= 0)
+  int hist[34];
+  int bucket_start[34], chunk_base[34];
+};
+
+// v += half F/m ; x += dt v ; wrap ; max drift^2 against the list snapshot
+// (k_kick_drift + k_max_drift fused, same arithmetic)
+__global__ void __launch_bounds__(256) k_md_kick_drift(int n, double *__restrict__ pos,
+                                                       double *__restrict__ vel,
+                                                       const double *__restrict__ f,
+                                                       const double *__restrict__ mass,
+                                                       const double *__restrict__ ref, double half,
+                                                       double dt, Box box,
+                                                       DevPlan *__restrict__ plan) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  unsigned long long best = 0;
+  if (i < n) {
+    const double m = mass[i];
+    double x[3];
+#pragma unroll
+    for (int ax = 0; ax < 3; ++ax) {
+      const int64_t k = 3 * (int64_t)i + ax;
+      const double v = __dadd_rn(vel[k], __ddiv_rn(__dmul_rn(half, f[k]), m));
+      vel[k] = v;
+      double xx = __dadd_rn(pos[k], __dmul_rn(dt, v));
+      if (box.per[ax]) xx = np_remainder(xx, box.L[ax]);
+      pos[k] = xx;
+      x[ax] = xx;
+    }
+    double r[3], d[3];
+    load3(ref, i, r);
+    best = __double_as_longlong(disp_r2(r, x, box, d));
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    unsigned long long v = __shfl_down_sync(0xffffffffu, best, o);
+    best = v > best ? v : best;
+  }
+  if ((threadIdx.x & 31) == 0 && best) atomicMax(&plan->drift_bits, best);
+}
+
+// rebuild decision for this step (skin/2 trigger or the fixed cadence)
+__global__ void k_md_decide(DevPlan *__restrict__ plan, double half_skin2, int rebuild_every,
+                            cudaGraphConditionalHandle h_rebuild) {
+  const double d2 = __longlong_as_double((long long)plan->drift_bits);
+  const int step = plan->step + 1;
+  const bool need = d2 > half_skin2 || (rebuild_every > 0 && step % rebuild_every == 0);
+  plan->step = step;
+  plan->drift_bits = 0ull;
+  if (need) plan->rebuilds += 1;
+  cudaGraphSetConditional(h_rebuild, need ? 1u : 0u);
+}
+
+// reset the per-build counters (full) or only the histogram (filter pass)
+__global__ void k_plan_reset(DevPlan *__restrict__ plan, int full) {
+  const int t = threadIdx.x;
+  if (t < 34) plan->hist[t] = 0;
+  if (full && t == 0) plan->max_row = 0;
+}
+
+// chunk plan from the row-length histogram (one thread): buckets of rows of
+// equal length, floor(32/L) rows per warp chunk (same plan as build_chunks)
+// (offsets = the list's CSR offsets: entries checked against the capacity;
+//  nullptr for the filtered rows, which are a subset of the list)
+__global__ void k_plan(DevPlan *__restrict__ plan, const int *__restrict__ offsets, int n,
+                       int entries_cap, int chunks_cap) {
+  if (threadIdx.x != 0) return;
+  int ovf = plan->overflow;
+  if (offsets) {
+    const int entries = offsets[n];
+    plan->entries = entries;
+    if (entries > entries_cap) {
+      ovf |= OVF_ENTRIES;
+      plan->list_overflow = 1;
+    }
+  }
+  if (plan->max_row > 32) ovf |= OVF_ROW;
+  int start = plan->hist[0], chunks = 0;
+  plan->bucket_start[0] = 0;
+  plan->chunk_base[0] = 0;
+  for (int L = 1; L <= 32; ++L) {
+    plan->bucket_start[L] = start;
+    plan->chunk_base[L] = chunks;
+    start += plan->hist[L];
+    chunks += (plan->hist[L] + 32 / L - 1) / (32 / L);
+  }
+  plan->bucket_start[33] = start;
+  plan->chunk_base[33] = chunks;
+  if (chunks > chunks_cap) ovf |= OVF_CHUNKS;
+  plan->overflow = ovf;
+  plan->nchunks = ovf ? 0 : chunks;
+  plan->n_empty = ovf ? 0 : plan->hist[0];
+}
+
+// after an entries overflow every row is made empty, so all later readers of
+// offsets stay inside the buffers
+__global__ void k_guard_offsets(int n, const DevPlan *__restrict__ plan, int *__restrict__ offsets) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i <= n && plan->list_overflow) offsets[i] = 0;
+}
+
+// one warp per chunk: lane -> {entry, i, j, L} from the device plan
+__global__ void k_fill_lanes_dev(const DevPlan *__restrict__ plan,
+                                 const int *__restrict__ sorted_atoms,
+                                 const int *__restrict__ offsets, const int *__restrict__ centry,
+                                 const int *__restrict__ nbr, int4 *__restrict__ lanes) {
+  const int c = blockIdx.x, lane = threadIdx.x;
+  if (c >= plan->nchunks) return;
+  int L = 1;
+  while (L < 32 && plan->chunk_base[L + 1] <= c) ++L;
+  const int rpc = 32 / L;
+  const int row = (c - plan->chunk_base[L]) * rpc + lane / L;
+  int4 v = make_int4(-1, 0, 0, L);
+  if (lane < rpc * L && row < plan->hist[L]) {
+    const int atom = sorted_atoms[plan->bucket_start[L] + row];
+    const int k = offsets[atom] + lane % L;
+    const int e = centry ? centry[k] : k;
+    v = make_int4(e, atom, nbr[e], L);
+  }
+  lanes[32 * (int64_t)c + lane] = v;
+}
+
+// histogram of row lengths into the device plan (block-private bins)
+__global__ void k_len_hist_plan(int n, const int *__restrict__ len, DevPlan *__restrict__ plan) {
+  __shared__ int h[34];
+  if (threadIdx.x < 34) h[threadIdx.x] = 0;
+  __syncthreads();
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    atomicAdd(h + min(len[i], 33), 1);
+  __syncthreads();
+  if (threadIdx.x < 34 && h[threadIdx.x]) atomicAdd(plan->hist + threadIdx.x, h[threadIdx.x]);
+}
+
+// second half-kick fused with the kinetic-energy block partials
+__global__ void __launch_bounds__(256) k_md_kick_ke(int n, double *__restrict__ vel,
+                                                    const double *__restrict__ f,
+                                                    const double *__restrict__ mass, double half,
+                                                    double *__restrict__ part) {
+  __shared__ double s[8];
+  double acc = 0.0;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const double m = mass[i];
+    double v[3];
+#pragma unroll
+    for (int ax = 0; ax < 3; ++ax) {
+      const int64_t k = 3 * (int64_t)i + ax;
+      v[ax] = __dadd_rn(vel[k], __ddiv_rn(__dmul_rn(half, f[k]), m));
+      vel[k] = v[ax];
+    }
+    acc += m * ((v[0] * v[0] + v[1] * v[1]) + v[2] * v[2]);
+  }
+  acc = warp_sum(acc);
+  if ((threadIdx.x & 31) == 0) s[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += s[w];
+    part[blockIdx.x] = t;
+  }
+}
+
+// kinetic energy -> result[7]; [E_pot, E_kin] recorded every `every` steps;
+// the WHILE handle continues while steps remain and nothing overflowed
+__global__ void k_md_tail(int nb, const double *__restrict__ part, double scale,
+                          double *__restrict__ result, DevPlan *__restrict__ plan,
+                          double *__restrict__ series, int every,
+                          cudaGraphConditionalHandle h_loop) {
+  __shared__ double s[256];
+  double acc = 0.0;
+  for (int b = threadIdx.x; b < nb; b += 256) acc += part[b];
+  s[threadIdx.x] = acc;
+  __syncthreads();
+  for (int h = 128; h > 0; h >>= 1) {
+    if (threadIdx.x < h) s[threadIdx.x] += s[threadIdx.x + h];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    const double ke = s[0] * scale;
+    result[7] = ke;
+    const int step = plan->step;
+    if (series && every > 0 && step % every == 0) {
+      series[2 * (step / every)] = result[0];
+      series[2 * (step / every) + 1] = ke;
+    }
+    cudaGraphSetConditional(h_loop, (step < plan->target && plan->overflow == 0) ? 1u : 0u);
+  }
+}
+
+}  // namespace tb

@@ -194,6 +194,56 @@ __global__ void k_cell_gather(int n, const double *__restrict__ pos,
                          __ldg(pos + 3 * (int64_t)i + 2), 0.0);
 }
 
+// Stencil of cell `id`: distinct x and y cells (sx[nx], sy[ny]) and, per
+// (x, y) column, the distinct z cells merged into runs of consecutive ids
+// [zlo[r], zhi[r]] -- contiguous ranges of the cell-sorted arrays.  Periodic
+// axes with >= 3 cells (the common case) skip the generic de-duplication.
+struct Stencil {
+  int sx[3], sy[3], nx, ny;
+  int zlo[3], zhi[3], nr;
+};
+
+__device__ __forceinline__ void make_stencil(int id, const Grid &g, Stencil &st) {
+  const int c[3] = {id / (g.nc[1] * g.nc[2]), (id / g.nc[2]) % g.nc[1], id % g.nc[2]};
+  int sz[3], nz;
+#pragma unroll
+  for (int ax = 0; ax < 3; ++ax) {
+    int *o = ax == 0 ? st.sx : (ax == 1 ? st.sy : sz);
+    int &k = ax == 0 ? st.nx : (ax == 1 ? st.ny : nz);
+    const int nc = g.nc[ax], cc = c[ax];
+    if (g.box.per[ax] && nc >= 3) {
+      o[0] = cc == 0 ? nc - 1 : cc - 1;
+      o[1] = cc;
+      o[2] = cc == nc - 1 ? 0 : cc + 1;
+      k = 3;
+    } else {
+      k = stencil_axis(cc, nc, g.box.per[ax], o);
+    }
+  }
+  int zs[3] = {sz[0], nz > 1 ? sz[1] : 0, nz > 2 ? sz[2] : 0};
+#pragma unroll
+  for (int u = 1; u < 3; ++u)  // sort (<= 3 values)
+#pragma unroll
+    for (int v = 2; v > 0; --v)
+      if (v <= u && v < nz && zs[v - 1] > zs[v]) {
+        int tmp = zs[v];
+        zs[v] = zs[v - 1];
+        zs[v - 1] = tmp;
+      }
+  st.nr = 0;
+#pragma unroll
+  for (int u = 0; u < 3; ++u) {
+    if (u >= nz) break;
+    if (st.nr > 0 && zs[u] == st.zhi[st.nr - 1] + 1) {
+      st.zhi[st.nr - 1] = zs[u];
+    } else {
+      st.zlo[st.nr] = zs[u];
+      st.zhi[st.nr] = zs[u];
+      ++st.nr;
+    }
+  }
+}
+
 // Threads walk atoms in cell order (neighbouring threads share stencil cells,
 // so candidate loads hit L1); for every (x,y) stencil pair the distinct z cells
 // are merged into contiguous runs of the cell-sorted arrays.
@@ -205,63 +255,24 @@ __global__ void __launch_bounds__(128) k_nl_scan(int n, int n_owned, const doubl
                                                  int *__restrict__ row_count,
                                                  const int *__restrict__ offsets,
                                                  int *__restrict__ nbr, int *__restrict__ max_row,
-                                                 int *__restrict__ nl_row) {
+                                                 int *__restrict__ nl_row,
+                                                 const int *__restrict__ skip = nullptr) {
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  // device-resident rebuild: the list overflowed its capacity, write nothing
+  if (FILL && skip && *skip) return;
   int cnt = 0;
   if (t < n && cell_atoms[t] < n_owned) {  // ghosts (i >= n_owned) get empty rows
     const int i = cell_atoms[t];
     const double4 pi = cpos[t];
     const double xi[3] = {pi.x, pi.y, pi.z};
-    const int id = atom_cell[i];
-    const int c[3] = {id / (g.nc[1] * g.nc[2]), (id / g.nc[2]) % g.nc[1], id % g.nc[2]};
-    int sx[3], sy[3], sz[3], nx, ny, nz;
-    // distinct stencil cells per axis; periodic axes with >= 3 cells (the
-    // common case) without the generic de-duplication
-#pragma unroll
-    for (int ax = 0; ax < 3; ++ax) {
-      int *o = ax == 0 ? sx : (ax == 1 ? sy : sz);
-      int &k = ax == 0 ? nx : (ax == 1 ? ny : nz);
-      const int nc = g.nc[ax], cc = c[ax];
-      if (g.box.per[ax] && nc >= 3) {
-        o[0] = cc == 0 ? nc - 1 : cc - 1;
-        o[1] = cc;
-        o[2] = cc == nc - 1 ? 0 : cc + 1;
-        k = 3;
-      } else {
-        k = stencil_axis(cc, nc, g.box.per[ax], o);
-      }
-    }
-    // merge the distinct z cells into runs of consecutive ids
-    int zlo[3], zhi[3], nr = 0;
-    {
-      int zs[3] = {sz[0], nz > 1 ? sz[1] : 0, nz > 2 ? sz[2] : 0};
-#pragma unroll
-      for (int u = 1; u < 3; ++u)  // sort (<= 3 values)
-#pragma unroll
-        for (int v = 2; v > 0; --v)
-          if (v <= u && v < nz && zs[v - 1] > zs[v]) {
-            int tmp = zs[v];
-            zs[v] = zs[v - 1];
-            zs[v - 1] = tmp;
-          }
-#pragma unroll
-      for (int u = 0; u < 3; ++u) {
-        if (u >= nz) break;
-        if (nr > 0 && zs[u] == zhi[nr - 1] + 1) {
-          zhi[nr - 1] = zs[u];
-        } else {
-          zlo[nr] = zs[u];
-          zhi[nr] = zs[u];
-          ++nr;
-        }
-      }
-    }
+    Stencil sc;
+    make_stencil(atom_cell[i], g, sc);
     const int base = FILL ? offsets[i] : 0;
-    for (int a = 0; a < nx; ++a)
-      for (int b = 0; b < ny; ++b) {
-        const int row = (sx[a] * g.nc[1] + sy[b]) * g.nc[2];
-        for (int r = 0; r < nr; ++r) {
-          const int s0 = cell_start[row + zlo[r]], s1 = cell_start[row + zhi[r] + 1];
+    for (int a = 0; a < sc.nx; ++a)
+      for (int b = 0; b < sc.ny; ++b) {
+        const int row = (sc.sx[a] * g.nc[1] + sc.sy[b]) * g.nc[2];
+        for (int r = 0; r < sc.nr; ++r) {
+          const int s0 = cell_start[row + sc.zlo[r]], s1 = cell_start[row + sc.zhi[r] + 1];
           for (int s = s0; s < s1; ++s) {
             if (s == t) continue;
             const double4 pj = cpos[s];
@@ -297,6 +308,96 @@ __global__ void __launch_bounds__(128) k_nl_scan(int n, int n_owned, const doubl
   if (!FILL) {
     int m = __reduce_max_sync(0xffffffffu, cnt);
     if ((threadIdx.x & 31) == 0 && m) atomicMax(max_row, m);
+  }
+}
+
+// Single-pass list scan for rows of <= TMPW entries: G lanes per atom (atoms
+// in cell order) stride over the stencil's contiguous candidate ranges; hits
+// are compacted with a group ballot into a per-atom scratch row tmp[i][TMPW]
+// (candidate order).  Writes row_count (the true count, also when it exceeds
+// TMPW), max_row and the row-length histogram.  k_nl_compact then sorts each
+// row and writes it to its CSR slot, so the list is identical to k_nl_scan's.
+constexpr int TMPW = 32;
+template <int G>
+__global__ void __launch_bounds__(256) k_nl_scan_tmp(int n, int n_owned,
+                                                     const double4 *__restrict__ cpos, Grid g,
+                                                     double bc2, const int *__restrict__ atom_cell,
+                                                     const int *__restrict__ cell_start,
+                                                     const int *__restrict__ cell_atoms,
+                                                     int *__restrict__ row_count,
+                                                     int *__restrict__ tmp,
+                                                     int *__restrict__ max_row,
+                                                     int *__restrict__ hist) {
+  __shared__ int s_hist[34];
+  if (threadIdx.x < 34) s_hist[threadIdx.x] = 0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31, gl = lane % G;
+  const unsigned gmask = (G == 32 ? 0xffffffffu : ((1u << G) - 1u)) << (lane - gl);
+  const int t = (blockIdx.x * blockDim.x + threadIdx.x) / G;
+  int cnt = 0;
+  if (t < n) {
+    const int i = cell_atoms[t];
+    if (i < n_owned) {
+      const double4 pi = cpos[t];
+      const double xi[3] = {pi.x, pi.y, pi.z};
+      Stencil sc;
+      make_stencil(atom_cell[i], g, sc);
+      int *row_out = tmp + (int64_t)i * TMPW;
+      for (int a = 0; a < sc.nx; ++a)
+        for (int b = 0; b < sc.ny; ++b) {
+          const int row = (sc.sx[a] * g.nc[1] + sc.sy[b]) * g.nc[2];
+          for (int r = 0; r < sc.nr; ++r) {
+            const int s0 = cell_start[row + sc.zlo[r]], s1 = cell_start[row + sc.zhi[r] + 1];
+            for (int sb = s0; sb < s1; sb += G) {
+              const int s = sb + gl;
+              bool hit = false;
+              if (s < s1 && s != t) {
+                const double4 pj = cpos[s];
+                const double xj[3] = {pj.x, pj.y, pj.z};
+                double d[3];
+                hit = disp_r2(xi, xj, g.box, d) < bc2;
+              }
+              const unsigned bal = __ballot_sync(gmask, hit);
+              if (hit) {
+                const int at = cnt + __popc(bal & gmask & ((1u << lane) - 1u));
+                if (at < TMPW) row_out[at] = cell_atoms[s];
+              }
+              cnt += __popc(bal);
+            }
+          }
+        }
+    }
+    if (gl == 0) {
+      row_count[i] = cnt;
+      atomicAdd(s_hist + min(cnt, 33), 1);
+    }
+  }
+  const int m = __reduce_max_sync(0xffffffffu, cnt);
+  if (lane == 0 && m) atomicMax(max_row, m);
+  __syncthreads();
+  if (threadIdx.x < 34 && s_hist[threadIdx.x]) atomicAdd(hist + threadIdx.x, s_hist[threadIdx.x]);
+}
+
+// scratch rows -> CSR rows ascending by j (rank sort; j's of a row are distinct)
+template <int G>
+__global__ void __launch_bounds__(256) k_nl_compact(int n, const int *__restrict__ tmp,
+                                                    const int *__restrict__ row_count,
+                                                    const int *__restrict__ offsets,
+                                                    int *__restrict__ nbr, int *__restrict__ nl_row,
+                                                    const int *__restrict__ skip) {
+  if (skip && *skip) return;
+  const int i = (blockIdx.x * blockDim.x + threadIdx.x) / G, gl = threadIdx.x % G;
+  if (i >= n) return;
+  const int cnt = row_count[i];
+  if (cnt > TMPW) return;  // rows this long take the two-pass scan
+  const int *src = tmp + (int64_t)i * TMPW;
+  const int base = offsets[i];
+  for (int k = gl; k < cnt; k += G) {
+    const int v = src[k];
+    int rank = 0;
+    for (int q = 0; q < cnt; ++q) rank += src[q] < v;
+    nbr[base + rank] = v;
+    nl_row[base + rank] = i;
   }
 }
 

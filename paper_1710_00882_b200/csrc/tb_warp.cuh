@@ -46,6 +46,7 @@ struct WArgs {
   const int4 *__restrict__ lanes;      // [nchunks*32] {entry, i, j, L}; entry -1 = idle lane
   const int *__restrict__ empty_atoms; // atoms with empty rows (per_atom = 0)
   int nchunks, n_empty;
+  const int *__restrict__ dinfo;       // non-null: {nchunks, n_empty} in device memory (tb_md_run)
   int count_packed;                    // rows are the full skin rows: count zeta_visits here
   double *__restrict__ facc;           // ATOMIC: zeroed force accumulator (n,3)
 };
@@ -429,7 +430,12 @@ __global__ void __launch_bounds__(WNT, TB_WARP_MINB)
     __syncthreads();
   }
   const Tables<T, S> &tab = (S > 1) ? s_tab : gtab;
-  for (int k = blockIdx.x * WNT + threadIdx.x; k < w.n_empty; k += gridDim.x * WNT) {
+  int nchunks = w.nchunks, n_empty = w.n_empty;
+  if (w.dinfo) {
+    nchunks = __ldg(w.dinfo);
+    n_empty = __ldg(w.dinfo + 1);
+  }
+  for (int k = blockIdx.x * WNT + threadIdx.x; k < n_empty; k += gridDim.x * WNT) {
     const int m = w.empty_atoms[k];
     if (a.per_atom) a.per_atom[m] = 0.0;
     const int sm = a.species[m];
@@ -447,13 +453,13 @@ __global__ void __launch_bounds__(WNT, TB_WARP_MINB)
   const int stride = gridDim.x * WPB;
   int c = blockIdx.x * WPB + wid;
   const int4 idle = make_int4(-1, 0, 0, 1);
-  int4 cur = c < w.nchunks ? __ldg(w.lanes + 32 * (int64_t)c + lane) : idle;
-  int4 nxt = c + stride < w.nchunks ? __ldg(w.lanes + 32 * (int64_t)(c + stride) + lane) : idle;
+  int4 cur = c < nchunks ? __ldg(w.lanes + 32 * (int64_t)c + lane) : idle;
+  int4 nxt = c + stride < nchunks ? __ldg(w.lanes + 32 * (int64_t)(c + stride) + lane) : idle;
   stage_chunk<S>(s_stage[wid][0], cur, lane, a.pos, a.species);
   cp_async_commit();
   int buf = 0;
-  for (; c < w.nchunks; c += stride) {
-    const int4 nx2 = c + 2 * stride < w.nchunks
+  for (; c < nchunks; c += stride) {
+    const int4 nx2 = c + 2 * stride < nchunks
                          ? __ldg(w.lanes + 32 * (int64_t)(c + 2 * stride) + lane)
                          : idle;
     stage_chunk<S>(s_stage[wid][buf ^ 1], nxt, lane, a.pos, a.species);

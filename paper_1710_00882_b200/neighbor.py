@@ -91,6 +91,25 @@ class NeighborList:
         off, nbr = self._export()
         return nbr[off[i]:off[i + 1]]
 
+    def rebuild_on_device(self, positions, species, scatter="atomic"):
+        """Rebuild in place at `positions` (cuda float64 (n,3)) with the
+        device-side builder of the graph MD loop (tb_nlist_rebuild_device):
+        same pair set and row order as build_neighbor_list."""
+        ctx = self._nl.ctx
+        sp = species if species.dtype == torch_int32() else species.to(torch_int32())
+        ctx.check(ctx.lib.tb_nlist_rebuild_device(ctx.handle, self._nl.handle,
+                                                  _native.ptr(positions), _native.ptr(sp),
+                                                  _native.SCATTER[scatter]),
+                  "tb_nlist_rebuild_device")
+        self.reference_positions = positions.clone()
+        self._csr = None
+        return self
+
+
+def torch_int32():
+    import torch
+    return torch.int32
+
 
 def build_neighbor_list(state, r_cut, skin=0.3, device=None):
     """Full list at build_cutoff = r_cut + skin (neighbor.py:194-217)."""

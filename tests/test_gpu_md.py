@@ -29,10 +29,13 @@ def si512_state():
     return g, st, parse_params(str(g["table"]))
 
 
+@pytest.mark.parametrize("loop", ["graph", "step"])
 @pytest.mark.parametrize("precision", ["double", "single"])
-def test_device_nve_matches_reference_run(precision):
+def test_device_nve_matches_reference_run(precision, loop):
     g, st, t = si512_state()
-    rec = run_nve_device(st, t, RunConfig(dt=1.0, steps=100, skin=0.3), precision=precision)
+    rec = run_nve_device(st, t, RunConfig(dt=1.0, steps=100, skin=0.3), precision=precision,
+                         loop=loop)
+    assert rec["loop"] == loop
     ref_total = g["nve_total"]
     assert rec["rebuilds"] == int(g["nve_rebuilds"])
     scale = abs(ref_total[0])
@@ -51,14 +54,16 @@ def test_host_run_nve_matches_reference():
     assert np.max(np.abs(rec["total"] - ref)) <= 1e-9 * abs(ref[0])
 
 
+@pytest.mark.parametrize("loop", ["graph", "step"])
 @pytest.mark.parametrize("precision", ["double", "single"])
-def test_1000_step_drift_comparable_to_reference(oracle_mod, precision):
+def test_1000_step_drift_comparable_to_reference(oracle_mod, precision, loop):
     # BASELINE config 2 protocol (skin 0.3, rebuild every 10 steps + trigger,
     # dt 1 fs, 1000 K) on 8^3 cells (4096 atoms); reference = the oracle's run
     st, tname = structures.config(2, small=True)
     t = builtin_params(tname)
     cfg = RunConfig(dt=1.0, steps=1000, skin=0.3, rebuild_every=10)
-    rec = run_nve_device(st.copy(), t, cfg, precision=precision, record_every=1)
+    rec = run_nve_device(st.copy(), t, cfg, precision=precision, record_every=1, loop=loop)
+    assert rec["loop"] == loop
     ref = oracle_mod.run_nve(st.positions, st.velocities, st.species, st.masses,
                              st.box.lengths, st.box.periodic, t, dt=1.0, steps=1000, skin=0.3,
                              threads=8, rebuild_every=10)
@@ -69,3 +74,67 @@ def test_1000_step_drift_comparable_to_reference(oracle_mod, precision):
     if precision == "double":
         # early steps agree closely before chaos amplifies round-off
         assert np.max(np.abs(rec["total"][:50] - ref["total"][:50])) <= 1e-8 * abs(ref["total"][0])
+
+
+def _run_both(st, t, cfg, **kw):
+    a = run_nve_device(st.copy(), t, cfg, loop="graph", **kw)
+    b = run_nve_device(st.copy(), t, cfg, loop="step", **kw)
+    assert a["loop"] == "graph" and b["loop"] == "step"
+    return a, b
+
+
+@pytest.mark.parametrize("scatter", ["atomic", "gather"])
+def test_graph_loop_matches_step_loop_si(scatter):
+    # device-side rebuild decision + rebuild inside the graph == host-driven loop
+    st, tname = structures.config(2, small=True)
+    t = builtin_params(tname)
+    cfg = RunConfig(dt=1.0, steps=300, skin=0.3, rebuild_every=0)
+    a, b = _run_both(st, t, cfg, scatter=scatter, record_every=1)
+    assert a["rebuilds"] == b["rebuilds"] and a["rebuilds"] > 5
+    scale = abs(b["total"][0])
+    assert np.max(np.abs(a["total"] - b["total"])) <= 1e-9 * scale
+    assert np.abs(a["positions"] - b["positions"]).max() <= 1e-7
+    if scatter == "gather":
+        # deterministic forces and a deterministic (radix-sorted) chunk plan
+        c = run_nve_device(st.copy(), t, cfg, loop="graph", scatter=scatter, record_every=1)
+        assert np.array_equal(c["positions"], a["positions"])
+
+
+@pytest.mark.parametrize("precision", ["double", "single"])
+def test_graph_loop_matches_step_loop_sic(precision):
+    # two species: the species-pair compute filter is rebuilt on the device
+    st, tname = structures.config(3, small=True)
+    t = builtin_params(tname)
+    cfg = RunConfig(dt=0.5, steps=200, skin=0.3, rebuild_every=10)
+    a, b = _run_both(st, t, cfg, precision=precision, record_every=5)
+    assert a["rebuilds"] == b["rebuilds"] >= 20
+    scale = abs(b["total"][0])
+    tol = 1e-9 if precision == "double" else 1e-5
+    assert np.max(np.abs(a["total"] - b["total"])) <= tol * scale
+
+
+def test_graph_loop_overflow_replay():
+    # zero spare capacity: the first rebuild that grows the list overflows,
+    # the run restarts from its entry state with regrown buffers
+    from paper_1710_00882_b200 import _native
+    st, tname = structures.config(2, small=True)
+    t = builtin_params(tname)
+    cfg = RunConfig(dt=1.0, steps=200, skin=0.3)
+    ctx = _native.default_context(0)
+    ctx.set_option(_native.OPT_LIST_MARGIN, 0)
+    try:
+        a = run_nve_device(st.copy(), t, cfg, loop="graph", record_every=1)
+    finally:
+        ctx.set_option(_native.OPT_LIST_MARGIN, 25)
+    b = run_nve_device(st.copy(), t, cfg, loop="step", record_every=1)
+    assert a["rebuilds"] >= b["rebuilds"]
+    assert np.max(np.abs(a["total"] - b["total"])) <= 1e-9 * abs(b["total"][0])
+
+
+def test_graph_loop_free_axis_falls_back():
+    g, st, t = si512_state()
+    st.box = SimulationBox(st.box.lengths, (True, True, False))
+    rec = run_nve_device(st, t, RunConfig(dt=1.0, steps=5, skin=0.3), loop="auto")
+    assert rec["loop"] == "step"
+    with pytest.raises(RuntimeError):
+        run_nve_device(st, t, RunConfig(dt=1.0, steps=5, skin=0.3), loop="graph")
