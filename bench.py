@@ -45,21 +45,40 @@ sys.path.insert(0, ROOT)
 METRIC = "Tersoff atom-steps/s (E+F evals)"
 UNIT = "atom-steps/s"
 
-# fp64-weighted op counts of the reference ScalarOpt
-# expression tree (add/mul = 1, div 15, sqrt 13, exp 31, sin = cos 26, pow 125)
-FLOPS_PAIR = 19 + 25 + 3 * 15 + 2 * 31 + 4 * 125 + 8 + 13   # + distance
-FLOPS_TRIP = 32 + 55 + 4 * 15 + 31
-FLOPS_TAPER = 2 + 3 + 15 + 26 + 26                           # per tapered f_C
+# the reference ScalarOpt expression tree charged once per
+# live pair / triplet, math-library calls weighted by their dynamic flop counts
+# on sm_100a (ncu, tools/native/op_weights.cu -> profiles/roofline.json);
+# the static SASS counts of SURVEY 8(d) are the fallback.
+_W_STATIC = {"fp64": {"div": 15, "sqrt": 13, "exp": 31, "sin": 26, "cos": 26, "pow": 125},
+             "fp32": {"div": 10, "sqrt": 5, "exp": 10, "sin": 20, "cos": 20, "pow": 63}}
+
+
+def _op_weights():
+    try:
+        with open(os.path.join(ROOT, "profiles", "roofline.json")) as fh:
+            w = json.load(fh)["weights"]
+        return {p: {k: float(w[p][k]) for k in _W_STATIC[p]} for p in _W_STATIC}, "ncu-dynamic"
+    except (OSError, KeyError, ValueError):
+        return _W_STATIC, "static-sass"
+
+
+OP_WEIGHTS, OP_WEIGHTS_SOURCE = _op_weights()
+
+
+def _costs(w, distance):
+    pair = 19 + 25 + 3 * w["div"] + 2 * w["exp"] + 4 * w["pow"] + (8 + w["sqrt"] if distance else 0)
+    trip = 32 + 55 + 4 * w["div"] + w["exp"]
+    taper = 2 + 3 + w["div"] + w["sin"] + w["cos"]  # per tapered f_C
+    return pair, trip, taper
 
 
 def _jsonable(o):
     return o.item() if hasattr(o, "item") else str(o)
 
 
-# fp32-weighted counterparts (div 10, sqrt ~5, exp 10, pow 63, sin = cos 20)
-FLOPS32_PAIR = 19 + 25 + 3 * 10 + 2 * 10 + 4 * 63
-FLOPS32_TRIP = 32 + 55 + 4 * 10 + 10
-FLOPS32_TAPER = 2 + 3 + 10 + 20 + 20
+FLOPS_PAIR, FLOPS_TRIP, FLOPS_TAPER = _costs(OP_WEIGHTS["fp64"], True)
+# mixed mode: the distance stays fp64 and is not charged to the fp32 pipe
+FLOPS32_PAIR, FLOPS32_TRIP, FLOPS32_TAPER = _costs(OP_WEIGHTS["fp32"], False)
 
 
 def algorithmic_flops32(stats):
@@ -509,7 +528,11 @@ def gpu_arm(args):
                      "kernel_ms": kern_ms,
                      "flops_per_launch": flops,
                      "flop_convention": "SURVEY 8(d): reference ScalarOpt expression tree "
-                                        "charged once per live pair and live triplet",
+                                        "charged once per live pair and live triplet; "
+                                        f"library-call weights {OP_WEIGHTS_SOURCE} "
+                                        "(profiles/roofline.json)",
+                     "flops_per_unit": {"pair": FLOPS_PAIR, "triplet": FLOPS_TRIP,
+                                        "taper": FLOPS_TAPER},
                      "peak_source": peak["source"] if peak else None,
                      "counts": {"live_pairs": int(st[2]), "live_triplets": int(st[3]),
                                 "taper_pairs": int(st[4]), "taper_triplets": int(st[5]),

@@ -181,6 +181,12 @@ int tb_md_step(tb_context *ctx, tb_nlist *nl, int64_t n, double *d_positions,
 int tb_nlist_rebuild_device(tb_context *ctx, tb_nlist *nl, const double *d_positions,
                             const int32_t *d_species, int scatter);
 
+/* Warp-chunk layout of the list the Tersoff kernel runs on: *nchunks warps
+ * of 32 lanes, *lanes_used of them holding a list entry (lane occupancy,
+ * the B200 counterpart of the reference's lane_active / lane_total,
+ * kernels.py:80-92).  Zero chunks when the general tile kernel is used. */
+int tb_nlist_lanes(const tb_nlist *nl, int64_t *nchunks, int64_t *lanes_used);
+
 /* Device-resident NVE run: `steps` velocity-Verlet steps (same semantics as
  * tb_md_step: skin/2 trigger plus a fixed cadence when rebuild_every > 0,
  * system.py:355-380, 427-460) as ONE CUDA-graph launch with no host

@@ -53,6 +53,7 @@ SIGNATURES = {
     "tb_md_run": (_I, [_P, _P, _I64, _P, _P, _P, _P, _P, _D, _D, _D, _D, _I, _I, _I, _I64, _I,
                        _P, _P, _P]),
     "tb_nlist_rebuild_device": (_I, [_P, _P, _P, _P, _I]),
+    "tb_nlist_lanes": (_I, [_P, _P, _P]),
     "tb_profile": (_I, [_P, _I]),
     "tb_profile_read": (_I, [_P, _P, _P]),
     "tb_measure_peak": (_I, [_P, _I, ctypes.POINTER(_D)]),

@@ -104,6 +104,7 @@ struct tb_nlist {
   bool rev_valid = false;
   int nchunks = 0;  // > 0: warp-chunk fast path available (max_row <= 32)
   int n_empty = 0;  // atoms with empty rows: sorted_atoms[0, n_empty)
+  int64_t lanes_used = 0;  // warp-chunk lanes holding an entry (of 32 * nchunks)
   // capacities for the device-resident rebuild (tb_md_run): entry-sized
   // buffers hold ecap entries, the lane table ccap warp chunks
   double margin = -1.0;  // < 0: the context's list margin at the next build
@@ -469,6 +470,8 @@ static int build_chunks(tb_context *ctx, tb_nlist *nl, const int *row_len, const
   }
   plan.chunk_base[33] = chunks;
   nl->n_empty = hist[0];
+  nl->lanes_used = 0;
+  for (int L = 1; L <= 32; ++L) nl->lanes_used += (int64_t)L * hist[L];
   nl->ccap = chunks + (int64_t)(nl->margin * (double)chunks) + (nl->margin > 0 ? 64 : 0);
   if (chunks > 0) {
     CK(nl->lanes.ensure(sizeof(int4) * 32 * (size_t)nl->ccap));
@@ -734,6 +737,13 @@ extern "C" int tb_nlist_info(const tb_nlist *nl, int64_t *n_atoms, int64_t *n_en
   if (n_atoms) *n_atoms = nl->n;
   if (n_entries) *n_entries = nl->entries;
   if (max_row) *max_row = nl->max_row;
+  return TB_OK;
+}
+
+extern "C" int tb_nlist_lanes(const tb_nlist *nl, int64_t *nchunks, int64_t *lanes_used) {
+  if (!nl || !nchunks || !lanes_used) return TB_ERR_ARG;
+  *nchunks = nl->nchunks;
+  *lanes_used = nl->nchunks > 0 ? nl->lanes_used : 0;
   return TB_OK;
 }
 
@@ -1613,6 +1623,7 @@ extern "C" int tb_md_run(tb_context *ctx, tb_nlist *nl, int64_t n, double *d_pos
       nl->max_row = hp.max_row;
       nl->nchunks = hp.nchunks;
       nl->n_empty = hp.n_empty;
+      nl->lanes_used = hp.lanes_used;
       if (hp.rebuilds > 0 && scatter != TB_SCATTER_GATHER) nl->rev_valid = false;
       if (hp.rebuilds > 0 && filter_wanted) nl->fbuf_zero = scatter == TB_SCATTER_GATHER;
       if (rebuilds) *rebuilds = hp.rebuilds + extra;
@@ -1665,6 +1676,7 @@ extern "C" int tb_nlist_rebuild_device(tb_context *ctx, tb_nlist *nl, const doub
   nl->max_row = hp.max_row;
   nl->nchunks = hp.nchunks;
   nl->n_empty = hp.n_empty;
+  nl->lanes_used = hp.lanes_used;
   nl->rev_valid = scatter == TB_SCATTER_GATHER;
   nl->fbuf_zero = filter && scatter == TB_SCATTER_GATHER;
   if (filter) nl->filter_species = d_species;

@@ -31,7 +31,7 @@ struct DevPlan {
   int list_overflow;      // OVF_ENTRIES: the fill pass must not write
   int step, target;       // steps taken / to take in this launch
   int rebuilds;
-  int pad;
+  int lanes_used;         // sum_L L * hist[L] of the chunked rows
   unsigned long long drift_bits;  // max |x - x_ref|^2 of this step (bits; r^2 >= 0)
   int hist[34];
   int bucket_start[34], chunk_base[34];
@@ -108,13 +108,14 @@ __global__ void k_plan(DevPlan *__restrict__ plan, const int *__restrict__ offse
     }
   }
   if (plan->max_row > 32) ovf |= OVF_ROW;
-  int start = plan->hist[0], chunks = 0;
+  int start = plan->hist[0], chunks = 0, used = 0;
   plan->bucket_start[0] = 0;
   plan->chunk_base[0] = 0;
   for (int L = 1; L <= 32; ++L) {
     plan->bucket_start[L] = start;
     plan->chunk_base[L] = chunks;
     start += plan->hist[L];
+    used += L * plan->hist[L];
     chunks += (plan->hist[L] + 32 / L - 1) / (32 / L);
   }
   plan->bucket_start[33] = start;
@@ -123,6 +124,7 @@ __global__ void k_plan(DevPlan *__restrict__ plan, const int *__restrict__ offse
   plan->overflow = ovf;
   plan->nchunks = ovf ? 0 : chunks;
   plan->n_empty = ovf ? 0 : plan->hist[0];
+  plan->lanes_used = used;
 }
 
 // after an entries overflow every row is made empty, so all later readers of

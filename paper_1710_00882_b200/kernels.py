@@ -14,6 +14,7 @@ evaluates E, F, per-atom E and the virial, and the results come back.
 There is no CPU path: a missing library raises NativeUnavailable.
 """
 
+import ctypes
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -48,6 +49,20 @@ class KernelVariant:
 
     def describe(self):
         return f"{self.tag}[sm_100a,{self.precision},{self.scatter}]"
+
+    @property
+    def backend(self):
+        """Execution model in the shape of the reference's simd.Backend
+        (simd.py:151-181): name, lane width (a warp), precision."""
+        return DeviceBackend("sm_100a", 32, self.precision)
+
+
+@dataclass(frozen=True)
+class DeviceBackend:
+    name: str
+    width: int
+    precision: str
+    strict: bool = False
 
 
 def make_variant(tag="B200", backend=None, width=None, precision="double", strict=False,
@@ -126,8 +141,11 @@ def compute(state, nl, params, variant=None, threads=1, out=None):
                                  _native.SCATTER[variant.scatter], _native.ptr(forces),
                                  _native.ptr(per_atom), _native.ptr(energy), _native.ptr(virial),
                                  _native.ptr(stats)), "tb_compute")
+    chunks, used = ctypes.c_int64(), ctypes.c_int64()
+    ctx.check(ctx.lib.tb_nlist_lanes(nl._nl.handle, ctypes.byref(chunks), ctypes.byref(used)),
+              "tb_nlist_lanes")
     st = {"zeta_visits": int(stats[0]), "gathers": 0,
-          "lane_active": int(stats[1]), "lane_total": 0,
+          "lane_active": int(used.value), "lane_total": 32 * int(chunks.value),
           "packed_pairs": int(stats[1]), "live_pairs": int(stats[2]),
           "live_triplets": int(stats[3]), "taper_pairs": int(stats[4]),
           "taper_triplets": int(stats[5])}
@@ -148,6 +166,6 @@ def count_flops_and_visits(state, nl, params, variant):
     """Run once and report the work counters (kernels.py:537-544)."""
     res = compute(state, nl, params, variant)
     return {"zeta_visits": res.stats["zeta_visits"], "gathers": 0,
-            "lane_utilization": None,
+            "lane_utilization": res.lane_utilization,
             "live_pairs": res.stats["live_pairs"],
             "live_triplets": res.stats["live_triplets"]}

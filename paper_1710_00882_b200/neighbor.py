@@ -111,15 +111,17 @@ def torch_int32():
     return torch.int32
 
 
-def build_neighbor_list(state, r_cut, skin=0.3, device=None):
-    """Full list at build_cutoff = r_cut + skin (neighbor.py:194-217)."""
+def build_neighbor_list(state, r_cut, skin=0.3, device=None, reuse=None):
+    """Full list at build_cutoff = r_cut + skin (neighbor.py:194-217).
+    reuse (extension): a NeighborList whose device buffers are rebuilt in
+    place (ForceField keeps one list alive across rebuilds)."""
     if skin < 0:
         raise ConfigurationError(f"negative skin {skin:g}")
     pos = _positions(state)
     if device is None:
         device = 0 if isinstance(pos, np.ndarray) else pos.device.index
     ctx = _native.default_context(device)
-    nl = _native.NList(ctx)
+    nl = reuse._nl if reuse is not None and reuse._nl.ctx is ctx else _native.NList(ctx)
     L, per = _box_args(state.box)
     n = int(pos.shape[0])
     ctx.check(ctx.lib.tb_build_neighbors(ctx.handle, nl.handle, n, _native.ptr(pos),

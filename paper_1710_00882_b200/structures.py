@@ -17,7 +17,7 @@ on the (1/4,1/4,1/4)-shifted half.  Velocities follow seed_velocities
 
 import numpy as np
 
-from .system import ACCEL, KB_EV, SimulationBox, SimulationState
+from .system import SimulationBox, SimulationState, seed_velocities  # noqa: F401
 
 _DIAMOND_BASIS = np.array([
     [0.00, 0.00, 0.00], [0.00, 0.50, 0.50],
@@ -95,17 +95,6 @@ def gen_disordered(n, density=0.05, d_min=2.0, seed=1004, symbol="Si",
     box = SimulationBox([L, L, L], periodic=(True, True, True))
     return SimulationState(pos, box, species=np.zeros(n, np.int64),
                            masses=np.array([MASSES[symbol]]), symbols=(symbol,))
-
-
-def seed_velocities(state, temperature, rng=0):
-    """Maxwell-Boltzmann velocities, zero net momentum (system.py:149-157)."""
-    rng = np.random.default_rng(rng)
-    m = state.atom_masses
-    sigma = np.sqrt(KB_EV * temperature * ACCEL / m)
-    state.velocities = rng.normal(size=(state.natoms, 3)) * sigma[:, None]
-    p = (m[:, None] * state.velocities).sum(axis=0)
-    state.velocities -= p / m.sum()
-    return state
 
 
 # name -> (builder, parameter set, velocity temperature/seed)

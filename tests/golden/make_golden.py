@@ -24,6 +24,8 @@ Fixtures
   disordered.npz   1000-atom min-separation random Si packing (ScalarOpt)
   nl_frames.npz    neighbour-list edge cases (random 200-atom frames with
                    ppp / fff / ffp periodicity; test_neighbor.py:16-82)
+  harness.npz      gen_nanotube / gen_diamond positions, write_xyz text, a
+                   40-step run_stretch record, the bench CSV header
 """
 
 import os
@@ -174,7 +176,48 @@ def nl_frames():
     np.savez(os.path.join(HERE, "nl_frames.npz"), **out)
 
 
+def harness():
+    """Structure generators, XYZ text, the stretch driver and the bench CSV
+    schema of the reference (system.py:164-307, 478-550; bench.py:23-25)."""
+    import tempfile
+
+    from tersoffmd import bench as ref_bench
+    from tersoffmd import system as ref_system
+    out = {}
+    for n, cells in [(3, 1), (5, 10), (8, 4)]:
+        st = ref_system.gen_nanotube(n, cells)
+        out[f"tube_{n}_{cells}_positions"] = st.positions
+        out[f"tube_{n}_{cells}_lengths"] = st.box.lengths
+    dia = ref_system.gen_diamond(3)
+    out["diamond3_positions"] = dia.positions
+    out["diamond3_lengths"] = dia.box.lengths
+    st = ref_system.gen_nanotube(5, 2)
+    st.time = 12.5
+    with tempfile.TemporaryDirectory() as d:
+        path = os.path.join(d, "t.xyz")
+        ref_system.write_xyz(path, st)
+        ref_system.write_xyz(path, ref_system.gen_diamond(1), append=True)
+        out["xyz_text"] = np.array(open(path).read())
+    # stretch run on a (5,5) tube, carbon table (cli run --pull-speed)
+    table = R.builtin_params("C")
+    st = ref_system.gen_nanotube(5, 4)
+    ref_system.seed_velocities(st, 300.0, 7)
+    out["stretch_positions0"] = st.positions.copy()
+    out["stretch_velocities0"] = st.velocities.copy()
+    cfg = ref_system.RunConfig(dt=0.5, steps=40, variant=SCALAR, skin=0.3,
+                               stretch=ref_system.StretchSpec(axis=2, speed=0.02))
+    rec = ref_system.run_stretch(st, table, cfg)
+    for k in ("potential", "kinetic", "total", "strain", "force_sum_max"):
+        out[f"stretch_{k}"] = np.asarray(rec[k])
+    out["stretch_grip_atoms"] = np.array(rec["grip_atoms"])
+    out["stretch_rebuilds"] = rec["rebuilds"]
+    out["stretch_final_positions"] = st.positions
+    out["csv_fields"] = np.array(",".join(ref_bench.CSV_FIELDS))
+    np.savez(os.path.join(HERE, "harness.npz"), **out)
+
+
 def main():
+    harness()
     dimer()
     clusters()
     si512()
