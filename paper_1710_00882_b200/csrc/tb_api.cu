@@ -187,7 +187,7 @@ static Box make_box(const double *L, const int *per) {
 
 static inline int nblk(int64_t n, int t) { return (int)((n + t - 1) / t); }
 
-constexpr int SCAN_G = 8;  // lanes per atom in the list scan
+constexpr int SCAN_G = 8;  // lanes per atom in the CSR compaction
 
 // ---------------------------------------------------------------------------
 // parameter tables (potential.py:127-155 column order)
@@ -632,6 +632,12 @@ extern "C" int tb_build_neighbors_owned(tb_context *ctx, tb_nlist *nl, int64_t n
     g.nc[ax] = (int)nc;
     ncell *= nc;
   }
+  // stencil-implied minimum images (k_nl_cells): every periodic axis
+  // needs >= 4 cells (merged z-runs never mix images) strictly wider than bc
+  // (a pair within bc then lies in adjacent unwrapped cells)
+  g.stencil_image = nl->per[0] && nl->per[1] && nl->per[2] ? 2 : 1;
+  for (int ax = 0; ax < 3; ++ax)
+    if (nl->per[ax] && !(g.nc[ax] >= 4 && g.width[ax] > bc * (1.0 + 1e-9))) g.stencil_image = 0;
   if (ncell > (int64_t)1 << 28)
     return fail(ctx, TB_ERR_CONFIG, "cell grid of %lld cells is too large", (long long)ncell);
 
@@ -642,18 +648,19 @@ extern "C" int tb_build_neighbors_owned(tb_context *ctx, tb_nlist *nl, int64_t n
   CK(nl->cell_atoms.ensure(sizeof(int) * std::max(N, 1)));
   CK(nl->row_count.ensure(sizeof(int) * (N + 1)));
   CK(nl->offsets.ensure(sizeof(int) * (N + 1)));
-  CK(nl->maxrow.ensure(sizeof(int)));
+  CK(nl->maxrow.ensure(2 * sizeof(int)));  // [max row, unwrapped-coordinate flag]
   CK(nl->ref_pos.ensure(sizeof(double) * 3 * std::max(N, 1)));
 
   CK(nl->hist.ensure(sizeof(int) * 34));
   CK(nl->scratch.ensure(sizeof(int) * TMPW * (size_t)std::max(N, 1)));
   CK(cudaMemsetAsync(nl->cell_count.p, 0, sizeof(int) * (ncell + 1), ctx->stream));
-  CK(cudaMemsetAsync(nl->maxrow.p, 0, sizeof(int), ctx->stream));
+  CK(cudaMemsetAsync(nl->maxrow.p, 0, 2 * sizeof(int), ctx->stream));
   CK(cudaMemsetAsync(nl->hist.p, 0, sizeof(int) * 34, ctx->stream));
   CK(cudaMemsetAsync(nl->row_count.p, 0, sizeof(int) * (N + 1), ctx->stream));
   if (N) {
     k_cell_index<<<nblk(N, 256), 256, 0, ctx->stream>>>(N, d_pos, g, nl->atom_cell.as<int>(),
-                                                         nl->cell_count.as<int>());
+                                                         nl->cell_count.as<int>(),
+                                                         nl->maxrow.as<int>() + 1);
     CK(cudaGetLastError());
   }
   rc = exclusive_scan(ctx, nl->cell_count.as<int>(), nl->cell_start.as<int>(), ncell + 1);
@@ -672,10 +679,10 @@ extern "C" int tb_build_neighbors_owned(tb_context *ctx, tb_nlist *nl, int64_t n
     CK(cudaGetLastError());
     // single pass: rows of <= TMPW entries land in the scratch rows, counts,
     // max row and the row-length histogram (for the warp chunks) come along
-    k_nl_scan_tmp<SCAN_G><<<nblk((int64_t)N * SCAN_G, 256), 256, 0, ctx->stream>>>(
-        N, (int)n_owned, nl->cpos.as<double4>(), g, bc * bc, nl->atom_cell.as<int>(),
-        nl->cell_start.as<int>(), nl->cell_atoms.as<int>(), nl->row_count.as<int>(),
-        nl->scratch.as<int>(), nl->maxrow.as<int>(), nl->hist.as<int>());
+    k_nl_cells<<<nblk(ncell, 8), 256, 0, ctx->stream>>>(
+        (int)ncell, (int)n_owned, nl->cpos.as<double4>(), g, bc * bc, nl->cell_start.as<int>(),
+        nl->row_count.as<int>(), nl->scratch.as<int>(), nl->maxrow.as<int>(), nl->hist.as<int>(),
+        nl->maxrow.as<int>() + 1);
     CK(cudaGetLastError());
   }
   rc = exclusive_scan(ctx, nl->row_count.as<int>(), nl->offsets.as<int>(), N + 1);
@@ -1306,7 +1313,7 @@ static int enqueue_rebuild_device(tb_context *ctx, tb_nlist *nl, const double *d
   k_plan_reset<<<1, 64, 0, st>>>(plan, 1);
   CK(cudaMemsetAsync(nl->cell_count.p, 0, sizeof(int) * (nl->ncell + 1), st));
   k_cell_index<<<nblk(N, 256), 256, 0, st>>>(N, d_pos, g, nl->atom_cell.as<int>(),
-                                               nl->cell_count.as<int>());
+                                               nl->cell_count.as<int>(), &plan->unwrapped);
   int rc = exclusive_scan(ctx, nl->cell_count.as<int>(), nl->cell_start.as<int>(), nl->ncell + 1);
   if (rc) return rc;
   CK(cudaMemcpyAsync(nl->cell_count.p, nl->cell_start.p, sizeof(int) * (nl->ncell + 1),
@@ -1316,10 +1323,10 @@ static int enqueue_rebuild_device(tb_context *ctx, tb_nlist *nl, const double *d
   k_cell_gather<<<nblk(N, 256), 256, 0, st>>>(N, d_pos, nl->cell_atoms.as<int>(),
                                                 nl->cpos.as<double4>());
   const double bc2 = nl->bc * nl->bc;
-  k_nl_scan_tmp<SCAN_G><<<nblk((int64_t)N * SCAN_G, 256), 256, 0, st>>>(
-      N, N, nl->cpos.as<double4>(), g, bc2, nl->atom_cell.as<int>(), nl->cell_start.as<int>(),
-      nl->cell_atoms.as<int>(), nl->row_count.as<int>(), nl->scratch.as<int>(), &plan->max_row,
-      plan->hist);
+  k_nl_cells<<<nblk(nl->ncell, 8), 256, 0, st>>>(
+      (int)nl->ncell, N, nl->cpos.as<double4>(), g, bc2, nl->cell_start.as<int>(),
+      nl->row_count.as<int>(), nl->scratch.as<int>(), &plan->max_row, plan->hist,
+      &plan->unwrapped);
   CK(cudaGetLastError());
   rc = exclusive_scan(ctx, nl->row_count.as<int>(), nl->offsets.as<int>(), N + 1);
   if (rc) return rc;
@@ -1356,9 +1363,13 @@ static int enqueue_rebuild_device(tb_context *ctx, tb_nlist *nl, const double *d
     if (scatter == TB_SCATTER_GATHER)
       CK(cudaMemsetAsync(nl->fbuf.p, 0, sizeof(double) * 3 * (size_t)ecap, st));
   }
-  rc = radix_sort_rows(ctx, nl, row_len);
-  if (rc) return rc;
-  k_fill_lanes_dev<<<ccap, 32, 0, st>>>(plan, nl->sorted_atoms.as<int>(), loff, cent,
+  if (scatter == TB_SCATTER_GATHER) {
+    rc = radix_sort_rows(ctx, nl, row_len);  // stable: reproducible chunk layout
+    if (rc) return rc;
+  } else {
+    k_bucket_rows<<<nblk(N, 256), 256, 0, st>>>(N, row_len, plan, nl->sorted_atoms.as<int>());
+  }
+  k_fill_lanes_dev<<<nblk(ccap, 8), 256, 0, st>>>(plan, nl->sorted_atoms.as<int>(), loff, cent,
                                           nl->nbr.as<int>(), nl->lanes.as<int4>());
   if (scatter == TB_SCATTER_GATHER)
     k_nl_reverse<<<nblk(N, 256), 256, 0, st>>>(N, nl->offsets.as<int>(), nl->nbr.as<int>(),

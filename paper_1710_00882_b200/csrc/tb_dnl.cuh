@@ -32,9 +32,12 @@ struct DevPlan {
   int step, target;       // steps taken / to take in this launch
   int rebuilds;
   int lanes_used;         // sum_L L * hist[L] of the chunked rows
+  int unwrapped;          // k_cell_index: a periodic coordinate outside [0, L]
+  int pad;
   unsigned long long drift_bits;  // max |x - x_ref|^2 of this step (bits; r^2 >= 0)
   int hist[34];
   int bucket_start[34], chunk_base[34];
+  int cursor[34];         // k_bucket_rows
 };
 
 // v += half F/m ; x += dt v ; wrap ; max drift^2 against the list snapshot
@@ -87,8 +90,14 @@ __global__ void k_md_decide(DevPlan *__restrict__ plan, double half_skin2, int r
 // reset the per-build counters (full) or only the histogram (filter pass)
 __global__ void k_plan_reset(DevPlan *__restrict__ plan, int full) {
   const int t = threadIdx.x;
-  if (t < 34) plan->hist[t] = 0;
-  if (full && t == 0) plan->max_row = 0;
+  if (t < 34) {
+    plan->hist[t] = 0;
+    plan->cursor[t] = 0;
+  }
+  if (full && t == 0) {
+    plan->max_row = 0;
+    plan->unwrapped = 0;
+  }
 }
 
 // chunk plan from the row-length histogram (one thread): buckets of rows of
@@ -134,12 +143,33 @@ __global__ void k_guard_offsets(int n, const DevPlan *__restrict__ plan, int *__
   if (i <= n && plan->list_overflow) offsets[i] = 0;
 }
 
-// one warp per chunk: lane -> {entry, i, j, L} from the device plan
-__global__ void k_fill_lanes_dev(const DevPlan *__restrict__ plan,
+// rows bucketed by length with one atomic cursor per length (atomic-scatter
+// runs only: the order inside a bucket is arbitrary; gather runs keep the
+// stable radix sort so that their energy sums are reproducible)
+__global__ void k_bucket_rows(int n, const int *__restrict__ row_len, DevPlan *__restrict__ plan,
+                              int *__restrict__ sorted_atoms) {
+  __shared__ int s_cnt[34], s_base[34];
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (threadIdx.x < 34) s_cnt[threadIdx.x] = 0;
+  __syncthreads();
+  int L = -1, slot = 0;
+  if (i < n) {
+    L = min(row_len[i], 33);
+    slot = atomicAdd(s_cnt + L, 1);  // block-local rank, one global atomic per bucket
+  }
+  __syncthreads();
+  if (threadIdx.x < 33 && s_cnt[threadIdx.x])
+    s_base[threadIdx.x] = atomicAdd(plan->cursor + threadIdx.x, s_cnt[threadIdx.x]);
+  __syncthreads();
+  if (L >= 0 && L <= 32) sorted_atoms[plan->bucket_start[L] + s_base[L] + slot] = i;
+}
+
+// one warp per chunk (8 chunks per block): lane -> {entry, i, j, L}
+__global__ void __launch_bounds__(256) k_fill_lanes_dev(const DevPlan *__restrict__ plan,
                                  const int *__restrict__ sorted_atoms,
                                  const int *__restrict__ offsets, const int *__restrict__ centry,
                                  const int *__restrict__ nbr, int4 *__restrict__ lanes) {
-  const int c = blockIdx.x, lane = threadIdx.x;
+  const int c = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
   if (c >= plan->nchunks) return;
   int L = 1;
   while (L < 32 && plan->chunk_base[L + 1] <= c) ++L;

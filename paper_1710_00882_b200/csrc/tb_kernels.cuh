@@ -93,6 +93,11 @@ struct Grid {
   int nc[3];
   double origin[3], width[3];
   Box box;
+  // >= 1: every periodic axis has >= 4 cells wider than the build cutoff, so
+  // a candidate's minimum image is the one its stencil cell implies (the list
+  // scan then skips the per-candidate rint); 2: and every axis is periodic
+  // (set by the host build)
+  int stencil_image;
 };
 
 // per-axis min/max of positions for free axes (neighbor.py:71-76)
@@ -142,11 +147,18 @@ __device__ __forceinline__ void cell_coords(const double *p, const Grid &g, int 
 }
 
 __global__ void k_cell_index(int n, const double *__restrict__ pos, Grid g,
-                             int *__restrict__ atom_cell, int *__restrict__ cell_count) {
+                             int *__restrict__ atom_cell, int *__restrict__ cell_count,
+                             int *__restrict__ unwrapped = nullptr) {
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   double p[3];
   load3(pos, i, p);
+  if (unwrapped) {  // a periodic coordinate outside [0, L]: images beyond +-1
+    bool out = false;
+#pragma unroll
+    for (int ax = 0; ax < 3; ++ax) out |= g.box.per[ax] && !(p[ax] >= 0.0 && p[ax] <= g.box.L[ax]);
+    if (out) atomicOr(unwrapped, 1);
+  }
   int c[3];
   cell_coords(p, g, c);
   int id = (c[0] * g.nc[1] + c[1]) * g.nc[2] + c[2];
@@ -190,8 +202,9 @@ __global__ void k_cell_gather(int n, const double *__restrict__ pos,
   int t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= n) return;
   const int i = cell_atoms[t];
+  // .w carries the atom index (bit pattern) for the list scan
   cpos[t] = make_double4(__ldg(pos + 3 * (int64_t)i), __ldg(pos + 3 * (int64_t)i + 1),
-                         __ldg(pos + 3 * (int64_t)i + 2), 0.0);
+                         __ldg(pos + 3 * (int64_t)i + 2), __longlong_as_double((long long)i));
 }
 
 // Stencil of cell `id`: distinct x and y cells (sx[nx], sy[ny]) and, per
@@ -230,16 +243,31 @@ __device__ __forceinline__ void make_stencil(int id, const Grid &g, Stencil &st)
         zs[v] = zs[v - 1];
         zs[v - 1] = tmp;
       }
-  st.nr = 0;
-#pragma unroll
-  for (int u = 0; u < 3; ++u) {
-    if (u >= nz) break;
-    if (st.nr > 0 && zs[u] == st.zhi[st.nr - 1] + 1) {
-      st.zhi[st.nr - 1] = zs[u];
+  // merge into runs of consecutive ids (static indices only: registers)
+  st.zlo[0] = st.zhi[0] = zs[0];
+  st.zlo[1] = st.zhi[1] = st.zlo[2] = st.zhi[2] = 0;
+  st.nr = 1;
+  if (nz > 1) {
+    if (zs[1] == st.zhi[0] + 1) {
+      st.zhi[0] = zs[1];
     } else {
-      st.zlo[st.nr] = zs[u];
-      st.zhi[st.nr] = zs[u];
-      ++st.nr;
+      st.zlo[1] = st.zhi[1] = zs[1];
+      st.nr = 2;
+    }
+  }
+  if (nz > 2) {
+    if (st.nr == 1) {
+      if (zs[2] == st.zhi[0] + 1) {
+        st.zhi[0] = zs[2];
+      } else {
+        st.zlo[1] = st.zhi[1] = zs[2];
+        st.nr = 2;
+      }
+    } else if (zs[2] == st.zhi[1] + 1) {
+      st.zhi[1] = zs[2];
+    } else {
+      st.zlo[2] = st.zhi[2] = zs[2];
+      st.nr = 3;
     }
   }
 }
@@ -318,61 +346,172 @@ __global__ void __launch_bounds__(128) k_nl_scan(int n, int n_owned, const doubl
 // TMPW), max_row and the row-length histogram.  k_nl_compact then sorts each
 // row and writes it to its CSR slot, so the list is identical to k_nl_scan's.
 constexpr int TMPW = 32;
-template <int G>
-__global__ void __launch_bounds__(256) k_nl_scan_tmp(int n, int n_owned,
-                                                     const double4 *__restrict__ cpos, Grid g,
-                                                     double bc2, const int *__restrict__ atom_cell,
-                                                     const int *__restrict__ cell_start,
-                                                     const int *__restrict__ cell_atoms,
-                                                     int *__restrict__ row_count,
-                                                     int *__restrict__ tmp,
-                                                     int *__restrict__ max_row,
-                                                     int *__restrict__ hist) {
+
+__device__ __forceinline__ double stencil_lq(int s, int c, const Grid &g, int ax) {
+  // cell s as seen from cell c: offsets beyond +-1 are wrapped neighbours
+  const int dl = s - c;
+  return dl > 1 ? g.box.L[ax] : (dl < -1 ? -g.box.L[ax] : 0.0);
+}
+
+// Cell-centric single-pass list scan (rows of <= TMPW entries): one warp per
+// cell.  Every atom of a cell shares the cell's stencil, so the warp builds
+// the stencil's candidate ranges once (lane = (x, y, z-run) of the 27-cell
+// stencil, compacted and prefix-summed), flattens them, and each lane then
+// tests one candidate against every atom of the cell (positions broadcast
+// from L1).  Hits go to the atom's scratch row tmp[i][TMPW] in candidate
+// order via full-warp ballots; k_nl_compact sorts the rows.  Outputs: the
+// CSR counts (row_count incl. rows longer than TMPW), max_row, histogram.
+// With g.stencil_image (and coordinates inside [0, L]) a candidate's
+// displacement takes the image its stencil cell implies, d = (x_j - x_i) -
+// L*q with q in {-1, 0, 1}: the same operations, hence the same bits, as the
+// reference's d - L*rint(d/L) (neighbor.py:36-43) whenever the two q agree,
+// which they do for every pair within the build cutoff (cells strictly wider
+// than bc, >= 4 per periodic axis); pairs farther apart are rejected either
+// way.  Otherwise every candidate takes the exact min_image.
+__global__ void __launch_bounds__(256) k_nl_cells(int ncell, int n_owned,
+                                                  const double4 *__restrict__ cpos, Grid g,
+                                                  double bc2, const int *__restrict__ cell_start,
+                                                  int *__restrict__ row_count,
+                                                  int *__restrict__ tmp, int *__restrict__ max_row,
+                                                  int *__restrict__ hist,
+                                                  const int *__restrict__ unwrapped) {
   __shared__ int s_hist[34];
   if (threadIdx.x < 34) s_hist[threadIdx.x] = 0;
   __syncthreads();
-  const int lane = threadIdx.x & 31, gl = lane % G;
-  const unsigned gmask = (G == 32 ? 0xffffffffu : ((1u << G) - 1u)) << (lane - gl);
-  const int t = (blockIdx.x * blockDim.x + threadIdx.x) / G;
-  int cnt = 0;
-  if (t < n) {
-    const int i = cell_atoms[t];
-    if (i < n_owned) {
-      const double4 pi = cpos[t];
-      const double xi[3] = {pi.x, pi.y, pi.z};
-      Stencil sc;
-      make_stencil(atom_cell[i], g, sc);
-      int *row_out = tmp + (int64_t)i * TMPW;
-      for (int a = 0; a < sc.nx; ++a)
-        for (int b = 0; b < sc.ny; ++b) {
-          const int row = (sc.sx[a] * g.nc[1] + sc.sy[b]) * g.nc[2];
-          for (int r = 0; r < sc.nr; ++r) {
-            const int s0 = cell_start[row + sc.zlo[r]], s1 = cell_start[row + sc.zhi[r] + 1];
-            for (int sb = s0; sb < s1; sb += G) {
-              const int s = sb + gl;
-              bool hit = false;
-              if (s < s1 && s != t) {
-                const double4 pj = cpos[s];
-                const double xj[3] = {pj.x, pj.y, pj.z};
-                double d[3];
-                hit = disp_r2(xi, xj, g.box, d) < bc2;
-              }
-              const unsigned bal = __ballot_sync(gmask, hit);
-              if (hit) {
-                const int at = cnt + __popc(bal & gmask & ((1u << lane) - 1u));
-                if (at < TMPW) row_out[at] = cell_atoms[s];
-              }
-              cnt += __popc(bal);
-            }
+  const bool stencil_image = g.stencil_image && !*unwrapped;
+  const int lane = threadIdx.x & 31;
+  const unsigned lt = (1u << lane) - 1u;
+  const int cell = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  int maxc = 0;
+  if (cell < ncell) {
+    const int c0 = cell_start[cell], nA = cell_start[cell + 1] - c0;
+    if (nA > 0) {
+      // ---- the stencil's candidate ranges, one per lane (lane < 27) ----
+      int s0 = 0, len = 0;
+      double lx = 0.0, ly = 0.0, lz = 0.0;
+      if (g.stencil_image == 2) {
+        // all axes periodic with >= 4 cells: lane = one stencil cell, offsets
+        // (a-1, b-1, r-1), the image each offset implies; cells are distinct
+        const int nyz = g.nc[1] * g.nc[2];
+        const int ccx = cell / nyz, rem = cell - ccx * nyz;
+        const int ccy = rem / g.nc[2], ccz = rem - ccy * g.nc[2];
+        if (lane < 27) {
+          const int a = lane / 9, b = (lane / 3) % 3, r = lane % 3;
+          int x = ccx + a - 1, y = ccy + b - 1, z = ccz + r - 1;
+          lx = x < 0 ? g.box.L[0] : (x >= g.nc[0] ? -g.box.L[0] : 0.0);
+          ly = y < 0 ? g.box.L[1] : (y >= g.nc[1] ? -g.box.L[1] : 0.0);
+          lz = z < 0 ? g.box.L[2] : (z >= g.nc[2] ? -g.box.L[2] : 0.0);
+          x += x < 0 ? g.nc[0] : (x >= g.nc[0] ? -g.nc[0] : 0);
+          y += y < 0 ? g.nc[1] : (y >= g.nc[1] ? -g.nc[1] : 0);
+          z += z < 0 ? g.nc[2] : (z >= g.nc[2] ? -g.nc[2] : 0);
+          const int id = (x * g.nc[1] + y) * g.nc[2] + z;
+          s0 = cell_start[id];
+          len = cell_start[id + 1] - s0;
+        }
+      } else {
+        Stencil sc;
+        make_stencil(cell, g, sc);
+        const int a = lane / 9, b = (lane / 3) % 3, r = lane % 3;
+        const bool on = lane < 27 && a < sc.nx && b < sc.ny && r < sc.nr;
+        if (on) {
+          const int cx = a == 0 ? sc.sx[0] : (a == 1 ? sc.sx[1] : sc.sx[2]);
+          const int cy = b == 0 ? sc.sy[0] : (b == 1 ? sc.sy[1] : sc.sy[2]);
+          const int lo = r == 0 ? sc.zlo[0] : (r == 1 ? sc.zlo[1] : sc.zlo[2]);
+          const int hi = r == 0 ? sc.zhi[0] : (r == 1 ? sc.zhi[1] : sc.zhi[2]);
+          const int row = (cx * g.nc[1] + cy) * g.nc[2];
+          s0 = cell_start[row + lo];
+          len = cell_start[row + hi + 1] - s0;
+          if (stencil_image) {
+            const int ccx = cell / (g.nc[1] * g.nc[2]), ccy = (cell / g.nc[2]) % g.nc[1],
+                      ccz = cell % g.nc[2];
+            if (g.box.per[0]) lx = stencil_lq(cx, ccx, g, 0);
+            if (g.box.per[1]) ly = stencil_lq(cy, ccy, g, 1);
+            if (g.box.per[2]) lz = stencil_lq(lo, ccz, g, 2);
           }
         }
-    }
-    if (gl == 0) {
-      row_count[i] = cnt;
-      atomicAdd(s_hist + min(cnt, 33), 1);
+      }
+      // compact the non-empty ranges to lanes 0..nrg-1, prefix-sum their lengths
+      const unsigned ne = __ballot_sync(0xffffffffu, len > 0);
+      const int nrg = __popc(ne);
+      // gather range q to lane q: lane q reads from the lane of the q-th set bit
+      const unsigned fn = __fns(ne, 0, lane + 1);
+      const int from = fn < 32 ? (int)fn : 0;
+      s0 = __shfl_sync(0xffffffffu, s0, from);
+      len = __shfl_sync(0xffffffffu, len, from);
+      lx = __shfl_sync(0xffffffffu, lx, from);
+      ly = __shfl_sync(0xffffffffu, ly, from);
+      lz = __shfl_sync(0xffffffffu, lz, from);
+      if (lane >= nrg) len = 0;
+      int incl = len;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int v = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += v;
+      }
+      const int start = incl - len;  // first flattened candidate of range `lane`
+      const int total = __shfl_sync(0xffffffffu, incl, 31);
+      // ---- atoms of the cell in batches of 32: lane k counts atom k ----
+      for (int kb = 0; kb < nA; kb += 32) {
+        const int nk = min(32, nA - kb);
+        int cnt = 0;  // lane k: hits of atom kb + k
+        for (int base = 0; base < total; base += 32) {
+          const int c = base + lane;
+          // range of candidate c: ranges starting at or before c
+          const unsigned starts_here = __reduce_or_sync(
+              0xffffffffu, (lane < nrg && len > 0 && start >= base && start < base + 32)
+                               ? (1u << (start - base)) : 0u);
+          const int before = __popc(__ballot_sync(0xffffffffu, lane < nrg && start < base));
+          const int rid = before + __popc(starts_here & (lt | (1u << lane))) - 1;
+          const int rs0 = __shfl_sync(0xffffffffu, s0, rid & 31);
+          const int rst = __shfl_sync(0xffffffffu, start, rid & 31);
+          const double qx = __shfl_sync(0xffffffffu, lx, rid & 31);
+          const double qy = __shfl_sync(0xffffffffu, ly, rid & 31);
+          const double qz = __shfl_sync(0xffffffffu, lz, rid & 31);
+          const bool cand = c < total;
+          const int s = rs0 + (c - rst);
+          double4 pj = make_double4(0.0, 0.0, 0.0, 0.0);
+          if (cand) pj = cpos[s];
+          const double xj[3] = {pj.x, pj.y, pj.z};
+          for (int k = 0; k < nk; ++k) {
+            const int sk = c0 + kb + k;
+            const double4 pk = cpos[sk];  // same address across the warp: broadcast
+            const double xi[3] = {pk.x, pk.y, pk.z};
+            bool hit = false;
+            if (cand && s != sk) {
+              double d[3];
+              if (stencil_image) {
+                d[0] = __dsub_rn(__dsub_rn(xj[0], xi[0]), qx);
+                d[1] = __dsub_rn(__dsub_rn(xj[1], xi[1]), qy);
+                d[2] = __dsub_rn(__dsub_rn(xj[2], xi[2]), qz);
+                // the reference's r2 bit for bit: its rint(v/L) equals this q
+                // for every pair within the build cutoff (Grid::stencil_image)
+                hit = __dadd_rn(__dadd_rn(__dmul_rn(d[0], d[0]), __dmul_rn(d[1], d[1])),
+                                __dmul_rn(d[2], d[2])) < bc2;
+              } else {
+                hit = disp_r2(xi, xj, g.box, d) < bc2;
+              }
+            }
+            const unsigned bal = __ballot_sync(0xffffffffu, hit);
+            const int ik = (int)__double_as_longlong(pk.w);
+            const int ck = __shfl_sync(0xffffffffu, cnt, k);
+            if (hit && ik < n_owned) {
+              const int at = ck + __popc(bal & lt);
+              if (at < TMPW) tmp[(int64_t)ik * TMPW + at] = (int)__double_as_longlong(pj.w);
+            }
+            if (lane == k) cnt += __popc(bal);
+          }
+        }
+        if (lane < nk) {
+          const int ik = (int)__double_as_longlong(cpos[c0 + kb + lane].w);
+          const int v = ik < n_owned ? cnt : 0;  // ghosts (i >= n_owned) get empty rows
+          row_count[ik] = v;
+          atomicAdd(s_hist + min(v, 33), 1);
+          maxc = max(maxc, v);
+        }
+      }
     }
   }
-  const int m = __reduce_max_sync(0xffffffffu, cnt);
+  const int m = __reduce_max_sync(0xffffffffu, maxc);
   if (lane == 0 && m) atomicMax(max_row, m);
   __syncthreads();
   if (threadIdx.x < 34 && s_hist[threadIdx.x]) atomicAdd(hist + threadIdx.x, s_hist[threadIdx.x]);

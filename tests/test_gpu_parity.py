@@ -144,6 +144,23 @@ def test_configs_vs_oracle(oracle_mod, idx, precision, kernel_path):
         assert np.abs(r.virial - o["virial"]).max() <= 1e-9 * np.abs(o["virial"]).max()
 
 
+@pytest.mark.parametrize("shift", ["wrapped", "unwrapped"])
+def test_list_with_unwrapped_coordinates(oracle_mod, shift):
+    # the list scan takes each candidate's minimum image from its stencil cell
+    # only for coordinates inside [0, L]; images of unwrapped input (atoms
+    # several box lengths away) must still follow d - L*rint(d/L)
+    st, t = _config(2)
+    pos = st.positions.copy()
+    if shift == "unwrapped":
+        rng = np.random.default_rng(9)
+        pos += rng.integers(-2, 3, size=pos.shape) * st.box.lengths
+    fr = Frame(pos, st.box.lengths, st.box.periodic, st.species)
+    nl = B.build_neighbor_list(fr, t.r_cut, 0.3)
+    off, nb = oracle_mod.build_neighbor_list(pos, st.box.lengths, st.box.periodic, t.r_cut, 0.3,
+                                             threads=8)
+    assert np.array_equal(nl.offsets, off) and np.array_equal(nl.neighbors, nb)
+
+
 def test_total_force_vanishes_and_gather_deterministic(kernel_path):
     st, t = _config(4)
     nl = B.build_neighbor_list(st, t.r_cut, 0.3)
