@@ -499,6 +499,21 @@ def gpu_arm(args):
         step(prec)  # restore the fp64 result buffers
         torch.cuda.synchronize()
 
+    if args.extras and rank == 0 and args.config == 2:
+        # SURVEY 8(d) "full MD step": velocity Verlet + rebuilds amortised,
+        # BASELINE config 2 protocol, the whole run one CUDA-graph launch
+        extra["md"] = {}
+        for pname, pcode in (("double", 0), ("single", 1)):
+            r = md_measure(B, _native, ctx, state, table, dev, pcode, scat)
+            fl = algorithmic_flops(st) if pcode == 0 else algorithmic_flops32(st)
+            pk = peak if pcode == 0 else measure_peak(lib, ctx, 1)
+            r["roofline_frac"] = (fl / (r["ms_per_step"] / 1e3) / 1e12 / pk["tflops"]
+                                  if pk else None)
+            extra["md"][pname] = r
+        ctx.set_stream(stream.cuda_stream)
+        step(prec)
+        torch.cuda.synchronize()
+
     e2e = None
     if rank == 0:
         e2e = e2e_arm(args, B, state, table, nl, dev)
@@ -552,6 +567,66 @@ def gpu_arm(args):
     if ws > 1:
         torch.distributed.barrier()
         torch.distributed.destroy_process_group()
+
+
+def md_measure(B, _native, ctx, state, table, dev, precision, scat, steps=1000, warm=20):
+    """Device-resident NVE (tb_md_run): BASELINE config 2 protocol -- dt 1 fs,
+    skin 0.3, rebuild every 10 steps plus the skin/2 trigger -- timed with
+    CUDA events around one graph launch of `steps` steps after a `warm`-step
+    launch that captures the graph."""
+    import ctypes
+
+    import torch
+    from paper_1710_00882_b200.system import ACCEL
+    n = state.natoms
+    d = torch.device("cuda", dev)
+    pos = torch.from_numpy(state.positions.copy()).to(d)
+    vel = torch.from_numpy(state.velocities.copy()).to(d)
+    mass = torch.from_numpy(np.ascontiguousarray(state.atom_masses, dtype=np.float64)).to(d)
+    species = torch.from_numpy(state.species.astype(np.int32)).to(d)
+    forces = torch.empty((n, 3), dtype=torch.float64, device=d)
+    result = torch.zeros(8, dtype=torch.float64, device=d)
+    series = torch.zeros((steps // 100 + 1, 2), dtype=torch.float64, device=d)
+
+    class DS:
+        pass
+
+    ds = DS()
+    ds.positions, ds.species, ds.box = pos, species, state.box
+    s = torch.cuda.current_stream(d)
+    ctx.set_stream(s.cuda_stream)
+    nl = B.build_neighbor_list(ds, table.r_cut, 0.3, device=dev)
+    lib, P = ctx.lib, _native.ptr
+    ctx.check(lib.tb_compute_device(ctx.handle, nl._nl.handle, P(pos), P(species),
+                                    float(table.r_cut), precision, scat, P(forces), None,
+                                    P(result), None), "tb_compute_device")
+    nreb = ctypes.c_int64()
+
+    def run(k):
+        ctx.check(lib.tb_md_run(ctx.handle, nl._nl.handle, n, P(pos), P(vel), P(forces), P(mass),
+                                P(species), 1.0, float(ACCEL), float(table.r_cut), 0.3, 10,
+                                precision, scat, k, 100, P(series), P(result),
+                                ctypes.byref(nreb)), "tb_md_run")
+        return int(nreb.value)
+
+    run(warm)
+    torch.cuda.synchronize(d)
+    e0 = float(result[0]) + float(result[7])
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(s)
+    rebuilds = run(steps)
+    b.record(s)
+    torch.cuda.synchronize(d)
+    ms = a.elapsed_time(b)
+    e1 = float(result[0]) + float(result[7])
+    return {"value": n * steps / (ms / 1e3), "unit": UNIT, "steps": steps,
+            "ms_per_step": ms / steps, "rebuilds": rebuilds,
+            "rel_energy_change": abs(e1 - e0) / abs(e0),
+            "workload": f"config 2 NVE ({n} Si, 1000 K, dt 1 fs, skin 0.3, rebuild every 10 "
+                        f"steps + skin/2 trigger): velocity Verlet + device-side list rebuilds "
+                        f"+ E/F/virial per step, one CUDA-graph launch (tb_md_run)",
+            "l2": "not flushed: consecutive steps of one run",
+            "gpu_launches": "1 graph launch (WHILE/IF conditional nodes)"}
 
 
 def measure_peak(lib, ctx, precision):
