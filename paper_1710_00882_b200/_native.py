@@ -97,8 +97,9 @@ def ptr(a):
     if a is None:
         return None
     if isinstance(a, np.ndarray):
-        return a.ctypes.data_as(ctypes.c_void_p)
-    return ctypes.c_void_p(a.data_ptr())
+        # (the array interface is ~10x cheaper than ndarray.ctypes per call)
+        return a.__array_interface__["data"][0]
+    return a.data_ptr()
 
 
 class Context:

@@ -80,6 +80,7 @@ struct tb_context {
   double list_margin = 0.25;  // TB_OPT_LIST_MARGIN
   bool warp_per_chunk = getenv("TB_WARP_PER_CHUNK") != nullptr;
   bool no_filter = getenv("TB_NO_FILTER") != nullptr;  // disable the species-pair compute filter
+  bool err_unchecked = false;     // kernels may have raised error flags nobody read yet
   std::vector<int> last_species;  // host species of the last tb_compute (filter validity)
   const int *dplan = nullptr;  // tb_md_run capture: device {nchunks, n_empty}
   int last_blocks = 0;  // grid of the last Tersoff launch (partials to reduce)  // tb_set_option(TB_OPT_TILE_KERNEL): general tile kernel only
@@ -951,7 +952,9 @@ static ErrFlags err_init() {
 }
 
 static int reset_errors(tb_context *ctx) {
-  CK(ctx->errf.ensure(sizeof(ErrFlags)));
+  static_assert(sizeof(ErrFlags) <= 64, "result block layout");
+  CK(ctx->errf.ensure(256));  // [ErrFlags | tb_compute result @64 | stats @128]
+  ctx->err_unchecked = false;
   *ctx->h_err = err_init();
   CK(cudaMemcpyAsync(ctx->errf.p, ctx->h_err, sizeof(ErrFlags), cudaMemcpyHostToDevice,
                      ctx->stream));
@@ -977,6 +980,7 @@ static int enqueue_compute(tb_context *ctx, const tb_nlist *nl, const double *d_
     int rc = reset_errors(ctx);
     if (rc) return rc;
   }
+  ctx->err_unchecked = true;  // kernels below may raise flags (tb_compute reads them back)
   const int n = (int)nl->n;
   // tile sizing: atoms per block so that the tile's skin-list rows fit
   int C = SLOT_CAP;
@@ -1081,11 +1085,9 @@ static int enqueue_compute(tb_context *ctx, const tb_nlist *nl, const double *d_
 }
 
 // Map latched device error flags to the reference's exceptions and wording.
+// decode the flags the caller read back into h_err; resets them on error
 static int report_errors(tb_context *ctx, const tb_nlist *nl, const double *d_pos,
                          const int *d_species) {
-  CK(cudaMemcpyAsync(ctx->h_err, ctx->errf.p, sizeof(ErrFlags), cudaMemcpyDeviceToHost,
-                     ctx->stream));
-  CK(cudaStreamSynchronize(ctx->stream));
   ErrFlags e = *ctx->h_err;
   int rc = TB_OK;
   if (e.overflow) {
@@ -1134,7 +1136,10 @@ extern "C" int tb_compute(tb_context *ctx, const tb_nlist *nl, const double *pos
   CK(cudaSetDevice(ctx->device));
   const int64_t n = nl->n;
   if (n && (!positions || !species)) return fail(ctx, TB_ERR_ARG, "null positions/species");
-  int rc = reset_errors(ctx);
+  // error flags, result and counters share one small device block so that a
+  // call reads them back with one copy: [ErrFlags | result @64 | stats @128]
+  int rc = TB_OK;
+  if (ctx->err_unchecked || !ctx->errf.p) rc = reset_errors(ctx);
   if (rc) return rc;
   const double *d_pos = stage_in(ctx, positions, 3 * (size_t)n, ctx->pos, rc);
   if (rc) return rc;
@@ -1162,26 +1167,28 @@ extern "C" int tb_compute(tb_context *ctx, const tb_nlist *nl, const double *pos
     CK(ctx->per_atom.ensure(sizeof(double) * std::max<int64_t>(n, 1)));
     d_e = ctx->per_atom.as<double>();
   }
-  CK(ctx->result.ensure(sizeof(double) * 8));
-  CK(ctx->stats.ensure(sizeof(unsigned long long) * TB_NSTATS));
+  char *blk = ctx->errf.as<char>();
   rc = enqueue_compute(ctx, nl, d_pos, d_sp, r_cut, precision, scatter, d_f, d_e,
-                       ctx->result.as<double>(), ctx->stats.as<unsigned long long>());
+                       reinterpret_cast<double *>(blk + 64),
+                       reinterpret_cast<unsigned long long *>(blk + 128));
   if (rc) return rc;
   if (!f_dev && n)
     CK(cudaMemcpyAsync(forces, d_f, sizeof(double) * 3 * n, cudaMemcpyDeviceToHost, ctx->stream));
   if (per_atom && !e_dev && n)
     CK(cudaMemcpyAsync(per_atom, d_e, sizeof(double) * n, cudaMemcpyDeviceToHost, ctx->stream));
-  double *h = ctx->h_small;
-  CK(cudaMemcpyAsync(h, ctx->result.p, sizeof(double) * 7, cudaMemcpyDeviceToHost, ctx->stream));
-  unsigned long long *hs = reinterpret_cast<unsigned long long *>(h + 8);
-  CK(cudaMemcpyAsync(hs, ctx->stats.p, sizeof(unsigned long long) * TB_NSTATS,
-                     cudaMemcpyDeviceToHost, ctx->stream));
+  char *h = reinterpret_cast<char *>(ctx->h_small);
+  CK(cudaMemcpyAsync(h, blk, 128 + sizeof(unsigned long long) * TB_NSTATS, cudaMemcpyDeviceToHost,
+                     ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
+  ctx->err_unchecked = false;
+  memcpy(ctx->h_err, h, sizeof(ErrFlags));
   rc = report_errors(ctx, nl, d_pos, d_sp);
   if (rc) return rc;
-  *energy = h[0];
+  const double *hr = reinterpret_cast<const double *>(h + 64);
+  const unsigned long long *hs = reinterpret_cast<const unsigned long long *>(h + 128);
+  *energy = hr[0];
   if (virial)
-    for (int q = 0; q < 6; ++q) virial[q] = h[1 + q];
+    for (int q = 0; q < 6; ++q) virial[q] = hr[1 + q];
   if (stats)
     for (int q = 0; q < TB_NSTATS; ++q) stats[q] = (int64_t)hs[q];
   return TB_OK;
@@ -1196,6 +1203,13 @@ extern "C" int tb_compute_device(tb_context *ctx, const tb_nlist *nl, const doub
   return enqueue_compute(ctx, nl, d_positions, d_species, r_cut, precision, scatter, d_forces,
                          d_per_atom, d_result, reinterpret_cast<unsigned long long *>(d_stats));
 }
+
+#ifdef TB_TRACE
+extern "C" int tb_debug_trace(void *host, size_t bytes) {
+  return cudaMemcpyFromSymbol(host, tb::g_trace, std::min(bytes, sizeof(tb::g_trace))) == cudaSuccess
+             ? TB_OK : TB_ERR_CUDA;
+}
+#endif
 
 extern "C" int tb_check_errors(tb_context *ctx) {
   if (!ctx) return TB_ERR_ARG;
@@ -1215,6 +1229,7 @@ extern "C" int tb_check_errors(tb_context *ctx) {
     rc = fail(ctx, TB_ERR_INPUT, "atoms are coincident (list entry %u)",
               (unsigned)(e.coinc_key & 0xffffffffu));
   if (rc) reset_errors(ctx);
+  ctx->err_unchecked = false;
   return rc;
 }
 

@@ -24,6 +24,9 @@ namespace tb {
 #ifndef TB_WARP_MINB
 #define TB_WARP_MINB 4
 #endif
+#ifndef TB_WARP_MINB_F
+#define TB_WARP_MINB_F 4
+#endif
 constexpr int WNT = 128;  // threads per block of the warp kernel
 constexpr int WPB = WNT / 32;
 constexpr int QCAP = 4;   // k-iterations whose angular values are cached
@@ -311,37 +314,54 @@ __device__ __forceinline__ void chunk_body(const KArgs &a, const WArgs &w, const
     Sby += beta * bxy.y;
     Sbz += beta * bzr.x;
   }
+  double fx = 0.0, fy = 0.0, fz = 0.0;
   if (live) {
     const T inva = t_rcp(ra);
     const T ca = dvdr + Sal - Sc * inva;
-    const double fx = -(double)(ca * ex + inva * Sbx);
-    const double fy = -(double)(ca * ey + inva * Sby);
-    const double fz = -(double)(ca * ez + inva * Sbz);
+    fx = -(double)(ca * ex + inva * Sbx);
+    fy = -(double)(ca * ey + inva * Sby);
+    fz = -(double)(ca * ez + inva * Sbz);
     A.acc[32 * 1] += d[0] * fx;
     A.acc[32 * 2] += d[1] * fy;
     A.acc[32 * 3] += d[2] * fz;
     A.acc[32 * 4] += d[0] * fy;
     A.acc[32 * 5] += d[0] * fz;
     A.acc[32 * 6] += d[1] * fz;
-    if (MODE == 0) {
-      double *fj = w.facc + 3 * (int64_t)j, *fi = w.facc + 3 * (int64_t)i;  // facc: accumulator
+  }
+  if (MODE == 0) {
+    // F_i = -sum_a f_a (translation invariance of the terms on i): a segmented
+    // shuffle reduction over the row's L contiguous lanes, then one set of
+    // atomics per row instead of L same-address ones
+    double sx = fx, sy = fy, sz = fz;
+#pragma unroll
+    for (int off = 1; off < (LC > 0 ? LC : 32); off <<= 1) {
+      if (LC == 0 && off >= L) break;
+      const double ox = __shfl_down_sync(0xffffffffu, sx, off);
+      const double oy = __shfl_down_sync(0xffffffffu, sy, off);
+      const double oz = __shfl_down_sync(0xffffffffu, sz, off);
+      if (pos + off < L) {
+        sx += ox;
+        sy += oy;
+        sz += oz;
+      }
+    }
+    if (live) {
+      double *fj = w.facc + 3 * (int64_t)j;  // facc: accumulator
       atomicAdd(fj, fx);
       atomicAdd(fj + 1, fy);
       atomicAdd(fj + 2, fz);
-      atomicAdd(fi, -fx);  // F_i: translation invariance of the terms on i
-      atomicAdd(fi + 1, -fy);
-      atomicAdd(fi + 2, -fz);
-    } else {
-      double *fb = a.fbuf + 3 * (int64_t)e;
-      fb[0] = fx;
-      fb[1] = fy;
-      fb[2] = fz;
     }
-  } else if (MODE == 1 && valid) {
+    if (valid && pos == 0 && (lmask & rowmask)) {
+      double *fi = w.facc + 3 * (int64_t)i;
+      atomicAdd(fi, -sx);
+      atomicAdd(fi + 1, -sy);
+      atomicAdd(fi + 2, -sz);
+    }
+  } else if (valid) {  // dead entries store zeros
     double *fb = a.fbuf + 3 * (int64_t)e;
-    fb[0] = 0.0;
-    fb[1] = 0.0;
-    fb[2] = 0.0;
+    fb[0] = fx;
+    fb[1] = fy;
+    fb[2] = fz;
   }
   // ---- e_i: the first lane of each row sums the row's V (row order) ----
   if (valid && pos == 0) {
@@ -412,8 +432,19 @@ __device__ __forceinline__ void finalize_body(int n, double *__restrict__ facc,
   }
 }
 
+#ifdef TB_TRACE
+// per-warp timeline (debug builds): [globaltimer start, smid, clock64 at start
+// and after each of up to 12 chunks, nchunks done, globaltimer end]
+__device__ unsigned long long g_trace[4096 * 16];
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#endif
+
 template <class T, int S, bool LAM3, int MODE, bool ST>
-__global__ void __launch_bounds__(WNT, TB_WARP_MINB)
+__global__ void __launch_bounds__(WNT, sizeof(T) == 4 ? TB_WARP_MINB_F : TB_WARP_MINB)
     k_tersoff_warp(const KArgs a, const WArgs w, const __grid_constant__ Tables<T, S> gtab) {
   __shared__ Tables<T, S> s_tab;
   __shared__ double s_red[WPB][8];
@@ -458,6 +489,18 @@ __global__ void __launch_bounds__(WNT, TB_WARP_MINB)
   stage_chunk<S>(s_stage[wid][0], cur, lane, a.pos, a.species);
   cp_async_commit();
   int buf = 0;
+#ifdef TB_TRACE
+  const int gw = blockIdx.x * WPB + wid;
+  unsigned long long *tr = g_trace + 16 * (gw & 4095);
+  int ndone = 0;
+  if (lane == 0) {
+    unsigned smid;
+    asm volatile("mov.u32 %0, %smid;" : "=r"(smid));
+    tr[0] = gtimer();
+    tr[1] = smid;
+    tr[2] = clock64();
+  }
+#endif
   for (; c < nchunks; c += stride) {
     const int4 nx2 = c + 2 * stride < nchunks
                          ? __ldg(w.lanes + 32 * (int64_t)(c + 2 * stride) + lane)
@@ -474,11 +517,21 @@ __global__ void __launch_bounds__(WNT, TB_WARP_MINB)
       default: chunk_body<T, S, LAM3, MODE, ST, 0>(a, w, tab, s_cache[wid], s_tb[wid], lane, cur, stg, Ldyn, A);
     }
     __syncwarp();  // the stage and the lane table are rewritten next iteration
+#ifdef TB_TRACE
+    ++ndone;
+    if (lane == 0 && ndone <= 12) tr[2 + ndone] = clock64();
+#endif
     cur = nxt;
     nxt = nx2;
     buf ^= 1;
   }
   cp_async_wait<0>();
+#ifdef TB_TRACE
+  if (lane == 0) {
+    tr[14] = ndone;
+    tr[15] = gtimer();
+  }
+#endif
 
   // ---- stats and block partials (reduced by the finalize kernel) ----
   if (ST) {
