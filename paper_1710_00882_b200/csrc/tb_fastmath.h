@@ -125,6 +125,23 @@ TBFM_QUAL double tb_rcp(double y) {
   return fma(r, e, r);
 }
 
+// r = sqrt(x) and 1/r together (the displacement norm and the unit-vector
+// scale), 1e-30 < x < 1e30: single-precision rsqrt seed, two Newton steps on
+// y = 1/sqrt(x), then one Newton correction of r = x y (-> within 1 ulp).
+TBFM_QUAL void tb_sqrt_rsqrt(double x, double *r_out, double *rinv_out) {
+#if defined(__CUDA_ARCH__)
+  double y = (double)rsqrtf((float)x);
+#else
+  double y = (double)(1.0f / sqrtf((float)x));
+#endif
+  const double hx = 0.5 * x;
+  y = y * fma(-hx * y, y, 1.5);
+  y = y * fma(-hx * y, y, 1.5);
+  const double r = x * y;
+  *r_out = fma(fma(-r, r, x), 0.5 * y, r);
+  *rinv_out = y;
+}
+
 // log1p(u), u >= 0: w = 1 + u rounded; log1p(u) = log(w) + (u - (w - 1)) / w.
 TBFM_QUAL double tb_log1p(double u) {
   const double w = 1.0 + u;

@@ -6,9 +6,10 @@
 //   * g in the cancellation-free form gamma(1 + c^2 x^2 / (d^2 (d^2 + x^2)))
 //     (potential.py:190-199), written gamma + (gamma c^2/d^2) x^2 / den with one
 //     reciprocal of den shared by g and dg/dcos
-//   * bond order with 2 transcendental calls instead of the reference's 4 pow:
+//   * bond order with 2 log + 2 exp + 1 reciprocal instead of the reference's 4 pow:
 //       u = (beta zeta)^eta = exp(eta log t),  b = exp(-log1p(u)/(2 eta)),
-//       db/dzeta = -beta/2 * (u/t) * (b/(1+u))          (potential.py:202-215)
+//       db/dzeta = -beta/2 * (u/t) * (b/(1+u)) = -u b / (2 zeta (1+u))
+//       (potential.py:202-215)
 //     and the ZETA_TINY guard: zeta < 1e-30 => db = 0 (b still evaluated).
 #pragma once
 #include <cuda_runtime.h>
@@ -128,13 +129,17 @@ __device__ __forceinline__ void pair_part(T r, T zeta, const PairP<T> &p, T &v, 
     b = pow(T(1) + u, p.neg_half_inv_eta);
     db = T(0);
   } else {
-    // u = t^eta, b = (1+u)^(-1/2eta); db/dzeta = -beta/2 t^(eta-1) (1+u)^(-1/2eta-1)
-    //   = -beta/2 * exp((eta-1) log t) * b / (1+u)
+    // u = t^eta, b = (1+u)^(-1/2eta), and with t^(eta-1) = u/t, t = beta zeta:
+    //   db/dzeta = -beta/2 t^(eta-1) (1+u)^(-1/2eta-1) = -(1/2) u b / (zeta (1+u))
+    // one reciprocal serves db and the log1p correction (1/w = zeta / (zeta w))
     const T lt = t_log(t);
-    T u = t_exp(p.eta * lt);
-    T opu = T(1) + u;
-    b = t_exp(p.neg_half_inv_eta * t_log1p(u));
-    db = p.neg_half_beta * t_exp((p.eta - T(1)) * lt) * (b * t_rcp(opu));
+    const T u = t_exp(p.eta * lt);
+    const T w = T(1) + u;
+    const T rzw = t_rcp(zeta * w);
+    // log1p(u) = log(w) + (u - (w - 1)) / w, w = fl(1 + u)
+    const T l1p = t_log(w) + (u - (w - T(1))) * (zeta * rzw);
+    b = t_exp(p.neg_half_inv_eta * l1p);
+    db = T(-0.5) * (u * b) * rzw;
   }
   T inner = fr + b * fa;
   v = fc * inner;

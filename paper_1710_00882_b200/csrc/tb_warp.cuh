@@ -159,8 +159,8 @@ __device__ __forceinline__ void chunk_body(const KArgs &a, const WArgs &w, const
         ((unsigned long long)(__double_as_longlong(r2) >> 32) << 32) | (unsigned)e;
     atomicMin(&a.err->coinc_key, key);
   }
-  const double rd = live ? sqrt(r2) : 1.0;
-  const double invd = tb_rcp(rd);
+  double rd, invd;  // |d| and 1/|d| from one rsqrt
+  tb_sqrt_rsqrt(live ? r2 : 1.0, &rd, &invd);
   const T ex = (T)(d[0] * invd), ey = (T)(d[1] * invd), ez = (T)(d[2] * invd);
   const T ra = (T)rd;
   // f_C(r) of this entry acting as k in (i, q, this) for every species q of j
@@ -316,7 +316,7 @@ __device__ __forceinline__ void chunk_body(const KArgs &a, const WArgs &w, const
   }
   double fx = 0.0, fy = 0.0, fz = 0.0;
   if (live) {
-    const T inva = t_rcp(ra);
+    const T inva = sizeof(T) == 8 ? (T)invd : t_rcp(ra);
     const T ca = dvdr + Sal - Sc * inva;
     fx = -(double)(ca * ex + inva * Sbx);
     fy = -(double)(ca * ey + inva * Sby);
@@ -333,6 +333,15 @@ __device__ __forceinline__ void chunk_body(const KArgs &a, const WArgs &w, const
     // shuffle reduction over the row's L contiguous lanes, then one set of
     // atomics per row instead of L same-address ones
     double sx = fx, sy = fy, sz = fz;
+    if (LC > 0 && (LC & (LC - 1)) == 0) {
+      // rows of 2^k lanes are 2^k-aligned: butterfly, every lane gets the sum
+#pragma unroll
+      for (int off = 1; off < LC; off <<= 1) {
+        sx += __shfl_xor_sync(0xffffffffu, sx, off);
+        sy += __shfl_xor_sync(0xffffffffu, sy, off);
+        sz += __shfl_xor_sync(0xffffffffu, sz, off);
+      }
+    } else
 #pragma unroll
     for (int off = 1; off < (LC > 0 ? LC : 32); off <<= 1) {
       if (LC == 0 && off >= L) break;
@@ -435,7 +444,7 @@ __device__ __forceinline__ void finalize_body(int n, double *__restrict__ facc,
 #ifdef TB_TRACE
 // per-warp timeline (debug builds): [globaltimer start, smid, clock64 at start
 // and after each of up to 12 chunks, nchunks done, globaltimer end]
-__device__ unsigned long long g_trace[4096 * 16];
+__device__ unsigned long long g_trace[4096 * 16];  // last 2048 words: per-block entry/exit
 __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
@@ -453,6 +462,9 @@ __global__ void __launch_bounds__(WNT, sizeof(T) == 4 ? TB_WARP_MINB_F : TB_WARP
   __shared__ double s_acc[WPB][7][32];       // per-lane energy + virial
   __shared__ WTable<T> s_tb[WPB];            // lanes' neighbour data (per warp)
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#ifdef TB_TRACE
+  if (threadIdx.x == 0) g_trace[16 * 4096 - 2 * 1024 + 2 * (blockIdx.x & 1023)] = gtimer();
+#endif
   if (S > 1) {
     const int *src = reinterpret_cast<const int *>(&gtab);
     int *dst = reinterpret_cast<int *>(&s_tab);
@@ -556,6 +568,9 @@ __global__ void __launch_bounds__(WNT, sizeof(T) == 4 ? TB_WARP_MINB_F : TB_WARP
 #pragma unroll
     for (int q = 0; q < WPB; ++q) v += s_red[q][threadIdx.x];
     a.partials[8 * (int64_t)blockIdx.x + threadIdx.x] = v;
+#ifdef TB_TRACE
+    if (threadIdx.x == 0) g_trace[16 * 4096 - 2 * 1024 + 2 * (blockIdx.x & 1023) + 1] = gtimer();
+#endif
   }
 }
 

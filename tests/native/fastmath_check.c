@@ -18,7 +18,7 @@ static double urand(unsigned long long *s) {
 int main(int argc, char **argv) {
   long n = argc > 1 ? atol(argv[1]) : 2000000;
   unsigned long long s = 12345;
-  double me = 0, ml = 0, m1 = 0, mr = 0;
+  double me = 0, ml = 0, m1 = 0, mr = 0, msq = 0, mrs = 0;
   for (long i = 0; i < n; ++i) {
     double x = -708.0 + 1417.0 * urand(&s);
     double e = ulp_err(tb_exp(x), exp(x)); if (e > me) me = e;
@@ -32,8 +32,13 @@ int main(int argc, char **argv) {
     e = ulp_err(tb_log1p(u), log1p(u)); if (e > m1) m1 = e;
     double v = exp(-69.0 + 138.0 * urand(&s));  /* float-representable */
     e = ulp_err(tb_rcp(v), 1.0 / v); if (e > mr) mr = e;
+    double q = exp(-69.0 + 138.0 * urand(&s)), sq, rs;
+    if (i & 1) q = 1e-16 + 12.0 * urand(&s);  /* the r^2 < r_cut^2 range */
+    tb_sqrt_rsqrt(q, &sq, &rs);
+    e = ulp_err(sq, sqrt(q)); if (e > msq) msq = e;
+    e = ulp_err(rs, 1.0 / sqrt(q)); if (e > mrs) mrs = e;
   }
-  printf("{\"exp_ulp\": %.3f, \"log_ulp\": %.3f, \"log1p_ulp\": %.3f, \"rcp_ulp\": %.3f, \"n\": %ld}\n",
-         me, ml, m1, mr, n);
+  printf("{\"exp_ulp\": %.3f, \"log_ulp\": %.3f, \"log1p_ulp\": %.3f, \"rcp_ulp\": %.3f, "
+         "\"sqrt_ulp\": %.3f, \"rsqrt_ulp\": %.3f, \"n\": %ld}\n", me, ml, m1, mr, msq, mrs, n);
   return 0;
 }

@@ -21,3 +21,5 @@ def test_fastmath_ulp_bounds(tmp_path):
     assert out["log_ulp"] <= 2
     assert out["log1p_ulp"] <= 2
     assert out["rcp_ulp"] <= 1
+    assert out["sqrt_ulp"] <= 1
+    assert out["rsqrt_ulp"] <= 4

@@ -34,16 +34,33 @@ for prec in (0, 1):
         torch.cuda.synchronize()
         buf = np.zeros(4096 * 16, np.uint64)
         assert lib.tb_debug_trace(buf.ctypes.data, buf.nbytes) == 0
-        tr = buf.reshape(4096, 16).astype(np.int64)
+        blk = buf[-2048:].reshape(1024, 2).astype(np.int64)
+        blk = blk[blk[:, 0] != 0]
+        tr = buf.reshape(4096, 16).astype(np.int64)[:3968]
         nw = int(np.count_nonzero(tr[:, 0]))
         tr = tr[:nw]
         g0 = tr[:, 0] - tr[:, 0].min()
         gend = tr[:, 15] - tr[:, 0].min()
+        ctx.lib.tb_profile(ctx.handle, 1)
+        for _ in range(20):
+            if fl:
+                flush.zero_()
+            lib.tb_compute_device(ctx.handle, nl._nl.handle, P(pos), P(sp), float(t.r_cut), prec, 0,
+                                  P(f), P(pa), P(res), None)
+        ctx.lib.tb_profile(ctx.handle, 0)
+        tot = ctypes.c_double(); l = ctypes.c_int64()
+        ctx.lib.tb_profile_read(ctx.handle, ctypes.byref(tot), ctypes.byref(l))
+        out[f"event_us_{prec}_{fl}"] = 1e3 * tot.value / l.value
         nd = tr[:, 14]
         clk = tr[:, 2:15]
         d_first = clk[:, 1] - clk[:, 0]
         later = [clk[w, k + 1] - clk[w, k] for w in range(nw) for k in range(1, min(nd[w], 12))]
-        out[f"{'f64' if prec == 0 else 'mix'}/{'flush' if fl else 'warm'}"] = {
+        b0 = blk[:, 0].min()
+        key = f"{'f64' if prec == 0 else 'mix'}/{'flush' if fl else 'warm'}"
+        out[key + "/blocks"] = {"entry_ns_p50_max": [int(np.median(blk[:, 0] - b0)), int((blk[:, 0] - b0).max())],
+                                "exit_ns_min_p50_max": [int((blk[:, 1] - b0).min()), int(np.median(blk[:, 1] - b0)), int((blk[:, 1] - b0).max())],
+                                "first_warp_start_after_entry_ns": int(tr[:, 0].min() - b0)}
+        out[key] = {
             "warps": nw, "chunks_per_warp": np.bincount(nd).tolist(),
             "start_ns_p50_p100": [int(np.median(g0)), int(g0.max())],
             "end_ns_p0_p50_p100": [int(gend.min()), int(np.median(gend)), int(gend.max())],
