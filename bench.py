@@ -275,6 +275,28 @@ def gpu_arm_decomposed(args):
     for _ in range(max(3, args.warmup)):
         f, res = ff(dom)
     torch.cuda.synchronize()
+    # the whole decomposed step (halo P2P, Tersoff kernel + finalize, reverse
+    # forces, all-reduce) as one CUDA graph: NCCL ops are capturable
+    # (tools/nccl_capture_probe.py); any capture error falls back to eager
+    launch = "eager (Python host loop, NCCL batch_isend_irecv)"
+    graph = None
+    step_fn = lambda: ff(dom)  # noqa: E731
+    if backend == "nccl" and os.environ.get("BENCH_DD_GRAPH", "1") == "1":
+        try:
+            dist.barrier()
+            torch.cuda.synchronize()
+            graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(graph, stream=stream):
+                f_g, res_g = ff(dom)
+            graph.replay()
+            torch.cuda.synchronize()
+            step_fn = lambda: (graph.replay(), (f_g, res_g))[1]  # noqa: E731
+            launch = ("one CUDA graph per step: halo P2P + Tersoff kernel + finalize + reverse "
+                      "forces + all-reduce (NCCL ops captured)")
+        except Exception as e:  # noqa: BLE001
+            graph = None
+            launch = f"eager (graph capture failed: {str(e)[:80]})"
+            torch.cuda.synchronize()
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
     k = args.steps
     starts = [torch.cuda.Event(enable_timing=True) for _ in range(k)]
@@ -286,7 +308,7 @@ def gpu_arm_decomposed(args):
         for s_ in range(k):
             flush.zero_()
             starts[s_].record(stream)
-            f, res = ff(dom)
+            f, res = step_fn()
             ends[s_].record(stream)
         torch.cuda.synchronize()
     t_local = sum(a.elapsed_time(b) for a, b in zip(starts, ends)) / 1e3
@@ -317,7 +339,7 @@ def gpu_arm_decomposed(args):
     t0 = time.perf_counter()
     for _ in range(ke):
         dom.pos.copy_(pos_h, non_blocking=True)
-        f, res = ff(dom)
+        f, res = step_fn()
         f_h.copy_(f, non_blocking=True)
         e_host = float(res[0])
     torch.cuda.synchronize()
@@ -335,7 +357,7 @@ def gpu_arm_decomposed(args):
                    "precision": args.precision, "scatter": args.scatter,
                    "parallelism": f"spatial slabs x{ws}",
                    "l2": "flushed between timed steps (256 MiB write)",
-                   "launch": "eager (Python host loop, NCCL batch_isend_irecv)"},
+                   "launch": launch},
         "e2e": {"value": n_total * ke / float(te[0]), "unit": UNIT, "steps": ke,
                 "h2d_bytes_per_step": int(dom.pos.numel() * 8),
                 "d2h_bytes_per_step": int(dom.pos.numel() * 8 + 8),
@@ -350,6 +372,13 @@ def gpu_arm_decomposed(args):
     if rank == 0:
         print(json.dumps(line, default=_jsonable), flush=True)
     dist.barrier()
+    if graph is not None:
+        # tearing the process group down under a live captured graph can
+        # block at exit: release the graph, then leave without the teardown
+        del graph, step_fn
+        torch.cuda.synchronize()
+        sys.stdout.flush()
+        os._exit(0)
     dist.destroy_process_group()
 
 

@@ -231,8 +231,9 @@ class DecomposedForceField:
             dom.ghost_species = dom.species[:0]
         self.rebuilds += 1
         pos_l = self.halo_positions(dom)
-        sp_l = torch.cat([dom.species, dom.ghost_species]).contiguous()
-        self.engine.rebuild(pos_l, sp_l, dom.n_owned, self.box)
+        # species of [owned | ghosts] only change at a rebuild
+        dom._sp_l = torch.cat([dom.species, dom.ghost_species]).contiguous()
+        self.engine.rebuild(pos_l, dom._sp_l, dom.n_owned, self.box)
         return dom
 
     # ---- every evaluation ----
@@ -247,8 +248,10 @@ class DecomposedForceField:
     def __call__(self, dom):
         """Forces on the owned atoms, global energy and virial."""
         pos_l = self.halo_positions(dom)
-        sp_l = torch.cat([dom.species, dom.ghost_species]).contiguous() \
-            if self.nranks > 1 else dom.species
+        sp_l = getattr(dom, "_sp_l", None)
+        if sp_l is None:
+            sp_l = torch.cat([dom.species, dom.ghost_species]).contiguous() \
+                if self.nranks > 1 else dom.species
         forces_l, result = self.engine.compute(pos_l, sp_l)
         n = dom.n_owned
         f = forces_l[:n].clone()
