@@ -48,9 +48,11 @@ struct Tables {
 
 // ---- transcendental wrappers (overloads keep the templates readable) ----
 __device__ __forceinline__ double t_exp(double x) { return tb_exp(x); }
-__device__ __forceinline__ float t_exp(float x) { return expf(x); }
+// mixed mode: MUFU-based exp2/log2 (relative error ~2^-22 plus the argument
+// rounding), well inside the 1e-5 force tolerance of the mixed mode
+__device__ __forceinline__ float t_exp(float x) { return __expf(x); }
 __device__ __forceinline__ double t_log(double x) { return tb_log(x); }
-__device__ __forceinline__ float t_log(float x) { return logf(x); }
+__device__ __forceinline__ float t_log(float x) { return __logf(x); }
 __device__ __forceinline__ double t_log1p(double x) { return tb_log1p(x); }
 __device__ __forceinline__ float t_log1p(float x) { return log1pf(x); }
 __device__ __forceinline__ void t_sincospi(double x, double *s, double *c) { sincospi(x, s, c); }

@@ -6,6 +6,9 @@
 struct Big { double v[64]; };
 __global__ void k_empty(int *p) { if (p && threadIdx.x == 9999) p[0] = 1; }
 __global__ void k_big(const __grid_constant__ Big b, int *p) { if (threadIdx.x == 9999) p[0] = (int)b.v[3]; }
+__global__ void k_fill(float *p, size_t n) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) p[i] = 0.f;
+}
 __global__ void k_load(const int4 *__restrict__ l, double *out) {
   int4 v = __ldg(l + blockIdx.x * blockDim.x + threadIdx.x);
   if (v.x == 12345) out[0] = v.y;
@@ -16,6 +19,30 @@ int main() {
   int4 *l; cudaMalloc(&l, 592 * 128 * 16); cudaMemset(l, 0, 592 * 128 * 16);
   float *fl; size_t fb = 256 << 20; cudaMalloc(&fl, fb);
   Big big = {};
+  cudaStream_t st; cudaStreamCreate(&st);
+  cudaGraph_t gr; cudaGraphExec_t ge;
+  cudaStreamBeginCapture(st, cudaStreamCaptureModeGlobal);
+  k_empty<<<592, 128, 0, st>>>(d);
+  cudaStreamEndCapture(st, &gr);
+  cudaGraphInstantiate(&ge, gr, 0);
+  const char *names[] = {"empty_after_memset", "big_params_after_memset", "one_ldg_after_memset",
+                         "empty_after_fill_kernel", "empty_no_flush", "graph_empty_after_fill_kernel",
+                         "fill_kernel_itself"};
+  for (int mode = 3; mode < 7; ++mode) {
+    float tot = 0; int K = 200;
+    for (int it = 0; it < K + 10; ++it) {
+      if (mode != 4 && mode != 6) k_fill<<<148 * 8, 256, 0, st>>>(fl, fb / 4);
+      cudaEventRecord(a, st);
+      if (mode == 3 || mode == 4) k_empty<<<592, 128, 0, st>>>(d);
+      else if (mode == 5) cudaGraphLaunch(ge, st);
+      else k_fill<<<148 * 8, 256, 0, st>>>(fl, fb / 4);
+      cudaEventRecord(b, st);
+      cudaEventSynchronize(b);
+      float ms; cudaEventElapsedTime(&ms, a, b);
+      if (it >= 10) tot += ms;
+    }
+    printf("{\"mode\": \"%s\", \"us\": %.2f}\n", names[mode], 1e3 * tot / K);
+  }
   for (int mode = 0; mode < 3; ++mode) {
     float tot = 0; int K = 200;
     for (int it = 0; it < K + 10; ++it) {
@@ -29,7 +56,7 @@ int main() {
       float ms; cudaEventElapsedTime(&ms, a, b);
       if (it >= 10) tot += ms;
     }
-    printf("{\"mode\": \"%s\", \"us\": %.2f}\n", mode == 0 ? "empty" : mode == 1 ? "big_params" : "one_ldg_flushed", 1e3 * tot / K);
+    printf("{\"mode\": \"%s\", \"us\": %.2f}\n", names[mode], 1e3 * tot / K);
   }
   return 0;
 }
