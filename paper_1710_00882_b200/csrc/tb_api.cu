@@ -1070,9 +1070,15 @@ static int enqueue_compute(tb_context *ctx, const tb_nlist *nl, const double *d_
                                      : launch_prec<float>(ctx, nl, a, C, scatter);
   }
   if (rc) return rc;
-  int fb = std::min(nblk(scatter == TB_SCATTER_GATHER ? n : 3 * (int64_t)n, 256), 4 * 148);
+  // finalize grid: block 0 reduces E/W; the rest move the forces (atomic: 16-byte
+  // vectors, ~4 per thread; gather: one atom row per thread)
+  int fb = 1 + std::min(scatter == TB_SCATTER_GATHER ? nblk(n, 256) : nblk(3 * (int64_t)n, 256 * 2 * 4),
+                        4 * 148);
   // (a programmatic-dependent finalize launch, a cooperative grid-barrier
   //  finalize and a last-block reduction were all measured slower)
+#ifdef TB_DBG_NO_FINALIZE
+  if (getenv("TB_DBG_NO_FINALIZE")) return TB_OK;  // timing experiments only
+#endif
   if (scatter == TB_SCATTER_GATHER)
     k_finalize<1><<<fb, 256, 0, ctx->stream>>>(n, nullptr, a.off, nl->rev.as<int>(), a.fbuf,
                                                 d_forces, nparts, a.partials, d_result, a.stats,

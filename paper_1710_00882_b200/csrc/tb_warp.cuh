@@ -393,16 +393,61 @@ __device__ __forceinline__ void finalize_body(int n, double *__restrict__ facc,
                                               double *__restrict__ result,
                                               unsigned long long *__restrict__ stats_acc,
                                               unsigned long long *__restrict__ stats_out,
-                                              double (*s)[7] /* [NTHR][7] shared scratch */) {
+                                              double (*s)[7] /* [NTHR/32][7] shared scratch */) {
+  // block 0 reduces the block partials (E, W) and hands out the counters; the
+  // other blocks move the forces (a one-block grid does both)
+  if (blockIdx.x == 0) {
+    double acc[7] = {0, 0, 0, 0, 0, 0, 0};
+    for (int b = threadIdx.x; b < nparts; b += NTHR)
+#pragma unroll
+      for (int q = 0; q < 7; ++q) acc[q] += __ldcg(partials + 8 * (int64_t)b + q);
+    const int lane = threadIdx.x & 31, wrp = threadIdx.x >> 5;
+#pragma unroll
+    for (int q = 0; q < 7; ++q) acc[q] = warp_sum(acc[q]);  // fixed order: deterministic
+    if (lane == 0)
+#pragma unroll
+      for (int q = 0; q < 7; ++q) s[wrp][q] = acc[q];
+    __syncthreads();
+    if (threadIdx.x < 7) {
+      double v = 0.0;
+      for (int q = 0; q < NTHR / 32; ++q) v += s[q][threadIdx.x];
+      result[threadIdx.x] = v + 0.0;
+    }
+    if (threadIdx.x < 6) {
+      if (stats_out) stats_out[threadIdx.x] = __ldcg(stats_acc + threadIdx.x);
+      stats_acc[threadIdx.x] = 0ull;
+    }
+    if (gridDim.x > 1) return;
+  }
+  const int nb = gridDim.x > 1 ? gridDim.x - 1 : 1;
+  const int b0 = gridDim.x > 1 ? blockIdx.x - 1 : 0;
   if (MODE == 0) {
     const int64_t m3 = 3 * (int64_t)n;
-    for (int64_t k = blockIdx.x * (int64_t)NTHR + threadIdx.x; k < m3;
-         k += (int64_t)gridDim.x * NTHR) {
-      forces[k] = __ldcg(facc + k) + 0.0;
-      facc[k] = 0.0;
+    if ((reinterpret_cast<uintptr_t>(forces) & 15) == 0) {
+      // 16-byte vectors (facc is a cudaMalloc allocation; forces checked)
+      const int64_t m2 = m3 >> 1;
+      double2 *f2 = reinterpret_cast<double2 *>(forces);
+      double2 *a2 = reinterpret_cast<double2 *>(facc);
+      const double2 z = make_double2(0.0, 0.0);
+      for (int64_t k = b0 * (int64_t)NTHR + threadIdx.x; k < m2; k += (int64_t)nb * NTHR) {
+        double2 v = __ldcg(a2 + k);
+        v.x += 0.0;
+        v.y += 0.0;
+        f2[k] = v;
+        a2[k] = z;
+      }
+      if ((m3 & 1) && b0 == 0 && threadIdx.x == 0) {
+        forces[m3 - 1] = __ldcg(facc + m3 - 1) + 0.0;
+        facc[m3 - 1] = 0.0;
+      }
+    } else {
+      for (int64_t k = b0 * (int64_t)NTHR + threadIdx.x; k < m3; k += (int64_t)nb * NTHR) {
+        forces[k] = __ldcg(facc + k) + 0.0;
+        facc[k] = 0.0;
+      }
     }
   } else {
-    for (int m = blockIdx.x * NTHR + threadIdx.x; m < n; m += gridDim.x * NTHR) {
+    for (int m = b0 * NTHR + threadIdx.x; m < n; m += nb * NTHR) {
       double ix = 0.0, iy = 0.0, iz = 0.0, sx = 0.0, sy = 0.0, sz = 0.0;
       for (int e = off[m]; e < off[m + 1]; ++e) {
         const double *f = fbuf + 3 * (int64_t)__ldg(rev + e);
@@ -417,26 +462,6 @@ __device__ __forceinline__ void finalize_body(int n, double *__restrict__ facc,
       forces[3 * (int64_t)m] = (ix - sx) + 0.0;
       forces[3 * (int64_t)m + 1] = (iy - sy) + 0.0;
       forces[3 * (int64_t)m + 2] = (iz - sz) + 0.0;
-    }
-  }
-  if (blockIdx.x == 0) {
-    double acc[7] = {0, 0, 0, 0, 0, 0, 0};
-    for (int b = threadIdx.x; b < nparts; b += NTHR)
-#pragma unroll
-      for (int q = 0; q < 7; ++q) acc[q] += __ldcg(partials + 8 * (int64_t)b + q);
-#pragma unroll
-    for (int q = 0; q < 7; ++q) s[threadIdx.x][q] = acc[q];
-    __syncthreads();
-    for (int h = NTHR / 2; h > 0; h >>= 1) {
-      if (threadIdx.x < h)
-#pragma unroll
-        for (int q = 0; q < 7; ++q) s[threadIdx.x][q] += s[threadIdx.x + h][q];
-      __syncthreads();
-    }
-    if (threadIdx.x < 7) result[threadIdx.x] = s[0][threadIdx.x] + 0.0;
-    if (threadIdx.x < 6) {
-      if (stats_out) stats_out[threadIdx.x] = __ldcg(stats_acc + threadIdx.x);
-      stats_acc[threadIdx.x] = 0ull;
     }
   }
 }
@@ -689,7 +714,7 @@ __global__ void __launch_bounds__(256) k_finalize(int n, double *__restrict__ fa
                            const double *__restrict__ partials, double *__restrict__ result,
                            unsigned long long *__restrict__ stats_acc,
                            unsigned long long *__restrict__ stats_out) {
-  __shared__ double s[256][7];
+  __shared__ double s[256 / 32][7];
   finalize_body<MODE, 256>(n, facc, off, rev, fbuf, forces, nparts, partials, result, stats_acc,
                            stats_out, s);
 }
