@@ -139,6 +139,28 @@ def _exchange(sends, recv_shapes, dtype, device, left, right):
     return from_left[:recv_shapes[0][0]], from_right[:recv_shapes[1][0]]
 
 
+def _exchange_into(sends, recvs, left, right):
+    """_exchange with caller-owned receive buffers (contiguous row blocks,
+    written in place), as the per-step halos use them: no allocation, no
+    concatenation.  Zero-row messages and the gloo routing take _exchange
+    (both ends of a zero-row message do, so the padding stays matched)."""
+    dev = recvs[0].device
+    comm = _COMM_DEVICE.get("device")
+    if (comm is not None and str(comm) != str(dev)) or \
+            any(t.shape[0] == 0 for t in (*sends, *recvs)):
+        fl, fr = _exchange(sends, (tuple(recvs[0].shape), tuple(recvs[1].shape)), recvs[0].dtype,
+                           dev, left, right)
+        recvs[0].copy_(fl)
+        recvs[1].copy_(fr)
+        return
+    ops = [dist.P2POp(dist.isend, sends[0], left),
+           dist.P2POp(dist.irecv, recvs[1], right),
+           dist.P2POp(dist.isend, sends[1], right),
+           dist.P2POp(dist.irecv, recvs[0], left)]
+    for req in dist.batch_isend_irecv(ops):
+        req.wait()
+
+
 def _exchange_counts(a_left, a_right, device, left, right):
     s = (torch.tensor([a_left], dtype=torch.int64, device=device),
          torch.tensor([a_right], dtype=torch.int64, device=device))
@@ -230,23 +252,38 @@ class DecomposedForceField:
             dom.ghost_ids = np.zeros(0, np.int64)
             dom.ghost_species = dom.species[:0]
         self.rebuilds += 1
-        pos_l = self.halo_positions(dom)
+        # per-step buffers (fixed until the next rebuild): [owned | left ghosts |
+        # right ghosts] positions, the packed send rows and the returning forces;
         # species of [owned | ghosts] only change at a rebuild
+        if self.nranks > 1:
+            nsend = len(dom.send_left) + len(dom.send_right)
+            dom._idx_send = torch.cat([dom._idl, dom._idr]).contiguous()
+            dom._pos_l = torch.empty((dom.n_owned + dom.n_ghost_left + dom.n_ghost_right, 3),
+                                     dtype=torch.float64, device=self.device)
+            dom._send = torch.empty((nsend, 3), dtype=torch.float64, device=self.device)
+            dom._back = torch.empty((nsend, 3), dtype=torch.float64, device=self.device)
+        pos_l = self.halo_positions(dom)
         dom._sp_l = torch.cat([dom.species, dom.ghost_species]).contiguous()
         self.engine.rebuild(pos_l, dom._sp_l, dom.n_owned, self.box)
         return dom
 
     # ---- every evaluation ----
     def halo_positions(self, dom):
+        """[owned | left ghosts | right ghosts] positions (forward halo)."""
         if self.nranks == 1:
             return dom.pos
-        gl, gr = _exchange((dom.pos[dom._idl], dom.pos[dom._idr]),
-                           ((dom.n_ghost_left, 3), (dom.n_ghost_right, 3)), torch.float64,
-                           self.device, self.left, self.right)
-        return torch.cat([dom.pos, gl, gr], dim=0).contiguous()
+        n, ngl = dom.n_owned, dom.n_ghost_left
+        pos_l, send, nsl = dom._pos_l, dom._send, len(dom.send_left)
+        pos_l[:n].copy_(dom.pos)
+        torch.index_select(dom.pos, 0, dom._idx_send, out=send)
+        _exchange_into((send[:nsl], send[nsl:]), (pos_l[n:n + ngl], pos_l[n + ngl:]),
+                       self.left, self.right)
+        return pos_l
 
     def __call__(self, dom):
-        """Forces on the owned atoms, global energy and virial."""
+        """Forces on the owned atoms, global energy and virial.  The returned
+        force tensor is a view of the engine's buffer: valid until the next
+        call (copy it to keep it)."""
         pos_l = self.halo_positions(dom)
         sp_l = getattr(dom, "_sp_l", None)
         if sp_l is None:
@@ -254,23 +291,20 @@ class DecomposedForceField:
                 if self.nranks > 1 else dom.species
         forces_l, result = self.engine.compute(pos_l, sp_l)
         n = dom.n_owned
-        f = forces_l[:n].clone()
+        f = forces_l[:n]
         if self.nranks > 1:
             # reverse halo: forces on my left ghosts belong to rank-1's right
-            # column atoms and vice versa
-            fgl = forces_l[n:n + dom.n_ghost_left]
-            fgr = forces_l[n + dom.n_ghost_left:]
-            back_from_left, back_from_right = _exchange(
-                (fgl, fgr), ((len(dom.send_left), 3), (len(dom.send_right), 3)),
-                torch.float64, self.device, self.left, self.right)
-            # from_left carries forces on my left-column atoms (rank-1's right ghosts)
-            f.index_add_(0, dom._idl, back_from_left)
-            f.index_add_(0, dom._idr, back_from_right)
+            # column atoms and vice versa; from_left carries forces on my
+            # left-column atoms (rank-1's right ghosts)
+            ngl, nsl, back = dom.n_ghost_left, len(dom.send_left), dom._back
+            _exchange_into((forces_l[n:n + ngl], forces_l[n + ngl:]), (back[:nsl], back[nsl:]),
+                           self.left, self.right)
+            f.index_add_(0, dom._idx_send, back)
             comm = _COMM_DEVICE.get("device")
             if comm is not None and str(comm) != str(self.device):
                 r = result.to(comm)
                 dist.all_reduce(r)
-                result = r.to(self.device)
+                result.copy_(r)
             else:
                 dist.all_reduce(result)
         return f, result
@@ -301,14 +335,19 @@ class B200Engine:
             float(self.params.r_cut), float(self.skin)), "tb_build_neighbors_owned")
 
     def compute(self, pos_l, sp_l):
+        """Forces on [owned | ghosts] and [E, W6] into engine-owned buffers
+        (reused while the atom count is unchanged: capturable in a graph)."""
         P = self.native.ptr
         n = pos_l.shape[0]
-        forces = torch.empty((n, 3), dtype=torch.float64, device=self.device)
-        result = torch.zeros(8, dtype=torch.float64, device=self.device)
+        if getattr(self, "_n", None) != n:
+            self._forces = torch.empty((n, 3), dtype=torch.float64, device=self.device)
+            self._result = torch.zeros(8, dtype=torch.float64, device=self.device)
+            self._n = n
         self.ctx.check(self.ctx.lib.tb_compute_device(
             self.ctx.handle, self.nl.handle, P(pos_l), P(sp_l), float(self.params.r_cut),
-            self.prec, self.scat, P(forces), None, P(result), None), "tb_compute_device")
-        return forces, result[:7]
+            self.prec, self.scat, P(self._forces), None, P(self._result), None),
+            "tb_compute_device")
+        return self._forces, self._result[:7]
 
 
 def set_comm_device(device):
