@@ -218,6 +218,15 @@ static Tables<T, S> make_tables(const tb_context *ctx) {
     t.lam3x3 = (T)(3.0 * r[6]);
     t.m = (int)r[7];
   }
+  tab.gsym = 1;
+  for (int i = 0; i < S; ++i)
+    for (int j = 0; j < S; ++j)
+      for (int k = 0; k < S; ++k) {
+        const TripP<T> &x = tab.trip[(i * S + j) * S + k], &y = tab.trip[(i * S + k) * S + j];
+        if (!(x.gamma == y.gamma && x.gc2d2 == y.gc2d2 && x.m2gc2 == y.m2gc2 && x.d2 == y.d2 &&
+              x.h == y.h && x.lam3 == y.lam3 && x.lam3x3 == y.lam3x3 && x.m == y.m))
+          tab.gsym = 0;
+      }
   for (int q = 0; q < S * S; ++q) {
     const double *r = &ctx->pair_mat[8 * q];
     PairP<T> &p = tab.pair[q];

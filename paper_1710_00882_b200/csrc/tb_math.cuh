@@ -44,6 +44,11 @@ template <class T, int S>
 struct Tables {
   PairP<T> pair[S * S];
   TripP<T> trip[S * S * S];
+  // 1 when g(cos) of entry (i,j,k) equals that of (i,k,j) for every triple
+  // (gamma, c, d, h, lam3, m depend on i only, as in the Tersoff-1989 tables):
+  // the (i,b,a) term then reuses the (i,a,b) angular values
+  int gsym;
+  int pad_;
 };
 
 // ---- transcendental wrappers (overloads keep the templates readable) ----

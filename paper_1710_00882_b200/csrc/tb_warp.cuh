@@ -159,10 +159,27 @@ __device__ __forceinline__ void chunk_body(const KArgs &a, const WArgs &w, const
         ((unsigned long long)(__double_as_longlong(r2) >> 32) << 32) | (unsigned)e;
     atomicMin(&a.err->coinc_key, key);
   }
-  double rd, invd;  // |d| and 1/|d| from one rsqrt
-  tb_sqrt_rsqrt(live ? r2 : 1.0, &rd, &invd);
-  const T ex = (T)(d[0] * invd), ey = (T)(d[1] * invd), ez = (T)(d[2] * invd);
-  const T ra = (T)rd;
+  // |d| and 1/|d| from one rsqrt: fp64 Newton in fp64 mode; in the mixed mode
+  // the potential math is fp32 anyway (kernels.py:154-165 casts r to single),
+  // so one MUFU rsqrt of the fp32 r^2 (live test above stays fp64: exact pair set)
+  T ex, ey, ez, ra, inva;
+  if (sizeof(T) == 8) {
+    double rd, invd;
+    tb_sqrt_rsqrt(live ? r2 : 1.0, &rd, &invd);
+    ex = (T)(d[0] * invd);
+    ey = (T)(d[1] * invd);
+    ez = (T)(d[2] * invd);
+    ra = (T)rd;
+    inva = (T)invd;
+  } else {
+    const float r2f = live ? (float)r2 : 1.0f;
+    const float rinv = rsqrtf(r2f);
+    ra = (T)(r2f * rinv);
+    inva = (T)rinv;
+    ex = (T)((float)d[0] * rinv);
+    ey = (T)((float)d[1] * rinv);
+    ez = (T)((float)d[2] * rinv);
+  }
   // f_C(r) of this entry acting as k in (i, q, this) for every species q of j
   T fck[S], dfck[S];
 #pragma unroll
@@ -302,7 +319,7 @@ __device__ __forceinline__ void chunk_body(const KArgs &a, const WArgs &w, const
       if (t2) {  // (i,b,a): entry (si, sb, sa)
         const TripP<T> &tp = tab.trip[(si * S + sb) * S + sj];
         T g2 = g, dg2 = dg, exv = T(1), darg = T(0);
-        if (S > 1) angular(cost, tp, g2, dg2);
+        if (S > 1 && !tab.gsym) angular(cost, tp, g2, dg2);
         if (LAM3) lam3_term(rb - ra, tp, exv, darg);
         alpha += dzb * (df_a * g2 * exv - f_a * g2 * exv * darg);
         beta += dzb * (f_a * dg2 * exv);
@@ -316,7 +333,6 @@ __device__ __forceinline__ void chunk_body(const KArgs &a, const WArgs &w, const
   }
   double fx = 0.0, fy = 0.0, fz = 0.0;
   if (live) {
-    const T inva = sizeof(T) == 8 ? (T)invd : t_rcp(ra);
     const T ca = dvdr + Sal - Sc * inva;
     fx = -(double)(ca * ex + inva * Sbx);
     fy = -(double)(ca * ey + inva * Sby);
