@@ -81,6 +81,12 @@ struct tb_context {
   bool warp_per_chunk = getenv("TB_WARP_PER_CHUNK") != nullptr;
   bool no_filter = getenv("TB_NO_FILTER") != nullptr;  // disable the species-pair compute filter
   bool err_unchecked = false;     // kernels may have raised error flags nobody read yet
+  // tb_compute with host buffers: finalize also copies the error flags here
+  // (device alias of pinned host memory) and an event marks the end of the
+  // Tersoff kernel so the per-atom energies go back on the side stream
+  unsigned long long *fin_err_dst = nullptr;
+  cudaEvent_t ev_kernel_done = nullptr;
+  cudaStream_t side = nullptr;
   std::vector<int> last_species;  // host species of the last tb_compute (filter validity)
   const int *dplan = nullptr;  // tb_md_run capture: device {nchunks, n_empty}
   int last_blocks = 0;  // grid of the last Tersoff launch (partials to reduce)  // tb_set_option(TB_OPT_TILE_KERNEL): general tile kernel only
@@ -167,6 +173,27 @@ static bool is_device_ptr(const void *p) {
     return false;
   }
   return attr.type == cudaMemoryTypeDevice || attr.type == cudaMemoryTypeManaged;
+}
+
+// wait for a stream by polling (a synchronous call of ~0.1 ms: polling avoids
+// the scheduler wake-up latency of a blocking wait)
+static cudaError_t spin_sync(cudaStream_t s) {
+  cudaError_t e;
+  while ((e = cudaStreamQuery(s)) == cudaErrorNotReady) {
+  }
+  return e;
+}
+
+// device-accessible alias of a host pointer (pinned / registered host memory,
+// mapped under unified addressing), or nullptr for pageable memory
+static void *host_alias(const void *p) {
+  if (!p) return nullptr;
+  cudaPointerAttributes attr;
+  if (cudaPointerGetAttributes(&attr, p) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  return attr.type == cudaMemoryTypeHost ? attr.devicePointer : nullptr;
 }
 
 // python-style %g of a double for messages
@@ -286,6 +313,8 @@ extern "C" void tb_destroy(tb_context *ctx) {
       cudaEventDestroy(ev.first);
       cudaEventDestroy(ev.second);
     }
+  if (ctx->side) cudaStreamDestroy(ctx->side);
+  if (ctx->ev_kernel_done) cudaEventDestroy(ctx->ev_kernel_done);
   if (ctx->h_err) cudaFreeHost(ctx->h_err);
   if (ctx->h_small) cudaFreeHost(ctx->h_small);
   if (ctx->own) cudaStreamDestroy(ctx->own);
@@ -1088,13 +1117,16 @@ static int enqueue_compute(tb_context *ctx, const tb_nlist *nl, const double *d_
 #ifdef TB_DBG_NO_FINALIZE
   if (getenv("TB_DBG_NO_FINALIZE")) return TB_OK;  // timing experiments only
 #endif
+  if (ctx->ev_kernel_done) CK(cudaEventRecord(ctx->ev_kernel_done, ctx->stream));
+  const unsigned long long *err_src = reinterpret_cast<const unsigned long long *>(a.err);
   if (scatter == TB_SCATTER_GATHER)
     k_finalize<1><<<fb, 256, 0, ctx->stream>>>(n, nullptr, a.off, nl->rev.as<int>(), a.fbuf,
                                                 d_forces, nparts, a.partials, d_result, a.stats,
-                                                d_stats);
+                                                d_stats, err_src, ctx->fin_err_dst);
   else
     k_finalize<0><<<fb, 256, 0, ctx->stream>>>(n, a.forces, nullptr, nullptr, nullptr, d_forces,
-                                                nparts, a.partials, d_result, a.stats, d_stats);
+                                                nparts, a.partials, d_result, a.stats, d_stats,
+                                                err_src, ctx->fin_err_dst);
   CK(cudaGetLastError());
   return TB_OK;
 }
@@ -1151,8 +1183,6 @@ extern "C" int tb_compute(tb_context *ctx, const tb_nlist *nl, const double *pos
   CK(cudaSetDevice(ctx->device));
   const int64_t n = nl->n;
   if (n && (!positions || !species)) return fail(ctx, TB_ERR_ARG, "null positions/species");
-  // error flags, result and counters share one small device block so that a
-  // call reads them back with one copy: [ErrFlags | result @64 | stats @128]
   int rc = TB_OK;
   if (ctx->err_unchecked || !ctx->errf.p) rc = reset_errors(ctx);
   if (rc) return rc;
@@ -1170,31 +1200,67 @@ extern "C" int tb_compute(tb_context *ctx, const tb_nlist *nl, const double *pos
       const_cast<tb_nlist *>(nl)->filtered = false;
     }
   }
-  bool f_dev = is_device_ptr(forces);
-  double *d_f = forces;
-  if (!f_dev) {
+  if (n == 0) {  // validation only (parameters, list, cutoff); empty results
+    CK(ctx->result.ensure(sizeof(double) * 8));
+    CK(ctx->stats.ensure(sizeof(unsigned long long) * TB_NSTATS));
+    rc = enqueue_compute(ctx, nl, d_pos, d_sp, r_cut, precision, scatter, forces, per_atom,
+                         ctx->result.as<double>(), ctx->stats.as<unsigned long long>());
+    if (rc) return rc;
+    CK(cudaStreamSynchronize(ctx->stream));
+    *energy = 0.0;
+    if (virial)
+      for (int q = 0; q < 6; ++q) virial[q] = 0.0;
+    if (stats)
+      for (int q = 0; q < TB_NSTATS; ++q) stats[q] = 0;
+    return TB_OK;
+  }
+  // results: device buffers are written in place; pinned host buffers are
+  // written by the finalize kernel through their device alias (no copy-back);
+  // pageable host buffers go through staging and a copy
+  const bool f_dev = is_device_ptr(forces);
+  double *f_alias = f_dev ? nullptr : static_cast<double *>(host_alias(forces));
+  double *d_f = f_dev ? forces : f_alias;
+  if (!d_f) {
     CK(ctx->forces.ensure(sizeof(double) * 3 * std::max<int64_t>(n, 1)));
     d_f = ctx->forces.as<double>();
   }
-  bool e_dev = per_atom && is_device_ptr(per_atom);
+  const bool e_dev = per_atom && is_device_ptr(per_atom);
   double *d_e = per_atom;
   if (per_atom && !e_dev) {
     CK(ctx->per_atom.ensure(sizeof(double) * std::max<int64_t>(n, 1)));
     d_e = ctx->per_atom.as<double>();
   }
-  char *blk = ctx->errf.as<char>();
-  rc = enqueue_compute(ctx, nl, d_pos, d_sp, r_cut, precision, scatter, d_f, d_e,
-                       reinterpret_cast<double *>(blk + 64),
-                       reinterpret_cast<unsigned long long *>(blk + 128));
-  if (rc) return rc;
-  if (!f_dev && n)
-    CK(cudaMemcpyAsync(forces, d_f, sizeof(double) * 3 * n, cudaMemcpyDeviceToHost, ctx->stream));
-  if (per_atom && !e_dev && n)
-    CK(cudaMemcpyAsync(per_atom, d_e, sizeof(double) * n, cudaMemcpyDeviceToHost, ctx->stream));
+  // [ErrFlags | result @64 | stats @128] of this call land in pinned h_small,
+  // written by the finalize kernel
   char *h = reinterpret_cast<char *>(ctx->h_small);
-  CK(cudaMemcpyAsync(h, blk, 128 + sizeof(unsigned long long) * TB_NSTATS, cudaMemcpyDeviceToHost,
-                     ctx->stream));
-  CK(cudaStreamSynchronize(ctx->stream));
+  char *hd = static_cast<char *>(host_alias(h));
+  if (!hd) return fail(ctx, TB_ERR_CUDA, "pinned result block is not device-mapped");
+  const bool pa_async = per_atom && !e_dev && host_alias(per_atom);
+  if (pa_async && !ctx->side) {
+    CK(cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking));
+    CK(cudaEventCreateWithFlags(&ctx->ev_kernel_done, cudaEventDisableTiming));
+  }
+  ctx->fin_err_dst = reinterpret_cast<unsigned long long *>(hd);
+  cudaEvent_t keep_ev = ctx->ev_kernel_done;
+  if (!pa_async) ctx->ev_kernel_done = nullptr;
+  rc = enqueue_compute(ctx, nl, d_pos, d_sp, r_cut, precision, scatter, d_f, d_e,
+                       reinterpret_cast<double *>(hd + 64),
+                       reinterpret_cast<unsigned long long *>(hd + 128));
+  ctx->fin_err_dst = nullptr;
+  ctx->ev_kernel_done = keep_ev;
+  if (rc) return rc;
+  if (pa_async) {
+    // per-atom energies are final when the Tersoff kernel ends: copy them back
+    // on the side stream while the finalize kernel runs
+    CK(cudaStreamWaitEvent(ctx->side, ctx->ev_kernel_done, 0));
+    CK(cudaMemcpyAsync(per_atom, d_e, sizeof(double) * n, cudaMemcpyDeviceToHost, ctx->side));
+  } else if (per_atom && !e_dev) {
+    CK(cudaMemcpyAsync(per_atom, d_e, sizeof(double) * n, cudaMemcpyDeviceToHost, ctx->stream));
+  }
+  if (!f_dev && !f_alias)
+    CK(cudaMemcpyAsync(forces, d_f, sizeof(double) * 3 * n, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(spin_sync(ctx->stream));
+  if (pa_async) CK(spin_sync(ctx->side));
   ctx->err_unchecked = false;
   memcpy(ctx->h_err, h, sizeof(ErrFlags));
   rc = report_errors(ctx, nl, d_pos, d_sp);

@@ -409,6 +409,8 @@ __device__ __forceinline__ void finalize_body(int n, double *__restrict__ facc,
                                               double *__restrict__ result,
                                               unsigned long long *__restrict__ stats_acc,
                                               unsigned long long *__restrict__ stats_out,
+                                              const unsigned long long *__restrict__ err_src,
+                                              unsigned long long *__restrict__ err_dst,
                                               double (*s)[7] /* [NTHR/32][7] shared scratch */) {
   // block 0 reduces the block partials (E, W) and hands out the counters; the
   // other blocks move the forces (a one-block grid does both)
@@ -433,6 +435,9 @@ __device__ __forceinline__ void finalize_body(int n, double *__restrict__ facc,
       if (stats_out) stats_out[threadIdx.x] = __ldcg(stats_acc + threadIdx.x);
       stats_acc[threadIdx.x] = 0ull;
     }
+    // error flags of this evaluation next to the result (tb_compute's one block)
+    if (err_dst && threadIdx.x >= 32 && threadIdx.x < 32 + (int)(sizeof(ErrFlags) / 8))
+      err_dst[threadIdx.x - 32] = __ldcg(err_src + threadIdx.x - 32);
     if (gridDim.x > 1) return;
   }
   const int nb = gridDim.x > 1 ? gridDim.x - 1 : 1;
@@ -729,10 +734,12 @@ __global__ void __launch_bounds__(256) k_finalize(int n, double *__restrict__ fa
                            double *__restrict__ forces, int nparts,
                            const double *__restrict__ partials, double *__restrict__ result,
                            unsigned long long *__restrict__ stats_acc,
-                           unsigned long long *__restrict__ stats_out) {
+                           unsigned long long *__restrict__ stats_out,
+                           const unsigned long long *__restrict__ err_src,
+                           unsigned long long *__restrict__ err_dst) {
   __shared__ double s[256 / 32][7];
   finalize_body<MODE, 256>(n, facc, off, rev, fbuf, forces, nparts, partials, result, stats_acc,
-                           stats_out, s);
+                           stats_out, err_src, err_dst, s);
 }
 
 }  // namespace tb

@@ -15,12 +15,14 @@ There is no CPU path: a missing library raises NativeUnavailable.
 """
 
 import ctypes
+import weakref
 from dataclasses import dataclass, field
 
 import numpy as np
 
 from . import _native
 from .errors import ConfigurationError
+from .neighbor import _positions
 
 REFERENCE_TAGS = ("Reference", "ScalarOpt", "VecJ", "VecI")
 KERNEL_TAGS = ("B200",) + REFERENCE_TAGS
@@ -103,6 +105,36 @@ def _species_i32(state, n):
     return sp
 
 
+_PTRS = {}  # id(array) -> (weakref, shape, raw pointer): per-call pointer lookups cost ~1 us each
+
+
+def _ptr(a):
+    """Raw data pointer of an array or tensor, cached per live numpy array (a
+    changed shape -- the only way a live array's buffer can move -- misses)."""
+    if not isinstance(a, np.ndarray):
+        return _native.ptr(a)
+    e = _PTRS.get(id(a))
+    if e is not None and e[0]() is a and e[1] == a.shape:
+        return e[2]
+    p = _native.ptr(a)
+    if len(_PTRS) > 64:
+        _PTRS.clear()
+    _PTRS[id(a)] = (weakref.ref(a), a.shape, p)
+    return p
+
+
+class _Scratch:
+    """Per-context host buffers for the scalar results of tb_compute."""
+
+    def __init__(self):
+        self.energy = np.zeros(1)
+        self.virial = np.zeros(6)
+        self.stats = np.zeros(_native.NSTATS, dtype=np.int64)
+        self.p = (_native.ptr(self.energy), _native.ptr(self.virial), _native.ptr(self.stats))
+        self.chunks, self.used = ctypes.c_int64(), ctypes.c_int64()
+        self.refs = (ctypes.byref(self.chunks), ctypes.byref(self.used))
+
+
 def compute(state, nl, params, variant=None, threads=1, out=None):
     """One E+F(+virial) evaluation (kernels.py:517-527).
 
@@ -114,8 +146,7 @@ def compute(state, nl, params, variant=None, threads=1, out=None):
     buffers for a streaming driver); it is returned updated."""
     variant = variant or KernelVariant()
     ctx = nl.context
-    r_cut = ctx.set_table(params)
-    from .neighbor import _positions
+    ctx.set_table(params)
     pos = _positions(state)
     n = int(pos.shape[0])
     if n != nl.natoms:
@@ -133,26 +164,29 @@ def compute(state, nl, params, variant=None, threads=1, out=None):
     else:
         forces = np.empty((n, 3))
         per_atom = np.empty(n)
-    energy = np.zeros(1)
-    virial = np.zeros(6)
-    stats = np.zeros(_native.NSTATS, dtype=np.int64)
-    ctx.check(ctx.lib.tb_compute(ctx.handle, nl._nl.handle, _native.ptr(pos), _native.ptr(sp),
-                                 float(params.r_cut), _native.PRECISION[variant.precision],
-                                 _native.SCATTER[variant.scatter], _native.ptr(forces),
-                                 _native.ptr(per_atom), _native.ptr(energy), _native.ptr(virial),
-                                 _native.ptr(stats)), "tb_compute")
-    chunks, used = ctypes.c_int64(), ctypes.c_int64()
-    ctx.check(ctx.lib.tb_nlist_lanes(nl._nl.handle, ctypes.byref(chunks), ctypes.byref(used)),
-              "tb_nlist_lanes")
-    st = {"zeta_visits": int(stats[0]), "gathers": 0,
-          "lane_active": int(used.value), "lane_total": 32 * int(chunks.value),
-          "packed_pairs": int(stats[1]), "live_pairs": int(stats[2]),
-          "live_triplets": int(stats[3]), "taper_pairs": int(stats[4]),
-          "taper_triplets": int(stats[5])}
+    scr = getattr(ctx, "_scratch", None)
+    if scr is None:
+        scr = ctx._scratch = _Scratch()
+    lib = ctx.lib
+    rc = lib.tb_compute(ctx.handle, nl._nl.handle, _ptr(pos), _ptr(sp), float(params.r_cut),
+                        _native.PRECISION[variant.precision], _native.SCATTER[variant.scatter],
+                        _ptr(forces), _ptr(per_atom), *scr.p)
+    if rc:
+        ctx.check(rc, "tb_compute")
+    rc = lib.tb_nlist_lanes(nl._nl.handle, *scr.refs)
+    if rc:
+        ctx.check(rc, "tb_nlist_lanes")
+    stats = scr.stats.tolist()
+    st = {"zeta_visits": stats[0], "gathers": 0,
+          "lane_active": scr.used.value, "lane_total": 32 * scr.chunks.value,
+          "packed_pairs": stats[1], "live_pairs": stats[2],
+          "live_triplets": stats[3], "taper_pairs": stats[4],
+          "taper_triplets": stats[5]}
+    energy, virial = float(scr.energy[0]), scr.virial.copy()
     if out is not None:
-        out.potential_energy, out.stats, out.virial = float(energy[0]), st, virial
+        out.potential_energy, out.stats, out.virial = energy, st, virial
         return out
-    return ForceEnergyResult(forces, float(energy[0]), per_atom, st, virial)
+    return ForceEnergyResult(forces, energy, per_atom, st, virial)
 
 
 def kernel_function(variant, threads=1):
