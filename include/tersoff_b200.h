@@ -76,6 +76,12 @@ int tb_set_stream(tb_context *ctx, void *stream);
  * (default 25) of extra entries and warp chunks, the room tb_md_run's device
  * rebuild grows into before it has to replay from its entry state. */
 #define TB_OPT_LIST_MARGIN 2
+/* TB_OPT_LIVE_PACK = 0 / 1 / 2 (off / on / auto, default auto): before each
+ * evaluation cut every skin-list row to its entries with r < r_cut at the
+ * current positions (pack_adjacency, neighbor.py:330-360) and re-chunk the
+ * rows on the device, so that dead entries occupy no warp lanes.  Auto: on for
+ * atomic scatter over species-filtered rows (multi-species tables). */
+#define TB_OPT_LIVE_PACK 3
 int tb_set_option(tb_context *ctx, int option, int value);
 
 /* Synchronise the context's stream. */

@@ -24,6 +24,7 @@ SCATTER = {"atomic": 0, "gather": 1}
 NSTATS = 6
 OPT_TILE_KERNEL = 1
 OPT_LIST_MARGIN = 2  # percent of spare list entries / warp chunks (tb_md_run)
+OPT_LIVE_PACK = 3  # 0 off / 1 on / 2 auto: rows cut to r < r_cut and re-chunked per evaluation
 
 # symbol -> (restype, argtypes); the exported surface of the C ABI
 _P = ctypes.c_void_p

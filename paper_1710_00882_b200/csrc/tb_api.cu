@@ -77,6 +77,7 @@ struct tb_context {
   // kernel timing (tb_profile)
   bool profile = false;
   bool force_tile = false;
+  int live_pack = 2;  // TB_OPT_LIVE_PACK: 0 off, 1 on, 2 auto
   double list_margin = 0.25;  // TB_OPT_LIST_MARGIN
   bool warp_per_chunk = getenv("TB_WARP_PER_CHUNK") != nullptr;
   bool no_filter = getenv("TB_NO_FILTER") != nullptr;  // disable the species-pair compute filter
@@ -119,6 +120,11 @@ struct tb_nlist {
   Grid grid;
   int64_t ncell = 0;
   DevBuf plan;      // DevPlan
+  // live repack (TB_OPT_LIVE_PACK): rows cut to their entries with r < r_cut at
+  // the evaluation's positions (pack_adjacency, neighbor.py:330-360), re-chunked
+  // on the device every evaluation
+  DevBuf lplan, llen, lrow, lsorted, llanes;
+  int64_t lcap = 0;  // chunk capacity of llanes
   struct MdGraph *md = nullptr;
 };
 
@@ -339,6 +345,11 @@ extern "C" int tb_set_option(tb_context *ctx, int option, int value) {
     ctx->force_tile = value != 0;
     return TB_OK;
   }
+  if (option == TB_OPT_LIVE_PACK) {
+    if (value < 0 || value > 2) return fail(ctx, TB_ERR_ARG, "live-pack mode %d out of range", value);
+    ctx->live_pack = value;
+    return TB_OK;
+  }
   if (option == TB_OPT_LIST_MARGIN) {
     if (value < 0 || value > 1000) return fail(ctx, TB_ERR_ARG, "list margin %d%% out of range", value);
     ctx->list_margin = value / 100.0;
@@ -453,7 +464,8 @@ extern "C" void tb_nlist_destroy(tb_nlist *nl) {
                     &nl->cell_count, &nl->cell_start, &nl->cell_atoms, &nl->row_count,
                     &nl->maxrow, &nl->nl_row, &nl->sorted_atoms, &nl->sort_keys,
                     &nl->iota, &nl->lanes, &nl->hist, &nl->cpos, &nl->crow, &nl->coff,
-                    &nl->centry, &nl->fbuf, &nl->plan, &nl->scratch};
+                    &nl->centry, &nl->fbuf, &nl->plan, &nl->scratch, &nl->lplan, &nl->llen,
+                    &nl->lrow, &nl->lsorted, &nl->llanes};
   for (DevBuf *b : bufs) b->release();
   md_graph_release(nl);
   delete nl;
@@ -999,6 +1011,52 @@ static int reset_errors(tb_context *ctx) {
   return TB_OK;
 }
 
+// Live repack of the warp chunks (pack_adjacency at the evaluation's
+// positions, neighbor.py:330-360): every row is cut to its entries with
+// r^2 < r_cut^2 -- the same exact arithmetic as the kernel's own test -- and
+// the rows are re-bucketed by live length into warp chunks, all on the device
+// (k_live_rows, then the tb_md_run plan kernels).  Rows of the skin list that
+// are mostly dead (SiC: 12 Si-Si second neighbours at 3.08 A just outside the
+// 3.0 A cutoff) then no longer occupy idle lanes.
+static int live_repack(tb_context *ctx, tb_nlist *nl, const double *d_pos, double r_cut,
+                       bool filtered, const Box &box, ErrFlags *err) {
+  const int N = (int)nl->n;
+  const int64_t ent = filtered ? nl->ecap : std::max<int64_t>(nl->ecap, nl->entries);
+  // chunk bound: a bucket of length L holds floor(32/L) rows of L lanes, and
+  // floor(32/L) * L >= 17 for every L <= 32, so chunks <= entries / 17 + 34
+  const int64_t cap = ent / 17 + 34;
+  CK(nl->lplan.ensure(sizeof(DevPlan)));
+  CK(nl->llen.ensure(sizeof(int) * std::max(N, 1)));
+  CK(nl->lrow.ensure(sizeof(int) * std::max<int64_t>(ent, 1)));
+  CK(nl->lsorted.ensure(sizeof(int) * std::max(N, 1)));
+  if (nl->lcap < cap) {
+    CK(nl->llanes.ensure(sizeof(int4) * 32 * cap));
+    nl->lcap = cap;
+  }
+  DevPlan *plan = nl->lplan.as<DevPlan>();
+  const int *start = filtered ? nl->coff.as<int>() : nl->offsets.as<int>();
+  constexpr int G = 8;  // lanes per row
+  if (filtered)
+    k_live_rows<true, G><<<nblk((int64_t)N * G, 256), 256, 0, ctx->stream>>>(
+        N, d_pos, box, r_cut * r_cut, start, nl->crow.as<int>(), nl->centry.as<int>(),
+        nl->nbr.as<int>(), nl->llen.as<int>(), nl->lrow.as<int>(), err);
+  else
+    k_live_rows<false, G><<<nblk((int64_t)N * G, 256), 256, 0, ctx->stream>>>(
+        N, d_pos, box, r_cut * r_cut, start, nullptr, nullptr, nl->nbr.as<int>(),
+        nl->llen.as<int>(), nl->lrow.as<int>(), err);
+  CK(cudaGetLastError());
+  CK(cudaMemsetAsync(plan, 0, sizeof(DevPlan), ctx->stream));
+  k_len_hist_plan<<<std::min(nblk(N, 256), 296), 256, 0, ctx->stream>>>(N, nl->llen.as<int>(), plan);
+  k_plan<<<1, 32, 0, ctx->stream>>>(plan, nullptr, N, 0, (int)nl->lcap);
+  k_bucket_rows<<<nblk(N, 256), 256, 0, ctx->stream>>>(N, nl->llen.as<int>(), plan,
+                                                       nl->lsorted.as<int>());
+  k_fill_lanes_dev<<<(int)std::min<int64_t>(nblk(nl->lcap, 8), 148 * 8), 256, 0, ctx->stream>>>(
+      plan, nl->lsorted.as<int>(), start, nl->lrow.as<int>(), nl->nbr.as<int>(),
+      nl->llanes.as<int4>());
+  CK(cudaGetLastError());
+  return TB_OK;
+}
+
 // enqueue the evaluation; every pointer is a device pointer
 static int enqueue_compute(tb_context *ctx, const tb_nlist *nl, const double *d_pos,
                            const int *d_species, double r_cut, int precision, int scatter,
@@ -1088,17 +1146,35 @@ static int enqueue_compute(tb_context *ctx, const tb_nlist *nl, const double *d_
     w.nchunks = nl->nchunks;
     w.n_empty = nl->n_empty;
     w.dinfo = nullptr;
+    w.count_packed = filtered ? 0 : 1;
+    // live repack: atomic scatter only (the gather finalize reads every entry's
+    // slot, which must then be rewritten each evaluation); auto = species-
+    // filtered rows (SiC: 12 mostly dead Si-Si entries per Si row; c3 step
+    // 501 -> 395 us).  Long single-species rows (disordered Si, c4) gain
+    // 575 -> 371 us in the kernel but pay it back in the repack pass.
+    const bool live = !ctx->dplan && scatter == TB_SCATTER_ATOMIC &&
+                      (ctx->live_pack == 1 || (ctx->live_pack == 2 && filtered));
     if (ctx->dplan) {  // tb_md_run capture: chunk counts live in the device plan
       w.dinfo = ctx->dplan;
       w.nchunks = (int)nl->ccap;  // grid sizing only
+    } else if (live) {
+      int lrc = live_repack(ctx, const_cast<tb_nlist *>(nl), d_pos, r_cut, filtered, a.box, a.err);
+      if (lrc) return lrc;
+      w.lanes = nl->llanes.as<int4>();
+      w.empty_atoms = nl->lsorted.as<int>();
+      w.dinfo = nl->lplan.as<int>();  // DevPlan starts with {nchunks, n_empty}
+      w.nchunks = (int)nl->lcap;      // grid sizing only
+      // unfiltered: the chunked rows are exactly the packed rows (zeta_visits
+      // counted in the kernel); filtered rows miss entries the reference
+      // counts, so k_pack_stats still counts over the full rows
+      w.count_packed = filtered ? 0 : 1;
     }
     w.facc = ctx->facc.as<double>();
-    w.count_packed = filtered ? 0 : 1;
     const bool want_stats = d_stats != nullptr;
     rc = precision == TB_PREC_DOUBLE ? launch_warp_prec<double>(ctx, nl, a, w, scatter, want_stats)
                                      : launch_warp_prec<float>(ctx, nl, a, w, scatter, want_stats);
     nparts = ctx->last_blocks;
-    if (!rc && filtered && want_stats) {
+    if (!rc && filtered && want_stats && !w.count_packed) {
       k_pack_stats<<<nblk(n, 256), 256, 0, ctx->stream>>>(n, d_pos, a.box, a.rc2, a.off, a.nbr,
                                                            a.stats);
       CK(cudaGetLastError());
@@ -1465,7 +1541,7 @@ static int enqueue_rebuild_device(tb_context *ctx, tb_nlist *nl, const double *d
   } else {
     k_bucket_rows<<<nblk(N, 256), 256, 0, st>>>(N, row_len, plan, nl->sorted_atoms.as<int>());
   }
-  k_fill_lanes_dev<<<nblk(ccap, 8), 256, 0, st>>>(plan, nl->sorted_atoms.as<int>(), loff, cent,
+  k_fill_lanes_dev<<<(int)std::min<int64_t>(nblk(ccap, 8), 148 * 8), 256, 0, st>>>(plan, nl->sorted_atoms.as<int>(), loff, cent,
                                           nl->nbr.as<int>(), nl->lanes.as<int4>());
   if (scatter == TB_SCATTER_GATHER)
     k_nl_reverse<<<nblk(N, 256), 256, 0, st>>>(N, nl->offsets.as<int>(), nl->nbr.as<int>(),

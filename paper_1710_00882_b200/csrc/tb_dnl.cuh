@@ -164,25 +164,79 @@ __global__ void k_bucket_rows(int n, const int *__restrict__ row_len, DevPlan *_
   if (L >= 0 && L <= 32) sorted_atoms[plan->bucket_start[L] + s_base[L] + slot] = i;
 }
 
-// one warp per chunk (8 chunks per block): lane -> {entry, i, j, L}
+// one warp per chunk, grid-stride (any grid): lane -> {entry, i, j, L}; the
+// plan's bucket tables are staged in shared memory once per block
 __global__ void __launch_bounds__(256) k_fill_lanes_dev(const DevPlan *__restrict__ plan,
                                  const int *__restrict__ sorted_atoms,
                                  const int *__restrict__ offsets, const int *__restrict__ centry,
                                  const int *__restrict__ nbr, int4 *__restrict__ lanes) {
-  const int c = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
-  if (c >= plan->nchunks) return;
-  int L = 1;
-  while (L < 32 && plan->chunk_base[L + 1] <= c) ++L;
-  const int rpc = 32 / L;
-  const int row = (c - plan->chunk_base[L]) * rpc + lane / L;
-  int4 v = make_int4(-1, 0, 0, L);
-  if (lane < rpc * L && row < plan->hist[L]) {
-    const int atom = sorted_atoms[plan->bucket_start[L] + row];
-    const int k = offsets[atom] + lane % L;
-    const int e = centry ? centry[k] : k;
-    v = make_int4(e, atom, nbr[e], L);
+  __shared__ int s_base[34], s_start[34], s_hist[34];
+  if (threadIdx.x < 34) {
+    s_base[threadIdx.x] = plan->chunk_base[threadIdx.x];
+    s_start[threadIdx.x] = plan->bucket_start[threadIdx.x];
+    s_hist[threadIdx.x] = plan->hist[threadIdx.x];
   }
-  lanes[32 * (int64_t)c + lane] = v;
+  __syncthreads();
+  const int nch = plan->nchunks, lane = threadIdx.x & 31;
+  for (int c = blockIdx.x * 8 + (threadIdx.x >> 5); c < nch; c += gridDim.x * 8) {
+    int L = 1;
+    while (L < 32 && s_base[L + 1] <= c) ++L;
+    const int rpc = 32 / L;
+    const int row = (c - s_base[L]) * rpc + lane / L;
+    int4 v = make_int4(-1, 0, 0, L);
+    if (lane < rpc * L && row < s_hist[L]) {
+      const int atom = sorted_atoms[s_start[L] + row];
+      const int k = offsets[atom] + lane % L;
+      const int e = centry ? centry[k] : k;
+      v = make_int4(e, atom, nbr[e], L);
+    }
+    lanes[32 * (int64_t)c + lane] = v;
+  }
+}
+
+// live rows for the repack (tb_api.cu live_repack): the entries of row i
+// with r^2 < rc2 at the current positions, in row order, compacted to the
+// start of the row's slots.  G lanes per row test G entries at a time (one
+// round of dependent gathers instead of one per entry); also the non-finite
+// check for every atom (a non-finite atom's rows come out empty, so the
+// Tersoff kernel would never see it)
+template <bool FILT, int G>
+__global__ void __launch_bounds__(256) k_live_rows(int n, const double *__restrict__ pos, Box box,
+                                                   double rc2, const int *__restrict__ start,
+                                                   const int *__restrict__ crow,
+                                                   const int *__restrict__ centry,
+                                                   const int *__restrict__ nbr,
+                                                   int *__restrict__ llen, int *__restrict__ lrow,
+                                                   ErrFlags *__restrict__ err) {
+  static_assert(G > 0 && G < 32 && (32 % G) == 0, "row groups tile the warp");
+  const int i = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / G);
+  const int lane = threadIdx.x & 31, sub = lane % G, g0 = lane - sub;
+  const bool act = i < n;
+  int b = 0, end = 0;
+  double xi[3] = {0, 0, 0};
+  if (act) {
+    b = start[i];
+    end = FILT ? b + crow[i] : start[i + 1];
+    load3(pos, i, xi);
+    if (sub == 0 && !(isfinite(xi[0]) && isfinite(xi[1]) && isfinite(xi[2])))
+      atomicMin(&err->nonfinite_atom, i);
+  }
+  int q = 0;
+  for (int k0 = b; __any_sync(0xffffffffu, act && k0 < end); k0 += G) {
+    const int k = k0 + sub;
+    bool lv = false;
+    int e = 0;
+    if (act && k < end) {
+      e = FILT ? __ldg(centry + k) : k;
+      double xj[3], d[3];
+      load3(pos, __ldg(nbr + e), xj);
+      lv = disp_r2(xi, xj, box, d) < rc2;
+    }
+    const unsigned gm = (__ballot_sync(0xffffffffu, lv) >> g0) & ((1u << G) - 1u);
+    if (lv) lrow[b + q + __popc(gm & ((1u << sub) - 1u))] = e;
+    q += __popc(gm);
+  }
+  if (act && sub == 0) llen[i] = q;
 }
 
 // histogram of row lengths into the device plan (block-private bins)

@@ -75,6 +75,31 @@ def test_fp64_matches_reference(name, scatter, kernel_path):
     assert r.stats["zeta_visits"] == int(g["zeta_visits"])
 
 
+@pytest.mark.parametrize("live", [0, 1])
+@pytest.mark.parametrize("precision", ["double", "single"])
+@pytest.mark.parametrize("name", ["si512", "sic216", "disordered"])
+def test_live_repack_matches_reference(name, precision, live):
+    """TB_OPT_LIVE_PACK forced off / on (rows cut to r < r_cut and re-chunked on
+    the device before each evaluation): same results and counters."""
+    from paper_1710_00882_b200 import _native
+    g = load_golden(name)
+    t = parse_params(str(g["table"]))
+    ctx = _native.default_context(0)
+    ctx.set_option(_native.OPT_LIVE_PACK, live)
+    try:
+        fr = golden_frame(g)
+        nl, r = gpu_eval(fr, t, precision, "atomic")
+        r2 = B.compute(fr, nl, t, B.make_variant("B200", precision=precision))  # second pass
+    finally:
+        ctx.set_option(_native.OPT_LIVE_PACK, 2)
+    e = float(g["energy"])
+    tol = FP64_TOL if precision == "double" else MIXED_TOL
+    for res in (r, r2):
+        assert abs(res.potential_energy - e) <= tol * abs(e)
+        assert rel_f(res.forces, g["forces"]) <= tol
+        assert res.stats["zeta_visits"] == int(g["zeta_visits"])
+
+
 @pytest.mark.parametrize("name", ["si512", "sic216", "disordered"])
 def test_mixed_matches_reference_fp64(name, kernel_path):
     g = load_golden(name)

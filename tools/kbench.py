@@ -12,6 +12,8 @@ t = B.builtin_params(tn)
 n = st.natoms
 s = torch.cuda.Stream(); torch.cuda.set_stream(s)
 ctx = _native.default_context(0); ctx.set_stream(s.cuda_stream); ctx.set_table(t)
+if os.environ.get("KB_LIVE"):
+    ctx.set_option(_native.OPT_LIVE_PACK, int(os.environ["KB_LIVE"]))
 pos = torch.from_numpy(st.positions).cuda(); sp = torch.from_numpy(st.species.astype(np.int32)).cuda()
 f = torch.empty((n, 3), dtype=torch.float64, device="cuda"); pa = torch.empty(n, dtype=torch.float64, device="cuda")
 res = torch.zeros(8, dtype=torch.float64, device="cuda"); stt = torch.zeros(6, dtype=torch.int64, device="cuda")

@@ -12,6 +12,8 @@ st, tn = structures.config(cfg, small=os.environ.get("KB_SMALL") == "1")
 t = B.builtin_params(tn)
 n = st.natoms
 ctx = _native.default_context(0); ctx.set_table(t)
+if os.environ.get("KB_LIVE"):
+    ctx.set_option(_native.OPT_LIVE_PACK, int(os.environ["KB_LIVE"]))
 ctx.set_stream(torch.cuda.current_stream().cuda_stream)
 pos = torch.from_numpy(st.positions).cuda(); sp = torch.from_numpy(st.species.astype(np.int32)).cuda()
 f = torch.empty((n, 3), dtype=torch.float64, device="cuda"); pa = torch.empty(n, dtype=torch.float64, device="cuda")
