@@ -54,11 +54,21 @@ struct WArgs {
   double *__restrict__ facc;           // ATOMIC: zeroed force accumulator (n,3)
 };
 
+template <bool REG>
 struct WAcc {
-  // energy and virial live in the per-lane shared slots (acc[7][32]) to keep
-  // registers for occupancy; only the optional counters stay in registers
+  // energy and virial per lane: in registers for the mixed kernel (REG; its
+  // L1/shared pipe is the busiest unit), in the per-lane shared slots
+  // (acc[7][32]) for fp64, whose registers are spent on occupancy
   double *acc;  // &s_acc[wid][0][lane], stride 32
-  unsigned long long c_vis = 0, c_pk = 0, c_lp = 0, c_lt = 0, c_tp = 0, c_tt = 0;
+  double r[REG ? 7 : 1];
+  unsigned long long c_vis = 0, c_pk = 0, c_lp = 0, c_tp = 0, c_lt = 0, c_tt = 0;
+  __device__ __forceinline__ void add(int q, double v) {
+    if (REG)
+      r[q] += v;
+    else
+      acc[32 * q] += v;
+  }
+  __device__ __forceinline__ double get(int q) const { return REG ? r[q] : acc[32 * q]; }
 };
 
 // per-warp table of the lanes' neighbour data, read by the other lanes of
@@ -120,7 +130,7 @@ template <class T, int S, bool LAM3, int MODE, bool ST, int LC>
 __device__ __forceinline__ void chunk_body(const KArgs &a, const WArgs &w, const Tables<T, S> &tab,
                                            T (*s_cache)[3][32], WTable<T> &tb, const int lane,
                                            const int4 cur, const WStage &stg, const int Ldyn,
-                                           WAcc &A) {
+                                           WAcc<sizeof(T) == 4> &A) {
   static_assert(S <= 2, "the warp kernel handles up to two species");
   using T2 = typename Vec2<T>::t;
   const int e = cur.x, i = cur.y, j = cur.z;
@@ -206,6 +216,10 @@ __device__ __forceinline__ void chunk_body(const KArgs &a, const WArgs &w, const
   __syncwarp();
 
   // ---- phase 1: zeta (and the angular cache) ----
+  // the cache of (cos, g, dg) per partner: registers for the unrolled mixed
+  // kernel (compile-time indices), shared memory otherwise
+  constexpr bool RC = LC > 0 && sizeof(T) == 4;
+  T rcos[RC ? QCAP : 1], rg[RC ? QCAP : 1], rdg[RC ? QCAP : 1];
   T zeta = T(0);
   // only live partners of the row contribute (a dead b has f_C = dzeta = 0);
   // lanes iterate their own row's live mask (the table is in shared memory,
@@ -233,9 +247,15 @@ __device__ __forceinline__ void chunk_body(const KArgs &a, const WArgs &w, const
     T g, dg;
     angular(cost, tp, g, dg);
     if (q < QCAP) {
-      s_cache[q][0][lane] = cost;
-      s_cache[q][1][lane] = g;
-      s_cache[q][2][lane] = dg;
+      if (RC) {
+        rcos[q] = cost;
+        rg[q] = g;
+        rdg[q] = dg;
+      } else {
+        s_cache[q][0][lane] = cost;
+        s_cache[q][1][lane] = g;
+        s_cache[q][2][lane] = dg;
+      }
     }
     const T f = (S > 1 && sj == 1) ? bfc.y : bfc.x;  // f_C(r_b) with entry (i, a, b)
     if (pair_live && f != T(0)) {
@@ -295,9 +315,15 @@ __device__ __forceinline__ void chunk_body(const KArgs &a, const WArgs &w, const
     const T rb = bzr.y;
     T cost, g, dg;
     if (q < QCAP) {
-      cost = s_cache[q][0][lane];
-      g = s_cache[q][1][lane];
-      dg = s_cache[q][2][lane];
+      if (RC) {
+        cost = rcos[q];
+        g = rg[q];
+        dg = rdg[q];
+      } else {
+        cost = s_cache[q][0][lane];
+        g = s_cache[q][1][lane];
+        dg = s_cache[q][2][lane];
+      }
     } else {
       cost = ex * bxy.x + ey * bxy.y + ez * bzr.x;
       cost = fmin(T(1), fmax(T(-1), cost));
@@ -337,12 +363,12 @@ __device__ __forceinline__ void chunk_body(const KArgs &a, const WArgs &w, const
     fx = -(double)(ca * ex + inva * Sbx);
     fy = -(double)(ca * ey + inva * Sby);
     fz = -(double)(ca * ez + inva * Sbz);
-    A.acc[32 * 1] += d[0] * fx;
-    A.acc[32 * 2] += d[1] * fy;
-    A.acc[32 * 3] += d[2] * fz;
-    A.acc[32 * 4] += d[0] * fy;
-    A.acc[32 * 5] += d[0] * fz;
-    A.acc[32 * 6] += d[1] * fz;
+    A.add(1, d[0] * fx);
+    A.add(2, d[1] * fy);
+    A.add(3, d[2] * fz);
+    A.add(4, d[0] * fy);
+    A.add(5, d[0] * fz);
+    A.add(6, d[1] * fz);
   }
   if (MODE == 0) {
     // F_i = -sum_a f_a (translation invariance of the terms on i): a segmented
@@ -394,7 +420,7 @@ __device__ __forceinline__ void chunk_body(const KArgs &a, const WArgs &w, const
 #pragma unroll
     for (int q = 0; q < (LC > 0 ? LC : 1); ++q) se += tb.v[lane + q];
     for (int q = LC > 0 ? LC : 1; q < L; ++q) se += tb.v[lane + q];
-    A.acc[0] += se;
+    A.add(0, se);
     if (a.per_atom) a.per_atom[i] = se + 0.0;
   }
 }
@@ -531,10 +557,12 @@ __global__ void __launch_bounds__(WNT, sizeof(T) == 4 ? TB_WARP_MINB_F : TB_WARP
     if (sm < 0 || sm >= S) atomicMin(&a.err->bad_species_atom, m);
   }
 
-  WAcc A;
+  WAcc<sizeof(T) == 4> A;
 #pragma unroll
   for (int q = 0; q < 7; ++q) s_acc[wid][q][lane] = 0.0;
   A.acc = &s_acc[wid][0][lane];
+#pragma unroll
+  for (int q = 0; q < (sizeof(T) == 4 ? 7 : 1); ++q) A.r[q] = 0.0;
 
   // software pipeline over this warp's chunks: lane records in registers two
   // chunks ahead; the position/species gathers of the next chunk are issued
@@ -605,7 +633,7 @@ __global__ void __launch_bounds__(WNT, sizeof(T) == 4 ? TB_WARP_MINB_F : TB_WARP
   }
   double vals[7];
 #pragma unroll
-  for (int q = 0; q < 7; ++q) vals[q] = s_acc[wid][q][lane];
+  for (int q = 0; q < 7; ++q) vals[q] = A.get(q);
 #pragma unroll
   for (int q = 0; q < 7; ++q) {
     double v = warp_sum(vals[q]);

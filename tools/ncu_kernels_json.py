@@ -1,0 +1,41 @@
+"""Summarise the ncu raw exports of tools/ncu_kernels.sh into profiles/ JSON:
+duration, DRAM bytes and GB/s against the measured HBM peak, pipe / issue /
+L1 utilisation, lane efficiency.  Usage: python tools/ncu_kernels_json.py OUT.json"""
+import csv, glob, json, sys
+TS = {"ns": 1e-3, "nsecond": 1e-3, "us": 1.0, "usecond": 1.0, "ms": 1e3, "msecond": 1e3}
+BS = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+out = {"method": "ncu --set full --clock-control none, one k_tersoff_warp launch after two "
+                 "warm-up evaluations (tools/ncu_kernels.sh, tools/kone.py CONFIG PREC 0); "
+                 "cold caches (ncu default cache control)",
+       "peaks": {"dram_GBs_measured": 6552.3, "source": "MEASURED_PEAKS.json hbm_gbs"},
+       "kernels": {}}
+for f in sorted(glob.glob("gpurun_out/ncu_tk_c*_p*_raw.csv")):
+    rows = list(csv.reader(open(f)))
+    d, u = dict(zip(rows[0], rows[2])), dict(zip(rows[0], rows[1]))
+
+    def g(k):
+        try:
+            return float(d[k].replace(",", ""))
+        except (KeyError, ValueError):
+            return None
+    tag = f.split("ncu_tk_")[1].replace("_raw.csv", "")
+    dur = g("gpu__time_duration.sum") * TS[u["gpu__time_duration.sum"]]
+    byts = sum((g(k) or 0.0) * BS[u[k]] for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"))
+    out["kernels"][tag] = {
+        "kernel": d.get("Kernel Name", "")[:90],
+        "duration_us": round(dur, 2), "dram_bytes": byts,
+        "dram_GBs": round(byts / dur / 1e3, 1),
+        "dram_frac_of_measured": round(byts / dur / 1e3 / 6552.3, 4),
+        "fp64_pipe_pct": g("sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active"),
+        "fma_pipe_pct": g("sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active"),
+        "issue_active_pct": g("smsp__issue_active.avg.pct_of_peak_sustained_active"),
+        "l1tex_pct": g("l1tex__throughput.avg.pct_of_peak_sustained_active"),
+        "sm_active_of_elapsed_pct": round(100 * g("sm__cycles_active.avg") / g("sm__cycles_elapsed.avg"), 1),
+        "threads_per_inst": g("smsp__thread_inst_executed_per_inst_executed.ratio"),
+        "registers": g("launch__registers_per_thread"),
+        "occupancy_pct": g("sm__warps_active.avg.pct_of_peak_sustained_active"),
+    }
+json.dump(out, open(sys.argv[1], "w"), indent=1)
+for k, v in out["kernels"].items():
+    print(k, {a: v[a] for a in ("duration_us", "dram_GBs", "fp64_pipe_pct", "fma_pipe_pct",
+                                "issue_active_pct", "l1tex_pct", "sm_active_of_elapsed_pct")})
