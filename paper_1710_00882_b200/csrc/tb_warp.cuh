@@ -27,6 +27,9 @@ namespace tb {
 #ifndef TB_WARP_MINB_F
 #define TB_WARP_MINB_F 4
 #endif
+#ifndef TB_FP64_REG
+#define TB_FP64_REG 0  // fp64 kernel: energy/virial + angular cache in registers too
+#endif
 constexpr int WNT = 128;  // threads per block of the warp kernel
 constexpr int WPB = WNT / 32;
 constexpr int QCAP = 4;   // k-iterations whose angular values are cached
@@ -76,16 +79,57 @@ struct WAcc {
 template <class T> struct Vec2;
 template <> struct Vec2<double> { using t = double2; };
 template <> struct Vec2<float> { using t = float2; };
+template <class T> struct Vec4;
+template <> struct Vec4<double> { using t = double4; };
+template <> struct Vec4<float> { using t = float4; };
 
+// Mixed kernel (float): {e, r} as one float4 and, with one species,
+// {f_C, delta_zeta} as one float2 -- fewer shared-memory instructions for the
+// kernel whose L1/shared pipe is the bottleneck.  fp64 keeps the split
+// double2 arrays (measured faster there).
 template <class T>
 struct WTable {
   using T2 = typename Vec2<T>::t;
-  T2 exy[32];   // e_x, e_y
-  T2 ezr[32];   // e_z, r
-  T2 fc[32];    // f_C(r) with the k-role entry for j-species 0 / 1
+  using T4 = typename Vec4<T>::t;
+  static constexpr bool PACKED = sizeof(T) == 4;
+  T4 er[PACKED ? 32 : 1];   // e_x, e_y, e_z, r
+  T2 exy[PACKED ? 1 : 32];  // e_x, e_y
+  T2 ezr[PACKED ? 1 : 32];  // e_z, r
+  T2 fc[32];    // f_C(r) with the k-role entry for j-species 0 / 1; one species,
+                // packed: {f_C, delta_zeta} (delta_zeta stored after phase 1)
   T dz[32];     // delta_zeta of the (i, lane) pair
   double v[32]; // V of the (i, lane) pair (row sum -> e_i)
   int sp[32];   // species of the lane's neighbour
+  __device__ __forceinline__ T4 e(int k) const {
+    if (PACKED) return er[k];
+    T4 o;
+    const T2 a = exy[k], b = ezr[k];
+    o.x = a.x;
+    o.y = a.y;
+    o.z = b.x;
+    o.w = b.y;
+    return o;
+  }
+  __device__ __forceinline__ void set_e(int k, T x, T y, T z, T r) {
+    if (PACKED) {
+      T4 o;
+      o.x = x;
+      o.y = y;
+      o.z = z;
+      o.w = r;
+      er[k] = o;
+    } else {
+      T2 a, b;
+      a.x = x;
+      a.y = y;
+      b.x = z;
+      b.y = r;
+      exy[k] = a;
+      ezr[k] = b;
+    }
+  }
+  // delta_zeta of lane k: in fc[k].y for one species in the packed layout
+  static constexpr bool DZ_IN_FC = PACKED;
 };
 
 // per-warp double-buffered staging of the gathered operands (cp.async)
@@ -130,7 +174,7 @@ template <class T, int S, bool LAM3, int MODE, bool ST, int LC>
 __device__ __forceinline__ void chunk_body(const KArgs &a, const WArgs &w, const Tables<T, S> &tab,
                                            T (*s_cache)[3][32], WTable<T> &tb, const int lane,
                                            const int4 cur, const WStage &stg, const int Ldyn,
-                                           WAcc<sizeof(T) == 4> &A) {
+                                           WAcc<sizeof(T) == 4 || TB_FP64_REG> &A) {
   static_assert(S <= 2, "the warp kernel handles up to two species");
   using T2 = typename Vec2<T>::t;
   const int e = cur.x, i = cur.y, j = cur.z;
@@ -201,15 +245,10 @@ __device__ __forceinline__ void chunk_body(const KArgs &a, const WArgs &w, const
   const PairP<T> &pp = tab.pair[si * S + sj];
   const bool pair_live = live && ra < pp.Rp;
   {
-    T2 a2, b2, c2;
-    a2.x = ex;
-    a2.y = ey;
-    b2.x = ez;
-    b2.y = ra;
+    T2 c2;
     c2.x = fck[0];
     c2.y = fck[S > 1 ? 1 : 0];
-    tb.exy[lane] = a2;
-    tb.ezr[lane] = b2;
+    tb.set_e(lane, ex, ey, ez, ra);
     tb.fc[lane] = c2;
     if (S > 1) tb.sp[lane] = sj;
   }
@@ -218,7 +257,7 @@ __device__ __forceinline__ void chunk_body(const KArgs &a, const WArgs &w, const
   // ---- phase 1: zeta (and the angular cache) ----
   // the cache of (cos, g, dg) per partner: registers for the unrolled mixed
   // kernel (compile-time indices), shared memory otherwise
-  constexpr bool RC = LC > 0 && sizeof(T) == 4;
+  constexpr bool RC = LC > 0 && (sizeof(T) == 4 || TB_FP64_REG);
   T rcos[RC ? QCAP : 1], rg[RC ? QCAP : 1], rdg[RC ? QCAP : 1];
   T zeta = T(0);
   // only live partners of the row contribute (a dead b has f_C = dzeta = 0);
@@ -239,10 +278,11 @@ __device__ __forceinline__ void chunk_body(const KArgs &a, const WArgs &w, const
       src = __ffs(m) - 1;
       m &= m - 1;
     }
-    const T2 bxy = tb.exy[src], bzr = tb.ezr[src], bfc = tb.fc[src];
+    const typename Vec4<T>::t be = tb.e(src);
+    const T2 bfc = tb.fc[src];
     const int sb = S > 1 ? tb.sp[src] : 0;
     const TripP<T> &tp = tab.trip[(si * S + sj) * S + sb];
-    T cost = ex * bxy.x + ey * bxy.y + ez * bzr.x;
+    T cost = ex * be.x + ey * be.y + ez * be.z;
     cost = fmin(T(1), fmax(T(-1), cost));
     T g, dg;
     angular(cost, tp, g, dg);
@@ -266,7 +306,7 @@ __device__ __forceinline__ void chunk_body(const KArgs &a, const WArgs &w, const
       T term = f * g;
       if (LAM3) {
         T exv, darg;
-        lam3_term(ra - bzr.y, tp, exv, darg);
+        lam3_term(ra - be.w, tp, exv, darg);
         term *= exv;
       }
       zeta += term;
@@ -284,7 +324,10 @@ __device__ __forceinline__ void chunk_body(const KArgs &a, const WArgs &w, const
     pair_part(ra, zeta, pp, v, dvdr, dz);
 #endif
   }
-  tb.dz[lane] = dz;
+  if (S == 1 && WTable<T>::DZ_IN_FC)
+    tb.fc[lane].y = dz;
+  else
+    tb.dz[lane] = dz;
   tb.v[lane] = (double)v;
   __syncwarp();
 
@@ -301,8 +344,8 @@ __device__ __forceinline__ void chunk_body(const KArgs &a, const WArgs &w, const
       src = __ffs(m) - 1;
       m &= m - 1;
     }
-    const T dzb = tb.dz[src];
     const T2 bfc = tb.fc[src];
+    const T dzb = (S == 1 && WTable<T>::DZ_IN_FC) ? bfc.y : tb.dz[src];
     const int sb = S > 1 ? tb.sp[src] : 0;
     const T f_b = (S > 1 && sj == 1) ? bfc.y : bfc.x;  // f_C(r_b) in (i,a,b)
     const T f_a = pick(fck, sb);                        // f_C(r_a) in (i,b,a)
@@ -311,8 +354,8 @@ __device__ __forceinline__ void chunk_body(const KArgs &a, const WArgs &w, const
     // f_C may round to 0 in the taper while dF_C/dr does not: test both
     const bool t2 = (dzb != T(0)) && (f_a != T(0) || df_a != T(0));
     if (!(t1 || t2)) continue;
-    const T2 bxy = tb.exy[src], bzr = tb.ezr[src];
-    const T rb = bzr.y;
+    const typename Vec4<T>::t be = tb.e(src);
+    const T rb = be.w;
     T cost, g, dg;
     if (q < QCAP) {
       if (RC) {
@@ -325,7 +368,7 @@ __device__ __forceinline__ void chunk_body(const KArgs &a, const WArgs &w, const
         dg = s_cache[q][2][lane];
       }
     } else {
-      cost = ex * bxy.x + ey * bxy.y + ez * bzr.x;
+      cost = ex * be.x + ey * be.y + ez * be.z;
       cost = fmin(T(1), fmax(T(-1), cost));
       angular(cost, tab.trip[(si * S + sj) * S + sb], g, dg);
     }
@@ -353,9 +396,9 @@ __device__ __forceinline__ void chunk_body(const KArgs &a, const WArgs &w, const
     }
     Sal += alpha;
     Sc += beta * cost;
-    Sbx += beta * bxy.x;
-    Sby += beta * bxy.y;
-    Sbz += beta * bzr.x;
+    Sbx += beta * be.x;
+    Sby += beta * be.y;
+    Sbz += beta * be.z;
   }
   double fx = 0.0, fy = 0.0, fz = 0.0;
   if (live) {
@@ -557,12 +600,12 @@ __global__ void __launch_bounds__(WNT, sizeof(T) == 4 ? TB_WARP_MINB_F : TB_WARP
     if (sm < 0 || sm >= S) atomicMin(&a.err->bad_species_atom, m);
   }
 
-  WAcc<sizeof(T) == 4> A;
+  WAcc<sizeof(T) == 4 || TB_FP64_REG> A;
 #pragma unroll
   for (int q = 0; q < 7; ++q) s_acc[wid][q][lane] = 0.0;
   A.acc = &s_acc[wid][0][lane];
 #pragma unroll
-  for (int q = 0; q < (sizeof(T) == 4 ? 7 : 1); ++q) A.r[q] = 0.0;
+  for (int q = 0; q < (sizeof(T) == 4 || TB_FP64_REG ? 7 : 1); ++q) A.r[q] = 0.0;
 
   // software pipeline over this warp's chunks: lane records in registers two
   // chunks ahead; the position/species gathers of the next chunk are issued
