@@ -328,7 +328,8 @@ __device__ __forceinline__ void chunk_body(const KArgs &a, const WArgs &w, const
     tb.fc[lane].y = dz;
   else
     tb.dz[lane] = dz;
-  tb.v[lane] = (double)v;
+  const double vd = (double)v;
+  if (sizeof(T) == 8) tb.v[lane] = vd;
   __syncwarp();
 
   // ---- phase 2: force on this neighbour from the terms centred on i ----
@@ -401,11 +402,15 @@ __device__ __forceinline__ void chunk_body(const KArgs &a, const WArgs &w, const
     Sbz += beta * be.z;
   }
   double fx = 0.0, fy = 0.0, fz = 0.0;
+  T tfx = T(0), tfy = T(0), tfz = T(0);
   if (live) {
     const T ca = dvdr + Sal - Sc * inva;
-    fx = -(double)(ca * ex + inva * Sbx);
-    fy = -(double)(ca * ey + inva * Sby);
-    fz = -(double)(ca * ez + inva * Sbz);
+    tfx = -(ca * ex + inva * Sbx);
+    tfy = -(ca * ey + inva * Sby);
+    tfz = -(ca * ez + inva * Sbz);
+    fx = (double)tfx;
+    fy = (double)tfy;
+    fz = (double)tfz;
     A.add(1, d[0] * fx);
     A.add(2, d[1] * fy);
     A.add(3, d[2] * fz);
@@ -413,32 +418,65 @@ __device__ __forceinline__ void chunk_body(const KArgs &a, const WArgs &w, const
     A.add(5, d[0] * fz);
     A.add(6, d[1] * fz);
   }
-  if (MODE == 0) {
-    // F_i = -sum_a f_a (translation invariance of the terms on i): a segmented
-    // shuffle reduction over the row's L contiguous lanes, then one set of
-    // atomics per row instead of L same-address ones
-    double sx = fx, sy = fy, sz = fz;
-    if (LC > 0 && (LC & (LC - 1)) == 0) {
-      // rows of 2^k lanes are 2^k-aligned: butterfly, every lane gets the sum
+  // Row sums over the row's L contiguous lanes by shuffles: F_i = -sum_a f_a
+  // (translation invariance of the terms on i: one set of atomics per row
+  // instead of L same-address ones) and, in the mixed kernel, e_i = sum_a V_ia
+  // (fp64 sums; the mixed kernel sums its fp32 force pieces in fp32 first --
+  // fewer shuffles -- while fp64 keeps e_i as a row-order shared-memory sum)
+  constexpr bool MIXED = sizeof(T) == 4;
+  double ev = MIXED ? vd : 0.0;
+  T sx = tfx, sy = tfy, sz = tfz;
+  double dsx = fx, dsy = fy, dsz = fz;
+  if (LC > 0 && (LC & (LC - 1)) == 0) {
+    // rows of 2^k lanes are 2^k-aligned: butterfly, every lane gets the sums
 #pragma unroll
-      for (int off = 1; off < LC; off <<= 1) {
-        sx += __shfl_xor_sync(0xffffffffu, sx, off);
-        sy += __shfl_xor_sync(0xffffffffu, sy, off);
-        sz += __shfl_xor_sync(0xffffffffu, sz, off);
+    for (int off = 1; off < LC; off <<= 1) {
+      if (MODE == 0) {
+        if (MIXED) {
+          sx += __shfl_xor_sync(0xffffffffu, sx, off);
+          sy += __shfl_xor_sync(0xffffffffu, sy, off);
+          sz += __shfl_xor_sync(0xffffffffu, sz, off);
+        } else {
+          dsx += __shfl_xor_sync(0xffffffffu, dsx, off);
+          dsy += __shfl_xor_sync(0xffffffffu, dsy, off);
+          dsz += __shfl_xor_sync(0xffffffffu, dsz, off);
+        }
       }
-    } else
+      if (MIXED) ev += __shfl_xor_sync(0xffffffffu, ev, off);
+    }
+  } else {
 #pragma unroll
     for (int off = 1; off < (LC > 0 ? LC : 32); off <<= 1) {
       if (LC == 0 && off >= L) break;
-      const double ox = __shfl_down_sync(0xffffffffu, sx, off);
-      const double oy = __shfl_down_sync(0xffffffffu, sy, off);
-      const double oz = __shfl_down_sync(0xffffffffu, sz, off);
-      if (pos + off < L) {
-        sx += ox;
-        sy += oy;
-        sz += oz;
+      const bool in = pos + off < L;
+      if (MODE == 0) {
+        if (MIXED) {
+          const T ox = __shfl_down_sync(0xffffffffu, sx, off);
+          const T oy = __shfl_down_sync(0xffffffffu, sy, off);
+          const T oz = __shfl_down_sync(0xffffffffu, sz, off);
+          if (in) {
+            sx += ox;
+            sy += oy;
+            sz += oz;
+          }
+        } else {
+          const double ox = __shfl_down_sync(0xffffffffu, dsx, off);
+          const double oy = __shfl_down_sync(0xffffffffu, dsy, off);
+          const double oz = __shfl_down_sync(0xffffffffu, dsz, off);
+          if (in) {
+            dsx += ox;
+            dsy += oy;
+            dsz += oz;
+          }
+        }
+      }
+      if (MIXED) {
+        const double ov = __shfl_down_sync(0xffffffffu, ev, off);
+        if (in) ev += ov;
       }
     }
+  }
+  if (MODE == 0) {
     if (live) {
       double *fj = w.facc + 3 * (int64_t)j;  // facc: accumulator
       atomicAdd(fj, fx);
@@ -447,9 +485,9 @@ __device__ __forceinline__ void chunk_body(const KArgs &a, const WArgs &w, const
     }
     if (valid && pos == 0 && (lmask & rowmask)) {
       double *fi = w.facc + 3 * (int64_t)i;
-      atomicAdd(fi, -sx);
-      atomicAdd(fi + 1, -sy);
-      atomicAdd(fi + 2, -sz);
+      atomicAdd(fi, MIXED ? -(double)sx : -dsx);
+      atomicAdd(fi + 1, MIXED ? -(double)sy : -dsy);
+      atomicAdd(fi + 2, MIXED ? -(double)sz : -dsz);
     }
   } else if (valid) {  // dead entries store zeros
     double *fb = a.fbuf + 3 * (int64_t)e;
@@ -457,12 +495,15 @@ __device__ __forceinline__ void chunk_body(const KArgs &a, const WArgs &w, const
     fb[1] = fy;
     fb[2] = fz;
   }
-  // ---- e_i: the first lane of each row sums the row's V (row order) ----
+  // ---- e_i (the row's first lane) ----
   if (valid && pos == 0) {
-    double se = 0.0;
+    double se = ev;
+    if (!MIXED) {  // row order, from the shared table
+      se = 0.0;
 #pragma unroll
-    for (int q = 0; q < (LC > 0 ? LC : 1); ++q) se += tb.v[lane + q];
-    for (int q = LC > 0 ? LC : 1; q < L; ++q) se += tb.v[lane + q];
+      for (int q = 0; q < (LC > 0 ? LC : 1); ++q) se += tb.v[lane + q];
+      for (int q = LC > 0 ? LC : 1; q < L; ++q) se += tb.v[lane + q];
+    }
     A.add(0, se);
     if (a.per_atom) a.per_atom[i] = se + 0.0;
   }
