@@ -153,17 +153,21 @@ __device__ __forceinline__ void cp_async_wait() {
 }
 
 // issue the gathers of one chunk's operands into a stage
-template <int S>
+template <int S, bool HEAD>
 __device__ __forceinline__ void stage_chunk(WStage &st, const int4 rec, const int lane,
                                             const double *__restrict__ pos,
                                             const int *__restrict__ species) {
   if (rec.x >= 0) {
+    // HEAD (mixed kernel): x_i and s_i once per row (its first lane), read by
+    // the row's lanes from that slot -- less staging traffic on the L1/shared
+    // pipe that bounds the mixed kernel (fp64 measured faster per lane)
+    const bool head = !HEAD || lane % rec.w == 0;
 #pragma unroll
     for (int q = 0; q < 3; ++q) {
-      cp_async8(&st.xi[q][lane], pos + 3 * (int64_t)rec.y + q);
+      if (head) cp_async8(&st.xi[q][lane], pos + 3 * (int64_t)rec.y + q);
       cp_async8(&st.xj[q][lane], pos + 3 * (int64_t)rec.z + q);
     }
-    cp_async4(&st.si[lane], species + rec.y);
+    if (head) cp_async4(&st.si[lane], species + rec.y);
     if (S > 1) cp_async4(&st.sj[lane], species + rec.z);
   }
 }
@@ -187,10 +191,11 @@ __device__ __forceinline__ void chunk_body(const KArgs &a, const WArgs &w, const
   double d[3] = {0, 0, 0}, r2 = 1.0;
   int si = 0, sj = 0;
   if (valid) {
-    const double cxi[3] = {stg.xi[0][lane], stg.xi[1][lane], stg.xi[2][lane]};
+    const int src_i = sizeof(T) == 4 ? first : lane;  // see stage_chunk<S, HEAD>
+    const double cxi[3] = {stg.xi[0][src_i], stg.xi[1][src_i], stg.xi[2][src_i]};
     const double cxj[3] = {stg.xj[0][lane], stg.xj[1][lane], stg.xj[2][lane]};
     r2 = disp_r2(cxi, cxj, a.box, d);
-    si = stg.si[lane];
+    si = stg.si[src_i];
     sj = S > 1 ? stg.sj[lane] : 0;
     if (pos == 0) {
       if (!(isfinite(cxi[0]) && isfinite(cxi[1]) && isfinite(cxi[2])))
@@ -659,7 +664,7 @@ __global__ void __launch_bounds__(WNT, sizeof(T) == 4 ? TB_WARP_MINB_F : TB_WARP
   const int4 idle = make_int4(-1, 0, 0, 1);
   int4 cur = c < nchunks ? __ldg(w.lanes + 32 * (int64_t)c + lane) : idle;
   int4 nxt = c + stride < nchunks ? __ldg(w.lanes + 32 * (int64_t)(c + stride) + lane) : idle;
-  stage_chunk<S>(s_stage[wid][0], cur, lane, a.pos, a.species);
+  stage_chunk<S, sizeof(T) == 4>(s_stage[wid][0], cur, lane, a.pos, a.species);
   cp_async_commit();
   int buf = 0;
 #ifdef TB_TRACE
@@ -678,9 +683,10 @@ __global__ void __launch_bounds__(WNT, sizeof(T) == 4 ? TB_WARP_MINB_F : TB_WARP
     const int4 nx2 = c + 2 * stride < nchunks
                          ? __ldg(w.lanes + 32 * (int64_t)(c + 2 * stride) + lane)
                          : idle;
-    stage_chunk<S>(s_stage[wid][buf ^ 1], nxt, lane, a.pos, a.species);
+    stage_chunk<S, sizeof(T) == 4>(s_stage[wid][buf ^ 1], nxt, lane, a.pos, a.species);
     cp_async_commit();
     cp_async_wait<1>();  // this lane's gathers for the current chunk have landed
+    if (sizeof(T) == 4) __syncwarp();  // ... and the row heads' x_i / s_i are visible
     const WStage &stg = s_stage[wid][buf];
     const int Ldyn = __shfl_sync(0xffffffffu, cur.w, 0);
     // short rows (diamond: 4): fixed rotation, unrolled; longer rows: live masks
