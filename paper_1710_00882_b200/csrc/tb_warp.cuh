@@ -314,7 +314,11 @@ __device__ __forceinline__ void chunk_body(const KArgs &a, const WArgs &w, const
       }
     }
     const T f = (S > 1 && sj == 1) ? bfc.y : bfc.x;  // f_C(r_b) with entry (i, a, b)
-    if (pair_live && f != T(0)) {
+    if (S == 1 && !LAM3 && !ST) {
+      // a dead partner (f = 0) adds exactly 0 and a dead pair's zeta is never
+      // used: no branch
+      zeta += f * g;
+    } else if (pair_live && f != T(0)) {
       if (ST) {
         A.c_lt++;
         A.c_tt += f != T(1);
@@ -370,7 +374,9 @@ __device__ __forceinline__ void chunk_body(const KArgs &a, const WArgs &w, const
     const bool t1 = (dz != T(0)) && (f_b != T(0));
     // f_C may round to 0 in the taper while dF_C/dr does not: test both
     const bool t2 = (dzb != T(0)) && (f_a != T(0) || df_a != T(0));
-    if (!(t1 || t2)) continue;
+    // one species, no lam3: the (t1, t2) terms below are products with the
+    // zero factors themselves, so no branch is needed
+    if (!(S == 1 && !LAM3) && !(t1 || t2)) continue;
     const typename Vec4<T>::t be = tb.e(src);
     const T rb = be.w;
     T cost, g, dg;
