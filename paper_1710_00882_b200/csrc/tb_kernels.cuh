@@ -67,13 +67,37 @@ __device__ __forceinline__ double min_image(double d, double L, double invL) {
   return __dsub_rn(d, __dmul_rn(L, q));
 }
 
-// displacement x_j - x_i with min image and r2 = (dx*dx + dy*dy) + dz*dz
+// displacement x_j - x_i with min image and r2 = (dx*dx + dy*dy) + dz*dz.
+// Same arithmetic as min_image per axis; the all-periodic box (one uniform
+// branch) tests the three near-half-integer cases together so that the common
+// path has a single rarely-taken branch.
 __device__ __forceinline__ double disp_r2(const double *xi, const double *xj, const Box &b,
                                           double d[3]) {
+  if (b.per[0] & b.per[1] & b.per[2]) {
+    double v[3], q[3];
+    bool near = false;
 #pragma unroll
-  for (int ax = 0; ax < 3; ++ax) {
-    double v = __dsub_rn(xj[ax], xi[ax]);
-    d[ax] = b.per[ax] ? min_image(v, b.L[ax], b.invL[ax]) : v;
+    for (int ax = 0; ax < 3; ++ax) {
+      v[ax] = __dsub_rn(xj[ax], xi[ax]);
+      const double y = __dmul_rn(v[ax], b.invL[ax]);
+      q[ax] = rint(y);
+      near |= 0.5 - fabs(y - q[ax]) < 1e-9;
+    }
+    if (__builtin_expect(near, 0)) {
+#pragma unroll
+      for (int ax = 0; ax < 3; ++ax) {
+        const double y = __dmul_rn(v[ax], b.invL[ax]);
+        if (0.5 - fabs(y - q[ax]) < 1e-9) q[ax] = rint_quotient_exact(v[ax], b.L[ax]);
+      }
+    }
+#pragma unroll
+    for (int ax = 0; ax < 3; ++ax) d[ax] = __dsub_rn(v[ax], __dmul_rn(b.L[ax], q[ax]));
+  } else {
+#pragma unroll
+    for (int ax = 0; ax < 3; ++ax) {
+      double v = __dsub_rn(xj[ax], xi[ax]);
+      d[ax] = b.per[ax] ? min_image(v, b.L[ax], b.invL[ax]) : v;
+    }
   }
   return __dadd_rn(__dadd_rn(__dmul_rn(d[0], d[0]), __dmul_rn(d[1], d[1])),
                    __dmul_rn(d[2], d[2]));
