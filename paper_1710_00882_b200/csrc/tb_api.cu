@@ -260,6 +260,7 @@ static Tables<T, S> make_tables(const tb_context *ctx) {
               x.h == y.h && x.lam3 == y.lam3 && x.lam3x3 == y.lam3x3 && x.m == y.m))
           tab.gsym = 0;
       }
+  tab.fc_same = S == 1 && ctx->pair_mat[0] == ctx->trip_mat[0] && ctx->pair_mat[1] == ctx->trip_mat[1];
   for (int q = 0; q < S * S; ++q) {
     const double *r = &ctx->pair_mat[8 * q];
     PairP<T> &p = tab.pair[q];

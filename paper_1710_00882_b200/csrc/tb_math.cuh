@@ -48,7 +48,9 @@ struct Tables {
   // (gamma, c, d, h, lam3, m depend on i only, as in the Tersoff-1989 tables):
   // the (i,b,a) term then reuses the (i,a,b) angular values
   int gsym;
-  int pad_;
+  // 1 when the pair cutoff (R, D of entry (i,j,j)) equals the k-role cutoff of
+  // entry (i,j,j) -- one species: the pair term reuses the lane's f_C
+  int fc_same;
 };
 
 // ---- transcendental wrappers (overloads keep the templates readable) ----
@@ -115,16 +117,10 @@ __device__ __forceinline__ void lam3_term(T dr, const TripP<T> &p, T &ex, T &dar
 
 // Pair part of one ordered (i,j) bond at fixed zeta (potential.py:280-290):
 // returns V, dV/dr and delta_zeta = f_C f_A db/dzeta.
+// pair_part_fc: the same with f_C(r), dF_C/dr already known (r < R + D)
 template <class T>
-__device__ __forceinline__ void pair_part(T r, T zeta, const PairP<T> &p, T &v, T &dvdr,
-                                          T &dzeta) {
-  T fc, dfc;
-  if (!cutoff(r, p, fc, dfc)) {
-    v = T(0);
-    dvdr = T(0);
-    dzeta = T(0);
-    return;
-  }
+__device__ __forceinline__ void pair_part_fc(T r, T zeta, const PairP<T> &p, T fc, T dfc, T &v,
+                                             T &dvdr, T &dzeta) {
   T fr = p.A * t_exp(-p.lam1 * r);
   T fa = -p.B * t_exp(-p.lam2 * r);
   T t = p.beta * zeta;
@@ -152,6 +148,19 @@ __device__ __forceinline__ void pair_part(T r, T zeta, const PairP<T> &p, T &v, 
   v = fc * inner;
   dvdr = dfc * inner + fc * (-p.lam1 * fr + b * (-p.lam2 * fa));
   dzeta = fc * fa * db;
+}
+
+template <class T>
+__device__ __forceinline__ void pair_part(T r, T zeta, const PairP<T> &p, T &v, T &dvdr,
+                                          T &dzeta) {
+  T fc, dfc;
+  if (!cutoff(r, p, fc, dfc)) {
+    v = T(0);
+    dvdr = T(0);
+    dzeta = T(0);
+    return;
+  }
+  pair_part_fc(r, zeta, p, fc, dfc, v, dvdr, dzeta);
 }
 
 }  // namespace tb

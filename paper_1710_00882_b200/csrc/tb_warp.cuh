@@ -341,7 +341,10 @@ __device__ __forceinline__ void chunk_body(const KArgs &a, const WArgs &w, const
 #ifdef TB_DBG_NOPAIR
     v = zeta * T(1e-6); dvdr = ra * T(1e-3); dz = zeta * T(1e-9);
 #else
-    pair_part(ra, zeta, pp, v, dvdr, dz);
+    if (S == 1 && tab.fc_same)  // same R, D: f_C(r) of this entry is fck[0]
+      pair_part_fc(ra, zeta, pp, fck[0], dfck[0], v, dvdr, dz);
+    else
+      pair_part(ra, zeta, pp, v, dvdr, dz);
 #endif
   }
   if (S == 1 && WTable<T>::DZ_IN_FC)
