@@ -43,13 +43,38 @@ TBFM_QUAL uint64_t tbfm_bits(double d) {
 #endif
 }
 
+// Polynomial / reduction constants.  On the device they live in constant
+// memory so that DFMA reads them as c[][] operands (a 64-bit literal would
+// have to be moved into registers with two UMOVs at every use).
+#define TBFM_KLIST                                                                          \
+  1.4426950408889634, 6.93147180369123816490e-01, 1.90821492927058770002e-10,                \
+      6755399441055744.0, 1.0 / 6.0, 1.0 / 120.0, 1.0 / 24.0, 1.0 / 5040.0, 1.0 / 720.0,     \
+      1.0 / 362880.0, 1.0 / 40320.0, 1.0 / 39916800.0, 1.0 / 3628800.0, 1.0 / 479001600.0,  \
+      6.666666666666735130e-01, 3.999999999940941908e-01, 2.857142874366239149e-01,          \
+      2.222219843214978396e-01, 1.818357216161805012e-01, 1.531383769920937332e-01,          \
+      1.479819860511658591e-01
+enum {
+  TBK_L2E, TBK_LN2HI, TBK_LN2LO, TBK_SH, TBK_C3, TBK_C5, TBK_C4, TBK_C7, TBK_C6, TBK_C9,
+  TBK_C8, TBK_C11, TBK_C10, TBK_C12, TBK_LG1, TBK_LG2, TBK_LG3, TBK_LG4, TBK_LG5, TBK_LG6,
+  TBK_LG7
+};
+#if defined(__CUDACC__)
+__constant__ double tbfm_kc[] = {TBFM_KLIST};
+#endif
+static const double tbfm_kh[] = {TBFM_KLIST};
+#if defined(__CUDA_ARCH__)
+#define TBK(i) tbfm_kc[i]
+#else
+#define TBK(i) tbfm_kh[i]
+#endif
+
 // exp(x): x = k ln2 + r, |r| <= ln2/2; exp(r) by its degree-12 Taylor
 // polynomial (truncation < 2e-17 relative) in Estrin form; 2^k by exponent bits.
 TBFM_QUAL double tb_exp(double x) {
-  const double L2E = 1.4426950408889634;
-  const double LN2HI = 6.93147180369123816490e-01;
-  const double LN2LO = 1.90821492927058770002e-10;
-  const double SH = 6755399441055744.0;  // 1.5 * 2^52: round-to-nearest integer trick
+  const double L2E = TBK(TBK_L2E);
+  const double LN2HI = TBK(TBK_LN2HI);
+  const double LN2LO = TBK(TBK_LN2LO);
+  const double SH = TBK(TBK_SH);  // 1.5 * 2^52: round-to-nearest integer trick
   double kd = fma(x, L2E, SH);
   const int k = (int)(int64_t)(tbfm_bits(kd) & 0xffffffffull);  // low word = rint(x log2e)
   kd -= SH;
@@ -58,12 +83,12 @@ TBFM_QUAL double tb_exp(double x) {
   const double r2 = r * r, r4 = r2 * r2, r8 = r4 * r4;
   // c_n = 1/n!
   const double p01 = fma(r, 1.0, 1.0);
-  const double p23 = fma(r, 1.0 / 6.0, 0.5);
-  const double p45 = fma(r, 1.0 / 120.0, 1.0 / 24.0);
-  const double p67 = fma(r, 1.0 / 5040.0, 1.0 / 720.0);
-  const double p89 = fma(r, 1.0 / 362880.0, 1.0 / 40320.0);
-  const double pab = fma(r, 1.0 / 39916800.0, 1.0 / 3628800.0);
-  const double pc = 1.0 / 479001600.0;
+  const double p23 = fma(r, TBK(TBK_C3), 0.5);
+  const double p45 = fma(r, TBK(TBK_C5), TBK(TBK_C4));
+  const double p67 = fma(r, TBK(TBK_C7), TBK(TBK_C6));
+  const double p89 = fma(r, TBK(TBK_C9), TBK(TBK_C8));
+  const double pab = fma(r, TBK(TBK_C11), TBK(TBK_C10));
+  const double pc = TBK(TBK_C12);
   const double q03 = fma(r2, p23, p01);
   const double q47 = fma(r2, p67, p45);
   const double q8b = fma(r2, pab, p89);
@@ -92,10 +117,8 @@ TBFM_QUAL double tb_log(double x) {
   const double f = m - 1.0;
   const double s = f * tb_rcp(2.0 + f);
   const double z = s * s, w = z * z;
-  const double Lg1 = 6.666666666666735130e-01, Lg2 = 3.999999999940941908e-01,
-               Lg3 = 2.857142874366239149e-01, Lg4 = 2.222219843214978396e-01,
-               Lg5 = 1.818357216161805012e-01, Lg6 = 1.531383769920937332e-01,
-               Lg7 = 1.479819860511658591e-01;
+  const double Lg1 = TBK(TBK_LG1), Lg2 = TBK(TBK_LG2), Lg3 = TBK(TBK_LG3), Lg4 = TBK(TBK_LG4),
+               Lg5 = TBK(TBK_LG5), Lg6 = TBK(TBK_LG6), Lg7 = TBK(TBK_LG7);
   // R = z (Lg1 + z Lg2 + ... + z^6 Lg7), Estrin in z
   const double a = fma(z, Lg2, Lg1);
   const double b = fma(z, Lg4, Lg3);
@@ -105,8 +128,8 @@ TBFM_QUAL double tb_log(double x) {
   const double R = z * fma(w * w, cd, ab);
   const double hfsq = 0.5 * f * f;
   const double ed = (double)e;
-  const double LN2HI = 6.93147180369123816490e-01;
-  const double LN2LO = 1.90821492927058770002e-10;
+  const double LN2HI = TBK(TBK_LN2HI);
+  const double LN2LO = TBK(TBK_LN2LO);
   return fma(ed, LN2HI, f - (hfsq - (s * (hfsq + R) + ed * LN2LO)));
 }
 
