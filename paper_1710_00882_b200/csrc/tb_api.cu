@@ -917,12 +917,12 @@ static int launch_warp_t(tb_context *ctx, const tb_nlist *nl, KArgs &a, WArgs &w
     // by registers and the per-warp staging, not by a small default carveout
     CK(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
                             cudaSharedmemCarveoutMaxShared));
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, WNT, 0));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, WarpCfg<T>::nt, 0));
     per_sm = std::max(per_sm, 1);
   }
   int sms = 0;
   CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device));
-  int need = nblk(w.nchunks, WPB);
+  int need = nblk(w.nchunks, WarpCfg<T>::wpb);
   // persistent grid: one resident wave, warps stride over the chunks
   int nb = std::max(1, ctx->warp_per_chunk ? need : std::min(need, sms * per_sm));
   CK(ctx->partials.ensure(sizeof(double) * 8 * nb));
@@ -939,7 +939,7 @@ static int launch_warp_t(tb_context *ctx, const tb_nlist *nl, KArgs &a, WArgs &w
     }
     CK(cudaEventRecord(ev.first, ctx->stream));
   }
-  kern<<<nb, WNT, 0, ctx->stream>>>(a, w, tab);
+  kern<<<nb, WarpCfg<T>::nt, 0, ctx->stream>>>(a, w, tab);
   ctx->last_blocks = nb;
   CK(cudaGetLastError());
   if (ctx->profile) {

@@ -43,6 +43,19 @@ namespace tb {
 #endif
 constexpr int WNT = 128;  // threads per block of the warp kernel
 constexpr int WPB = WNT / 32;
+#ifndef TB_WNT64
+#define TB_WNT64 128  // fp64 block size (see DESIGN: 96 x 6 blocks measured)
+#endif
+#ifndef TB_WARP_MINB64
+#define TB_WARP_MINB64 4
+#endif
+// block shape of the warp kernel per precision
+template <class T>
+struct WarpCfg {
+  static constexpr int nt = sizeof(T) == 8 ? TB_WNT64 : WNT;
+  static constexpr int wpb = nt / 32;
+  static constexpr int minb = sizeof(T) == 8 ? TB_WARP_MINB64 : TB_WARP_MINB_F;
+};
 constexpr int QCAP = 4;   // k-iterations whose angular values are cached
 
 template <class V>
@@ -634,14 +647,15 @@ __device__ __forceinline__ unsigned long long gtimer() {
 #endif
 
 template <class T, int S, bool LAM3, int MODE, bool ST>
-__global__ void __launch_bounds__(WNT, sizeof(T) == 4 ? TB_WARP_MINB_F : TB_WARP_MINB)
+__global__ void __launch_bounds__(WarpCfg<T>::nt, WarpCfg<T>::minb)
     k_tersoff_warp(const KArgs a, const WArgs w, const __grid_constant__ Tables<T, S> gtab) {
+  constexpr int NT = WarpCfg<T>::nt, NW = WarpCfg<T>::wpb;
   __shared__ Tables<T, S> s_tab;
-  __shared__ double s_red[WPB][8];
-  __shared__ T s_cache[WPB][QCAP][3][32];  // cos, g, dg of (i,a,b) from phase 1
-  __shared__ WStage s_stage[WPB][2];         // gathered operands, double-buffered
-  __shared__ double s_acc[WPB][7][32];       // per-lane energy + virial
-  __shared__ WTable<T> s_tb[WPB];            // lanes' neighbour data (per warp)
+  __shared__ double s_red[NW][8];
+  __shared__ T s_cache[NW][QCAP][3][32];  // cos, g, dg of (i,a,b) from phase 1
+  __shared__ WStage s_stage[NW][2];         // gathered operands, double-buffered
+  __shared__ double s_acc[NW][7][32];       // per-lane energy + virial
+  __shared__ WTable<T> s_tb[NW];            // lanes' neighbour data (per warp)
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
 #ifdef TB_TRACE
   if (threadIdx.x == 0) g_trace[16 * 4096 - 2 * 1024 + 2 * (blockIdx.x & 1023)] = gtimer();
@@ -649,7 +663,7 @@ __global__ void __launch_bounds__(WNT, sizeof(T) == 4 ? TB_WARP_MINB_F : TB_WARP
   if (S > 1) {
     const int *src = reinterpret_cast<const int *>(&gtab);
     int *dst = reinterpret_cast<int *>(&s_tab);
-    for (int q = threadIdx.x; q < (int)(sizeof(Tables<T, S>) / sizeof(int)); q += WNT)
+    for (int q = threadIdx.x; q < (int)(sizeof(Tables<T, S>) / sizeof(int)); q += NT)
       dst[q] = src[q];
     __syncthreads();
   }
@@ -659,7 +673,7 @@ __global__ void __launch_bounds__(WNT, sizeof(T) == 4 ? TB_WARP_MINB_F : TB_WARP
     nchunks = __ldg(w.dinfo);
     n_empty = __ldg(w.dinfo + 1);
   }
-  for (int k = blockIdx.x * WNT + threadIdx.x; k < n_empty; k += gridDim.x * WNT) {
+  for (int k = blockIdx.x * NT + threadIdx.x; k < n_empty; k += gridDim.x * NT) {
     const int m = w.empty_atoms[k];
     if (a.per_atom) a.per_atom[m] = 0.0;
     const int sm = a.species[m];
@@ -679,7 +693,7 @@ __global__ void __launch_bounds__(WNT, sizeof(T) == 4 ? TB_WARP_MINB_F : TB_WARP
   // chunk order: a partial last round spreads over all SMs.  (Claiming chunks
   // from a global atomic counter was measured slower: no better balance at
   // the pipeline's look-ahead, and c5 fp64 atomic mode went 2.96 -> 5.76 ms.)
-  const int stride = gridDim.x * WPB;
+  const int stride = gridDim.x * NW;
   int c = wid * gridDim.x + blockIdx.x;
   const int4 idle = make_int4(-1, 0, 0, 1);
   int4 cur = c < nchunks ? __ldg(w.lanes + 32 * (int64_t)c + lane) : idle;
@@ -688,7 +702,7 @@ __global__ void __launch_bounds__(WNT, sizeof(T) == 4 ? TB_WARP_MINB_F : TB_WARP
   cp_async_commit();
   int buf = 0;
 #ifdef TB_TRACE
-  const int gw = blockIdx.x * WPB + wid;
+  const int gw = blockIdx.x * NW + wid;
   unsigned long long *tr = g_trace + 16 * (gw & 4095);
   int ndone = 0;
   if (lane == 0) {
@@ -753,7 +767,7 @@ __global__ void __launch_bounds__(WNT, sizeof(T) == 4 ? TB_WARP_MINB_F : TB_WARP
   if (threadIdx.x < 7) {
     double v = 0.0;
 #pragma unroll
-    for (int q = 0; q < WPB; ++q) v += s_red[q][threadIdx.x];
+    for (int q = 0; q < NW; ++q) v += s_red[q][threadIdx.x];
     a.partials[8 * (int64_t)blockIdx.x + threadIdx.x] = v;
 #ifdef TB_TRACE
     if (threadIdx.x == 0) g_trace[16 * 4096 - 2 * 1024 + 2 * (blockIdx.x & 1023) + 1] = gtimer();
