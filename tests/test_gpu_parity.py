@@ -241,3 +241,39 @@ def test_needs_rebuild_threshold():
     nlp = B.build_neighbor_list(p, 2.1, 0.3)
     p.positions[0, 0] = 9.95
     assert B.needs_rebuild(p, nlp)
+
+
+@pytest.mark.parametrize("precision", ["double", "single"])
+def test_pinned_host_buffers_match_pageable(precision):
+    """compute() with pinned host arrays (finalize writes forces / results
+    through their device aliases, per-atom energies on the side stream) gives
+    the same result as pageable arrays, repeatedly, including after an error."""
+    import torch
+    g = load_golden("si512")
+    t = parse_params(str(g["table"]))
+    fr = golden_frame(g)
+    nl = B.build_neighbor_list(fr, t.r_cut, 0.3)
+    var = B.make_variant("B200", precision=precision)
+    ref = B.compute(fr, nl, t, var)
+    n = len(fr.positions)
+    pos = torch.empty((n, 3), dtype=torch.float64).pin_memory().numpy()
+    pos[:] = fr.positions
+    sp = torch.empty(n, dtype=torch.int32).pin_memory().numpy()
+    sp[:] = np.asarray(fr.species)
+    pf = Frame(pos, fr.box.lengths, fr.box.periodic)
+    pf.species = sp
+    out = B.ForceEnergyResult(torch.empty((n, 3), dtype=torch.float64).pin_memory().numpy(), 0.0,
+                              torch.empty(n, dtype=torch.float64).pin_memory().numpy(), {})
+    for _ in range(3):
+        r = B.compute(pf, nl, t, var, out=out)
+        assert np.array_equal(r.forces, ref.forces) or rel_f(r.forces, ref.forces) < 1e-12
+        assert abs(r.potential_energy - ref.potential_energy) <= 1e-12 * abs(ref.potential_energy)
+        assert np.allclose(r.per_atom_energy, ref.per_atom_energy, rtol=0, atol=1e-12)
+        assert np.allclose(r.virial, ref.virial, rtol=1e-12, atol=1e-12)
+        assert r.stats["zeta_visits"] == ref.stats["zeta_visits"]
+    pos[3, 1] = np.nan  # an error reported through the pinned result block
+    with pytest.raises(B.InputError, match="non-finite"):
+        B.compute(pf, nl, t, var, out=out)
+    pos[3, 1] = fr.positions[3, 1]
+    r = B.compute(pf, nl, t, var, out=out)  # flags were reset: clean again
+    assert abs(r.potential_energy - ref.potential_energy) <= 1e-12 * abs(ref.potential_energy)
