@@ -104,7 +104,7 @@ struct tb_nlist {
   bool built = false;
   DevBuf offsets, nbr, rev, ref_pos, atom_cell, cell_count, cell_start, cell_atoms, row_count,
       maxrow, nl_row, sorted_atoms, sort_keys, iota, lanes, hist, cpos, crow, coff, centry,
-      scratch;  // TMPW-wide per-atom rows of the single-pass scan
+      fnbr, scratch;  // TMPW-wide per-atom rows of the single-pass scan
   bool filtered = false;                 // chunks built from the species-pair filter
   DevBuf fbuf;                           // gather mode: per-entry force pieces
   bool fbuf_zero = false;                // entries without lanes hold zeros
@@ -123,7 +123,8 @@ struct tb_nlist {
   // live repack (TB_OPT_LIVE_PACK): rows cut to their entries with r < r_cut at
   // the evaluation's positions (pack_adjacency, neighbor.py:330-360), re-chunked
   // on the device every evaluation
-  DevBuf lplan, llen, lrow, lsorted, llanes;
+  DevBuf lplan, llen, lrow, lrowj, lsorted, llanes;
+  bool fnbr_ok = false;  // fnbr matches centry (written by every filter pass since)
   int64_t lcap = 0;  // chunk capacity of llanes
   struct MdGraph *md = nullptr;
 };
@@ -465,8 +466,8 @@ extern "C" void tb_nlist_destroy(tb_nlist *nl) {
                     &nl->cell_count, &nl->cell_start, &nl->cell_atoms, &nl->row_count,
                     &nl->maxrow, &nl->nl_row, &nl->sorted_atoms, &nl->sort_keys,
                     &nl->iota, &nl->lanes, &nl->hist, &nl->cpos, &nl->crow, &nl->coff,
-                    &nl->centry, &nl->fbuf, &nl->plan, &nl->scratch, &nl->lplan, &nl->llen,
-                    &nl->lrow, &nl->lsorted, &nl->llanes};
+                    &nl->centry, &nl->fnbr, &nl->fbuf, &nl->plan, &nl->scratch, &nl->lplan,
+                    &nl->llen, &nl->lrow, &nl->lrowj, &nl->lsorted, &nl->llanes};
   for (DevBuf *b : bufs) b->release();
   md_graph_release(nl);
   delete nl;
@@ -573,9 +574,11 @@ static int build_filter(tb_context *ctx, tb_nlist *nl, const int *d_species) {
   CK(cudaGetLastError());
   int rc = exclusive_scan(ctx, nl->crow.as<int>(), nl->coff.as<int>(), N + 1);
   if (rc) return rc;
+  CK(nl->fnbr.ensure(sizeof(int) * std::max<int64_t>(nl->ecap, 1)));
   k_filter_rows<true><<<nblk(N, 128), 128, 0, ctx->stream>>>(
       N, nl->ref_pos.as<double>(), d_species, S, nt, b, nl->offsets.as<int>(), nl->nbr.as<int>(),
-      nullptr, nl->coff.as<int>(), nl->centry.as<int>());
+      nullptr, nl->coff.as<int>(), nl->centry.as<int>(), nl->fnbr.as<int>());
+  nl->fnbr_ok = true;
   CK(cudaGetLastError());
   CK(cudaMemsetAsync(nl->hist.p, 0, sizeof(int) * 34, ctx->stream));
   k_len_hist<<<std::min(nblk(N, 256), 296), 256, 0, ctx->stream>>>(N, nl->crow.as<int>(),
@@ -1029,6 +1032,7 @@ static int live_repack(tb_context *ctx, tb_nlist *nl, const double *d_pos, doubl
   CK(nl->lplan.ensure(sizeof(DevPlan)));
   CK(nl->llen.ensure(sizeof(int) * std::max(N, 1)));
   CK(nl->lrow.ensure(sizeof(int) * std::max<int64_t>(ent, 1)));
+  CK(nl->lrowj.ensure(sizeof(int) * std::max<int64_t>(ent, 1)));
   CK(nl->lsorted.ensure(sizeof(int) * std::max(N, 1)));
   if (nl->lcap < cap) {
     CK(nl->llanes.ensure(sizeof(int4) * 32 * cap));
@@ -1037,23 +1041,22 @@ static int live_repack(tb_context *ctx, tb_nlist *nl, const double *d_pos, doubl
   DevPlan *plan = nl->lplan.as<DevPlan>();
   const int *start = filtered ? nl->coff.as<int>() : nl->offsets.as<int>();
   constexpr int G = 8;  // lanes per row
+  CK(cudaMemsetAsync(plan, 0, sizeof(DevPlan), ctx->stream));
   if (filtered)
     k_live_rows<true, G><<<nblk((int64_t)N * G, 256), 256, 0, ctx->stream>>>(
         N, d_pos, box, r_cut * r_cut, start, nl->crow.as<int>(), nl->centry.as<int>(),
-        nl->nbr.as<int>(), nl->llen.as<int>(), nl->lrow.as<int>(), err);
+        nl->fnbr.as<int>(), nl->llen.as<int>(), nl->lrow.as<int>(), nl->lrowj.as<int>(), err);
   else
     k_live_rows<false, G><<<nblk((int64_t)N * G, 256), 256, 0, ctx->stream>>>(
         N, d_pos, box, r_cut * r_cut, start, nullptr, nullptr, nl->nbr.as<int>(),
-        nl->llen.as<int>(), nl->lrow.as<int>(), err);
+        nl->llen.as<int>(), nl->lrow.as<int>(), nl->lrowj.as<int>(), err);
   CK(cudaGetLastError());
-  CK(cudaMemsetAsync(plan, 0, sizeof(DevPlan), ctx->stream));
   k_len_hist_plan<<<std::min(nblk(N, 256), 296), 256, 0, ctx->stream>>>(N, nl->llen.as<int>(), plan);
   k_plan<<<1, 32, 0, ctx->stream>>>(plan, nullptr, N, 0, (int)nl->lcap);
-  k_bucket_rows<<<nblk(N, 256), 256, 0, ctx->stream>>>(N, nl->llen.as<int>(), plan,
-                                                       nl->lsorted.as<int>());
-  k_fill_lanes_dev<<<(int)std::min<int64_t>(nblk(nl->lcap, 8), 148 * 8), 256, 0, ctx->stream>>>(
-      plan, nl->lsorted.as<int>(), start, nl->lrow.as<int>(), nl->nbr.as<int>(),
-      nl->llanes.as<int4>());
+  k_bucket_fill<<<nblk(N, 256), 256, 0, ctx->stream>>>(N, nl->llen.as<int>(), start,
+                                                       nl->lrow.as<int>(), nl->lrowj.as<int>(),
+                                                       plan, nl->lsorted.as<int>(),
+                                                       nl->llanes.as<int4>());
   CK(cudaGetLastError());
   return TB_OK;
 }
@@ -1153,7 +1156,7 @@ static int enqueue_compute(tb_context *ctx, const tb_nlist *nl, const double *d_
     // filtered rows (SiC: 12 mostly dead Si-Si entries per Si row; c3 step
     // 501 -> 395 us).  Long single-species rows (disordered Si, c4) gain
     // 575 -> 371 us in the kernel but pay it back in the repack pass.
-    const bool live = !ctx->dplan && scatter == TB_SCATTER_ATOMIC &&
+    const bool live = !ctx->dplan && scatter == TB_SCATTER_ATOMIC && (!filtered || nl->fnbr_ok) &&
                       (ctx->live_pack == 1 || (ctx->live_pack == 2 && filtered));
     if (ctx->dplan) {  // tb_md_run capture: chunk counts live in the device plan
       w.dinfo = ctx->dplan;
@@ -1525,7 +1528,9 @@ static int enqueue_rebuild_device(tb_context *ctx, tb_nlist *nl, const double *d
     if (rc) return rc;
     k_filter_rows<true><<<nblk(N, 128), 128, 0, st>>>(
         N, nl->ref_pos.as<double>(), d_species, ctx->S, nt, b, nl->offsets.as<int>(),
-        nl->nbr.as<int>(), nullptr, nl->coff.as<int>(), nl->centry.as<int>());
+        nl->nbr.as<int>(), nullptr, nl->coff.as<int>(), nl->centry.as<int>(),
+        nl->fnbr.p ? nl->fnbr.as<int>() : nullptr);
+    nl->fnbr_ok = nl->fnbr.p != nullptr && nl->fnbr.cap >= sizeof(int) * (size_t)nl->ecap;
     k_plan_reset<<<1, 64, 0, st>>>(plan, 0);
     k_len_hist_plan<<<hb, 256, 0, st>>>(N, nl->crow.as<int>(), plan);
     k_plan<<<1, 32, 0, st>>>(plan, nullptr, N, ecap, ccap);

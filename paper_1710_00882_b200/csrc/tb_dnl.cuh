@@ -205,8 +205,9 @@ __global__ void __launch_bounds__(256) k_live_rows(int n, const double *__restri
                                                    double rc2, const int *__restrict__ start,
                                                    const int *__restrict__ crow,
                                                    const int *__restrict__ centry,
-                                                   const int *__restrict__ nbr,
+                                                   const int *__restrict__ jlist,
                                                    int *__restrict__ llen, int *__restrict__ lrow,
+                                                   int *__restrict__ lrowj,
                                                    ErrFlags *__restrict__ err) {
   static_assert(G > 0 && G < 32 && (32 % G) == 0, "row groups tile the warp");
   const int i = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / G);
@@ -225,18 +226,64 @@ __global__ void __launch_bounds__(256) k_live_rows(int n, const double *__restri
   for (int k0 = b; __any_sync(0xffffffffu, act && k0 < end); k0 += G) {
     const int k = k0 + sub;
     bool lv = false;
-    int e = 0;
+    int e = 0, j = 0;
     if (act && k < end) {
+      // jlist: the filtered entries' j (FILT, contiguous with centry) or the list's nbr
       e = FILT ? __ldg(centry + k) : k;
+      j = __ldg(jlist + k);
       double xj[3], d[3];
-      load3(pos, __ldg(nbr + e), xj);
+      load3(pos, j, xj);
       lv = disp_r2(xi, xj, box, d) < rc2;
     }
     const unsigned gm = (__ballot_sync(0xffffffffu, lv) >> g0) & ((1u << G) - 1u);
-    if (lv) lrow[b + q + __popc(gm & ((1u << sub) - 1u))] = e;
+    if (lv) {
+      const int at = b + q + __popc(gm & ((1u << sub) - 1u));
+      lrow[at] = e;
+      lrowj[at] = j;
+    }
     q += __popc(gm);
   }
   if (act && sub == 0) llen[i] = q;
+}
+
+// rows bucketed by live length AND written straight into their warp chunks
+// (k_bucket_rows + k_fill_lanes_dev in one pass, for the live repack): the
+// row taking slot s of bucket L owns lanes [(s % rpc) L, (s % rpc + 1) L) of
+// chunk chunk_base[L] + s / rpc, and the owner of a chunk's last row slot (or
+// of the bucket's last row) marks the chunk's remaining lanes idle
+__global__ void __launch_bounds__(256) k_bucket_fill(int n, const int *__restrict__ llen,
+                                                     const int *__restrict__ start,
+                                                     const int *__restrict__ lrow,
+                                                     const int *__restrict__ lrowj,
+                                                     DevPlan *__restrict__ plan,
+                                                     int *__restrict__ empty_atoms,
+                                                     int4 *__restrict__ lanes) {
+  __shared__ int s_cnt[34], s_base[34];
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (threadIdx.x < 34) s_cnt[threadIdx.x] = 0;
+  __syncthreads();
+  int L = -1, slot = 0;
+  if (i < n) {
+    L = min(llen[i], 33);
+    slot = atomicAdd(s_cnt + L, 1);
+  }
+  __syncthreads();
+  if (threadIdx.x < 33 && s_cnt[threadIdx.x])
+    s_base[threadIdx.x] = atomicAdd(plan->cursor + threadIdx.x, s_cnt[threadIdx.x]);
+  __syncthreads();
+  if (L < 0 || L > 32 || plan->overflow) return;  // (the chunk bound makes overflow impossible)
+  const int s = s_base[L] + slot;
+  if (L == 0) {
+    empty_atoms[s] = i;  // the kernel's empty-row list (per-atom energy 0)
+    return;
+  }
+  const int rpc = 32 / L, r = s % rpc;
+  int4 *dst = lanes + 32 * (int64_t)(plan->chunk_base[L] + s / rpc);
+  const int b = start[i];
+  for (int k = 0; k < L; ++k) dst[r * L + k] = make_int4(lrow[b + k], i, lrowj[b + k], L);
+  const bool last_in_chunk = r == rpc - 1, last_in_bucket = s == plan->hist[L] - 1;
+  if (last_in_chunk || last_in_bucket)
+    for (int k = (r + 1) * L; k < 32; ++k) dst[k] = make_int4(-1, 0, 0, L);
 }
 
 // histogram of row lengths into the device plan (block-private bins)

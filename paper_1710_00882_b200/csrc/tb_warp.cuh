@@ -829,7 +829,8 @@ template <bool FILL>
 __global__ void k_filter_rows(int n, const double *__restrict__ ref, const int *__restrict__ species,
                               int S, NeedTable nt, Box box, const int *__restrict__ offsets,
                               const int *__restrict__ nbr, int *__restrict__ crow,
-                              const int *__restrict__ coff, int *__restrict__ centry) {
+                              const int *__restrict__ coff, int *__restrict__ centry,
+                              int *__restrict__ fnbr = nullptr) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   int si = species[i];
@@ -845,7 +846,10 @@ __global__ void k_filter_rows(int n, const double *__restrict__ ref, const int *
     double xj[3], d[3];
     load3(ref, j, xj);
     if (disp_r2(xi, xj, box, d) < (double)nt.need2[si * 4 + sj]) {
-      if (FILL) centry[base + cnt] = e;
+      if (FILL) {
+        centry[base + cnt] = e;
+        if (fnbr) fnbr[base + cnt] = j;  // j of the filtered entry (live repack)
+      }
       ++cnt;
     }
   }
