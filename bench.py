@@ -329,6 +329,29 @@ def gpu_arm_decomposed(args):
     tot, cnt = ctypes.c_double(), ctypes.c_int64()
     ctx.check(lib.tb_profile_read(ctx.handle, ctypes.byref(tot), ctypes.byref(cnt)))
     kern_ms = tot.value / max(cnt.value, 1)
+    # rank 0's algorithmic flops (its owned rows) for the kernel roofline
+    roof = {"bound": "fp64" if args.precision == "double" else "fp32",
+            "kernel_ms_rank0": kern_ms, "achieved": None, "peak": None,
+            "unit": "TFLOP/s", "frac": None, "traffic": None}
+    if rank == 0:
+        pcode = _native.PRECISION[args.precision]
+        st_t = torch.zeros(_native.NSTATS, dtype=torch.int64, device=dev)
+        r8 = torch.zeros(8, dtype=torch.float64, device=dev)
+        pos_l = dom._pos_l  # [owned | ghosts] of the last step (no collective on one rank)
+        f_t = torch.empty((pos_l.shape[0], 3), dtype=torch.float64, device=dev)
+        rc = lib.tb_compute_device(ctx.handle, eng.nl.handle, _native.ptr(pos_l),
+                                   _native.ptr(dom._sp_l), float(table.r_cut), pcode,
+                                   _native.SCATTER[args.scatter], _native.ptr(f_t), None,
+                                   _native.ptr(r8), _native.ptr(st_t))
+        torch.cuda.synchronize()
+        pk = measure_peak(lib, ctx, pcode)
+        if rc == 0 and pk:
+            stv = st_t.cpu().numpy()
+            flops = algorithmic_flops(stv) if pcode == 0 else algorithmic_flops32(stv)
+            ach = flops / (kern_ms * 1e-3) / 1e12
+            roof.update({"achieved": ach, "peak": pk["tflops"], "frac": ach / pk["tflops"],
+                         "flops_per_launch_rank0": flops, "peak_source": pk["source"],
+                         "kernel": "k_tersoff_warp (rank 0: its owned rows of [owned | ghosts])"})
     # e2e: owned positions from pinned host memory each step, forces back
     pos_h = torch.empty(tuple(dom.pos.shape), dtype=torch.float64).pin_memory()
     pos_h.copy_(dom.pos)
@@ -364,9 +387,7 @@ def gpu_arm_decomposed(args):
                 "path": "decomp.DecomposedForceField per rank, pinned host positions in, "
                         "forces out, energy to host"},
         "gpu_launches": 2 * k,
-        "roofline": {"bound": "fp64" if args.precision == "double" else "fp32",
-                     "kernel_ms_rank0": kern_ms, "achieved": None, "peak": None,
-                     "unit": "TFLOP/s", "frac": None, "traffic": None},
+        "roofline": roof,
         "clocks": sampler.summary(), "energy_eV": energy,
     }
     if rank == 0:
