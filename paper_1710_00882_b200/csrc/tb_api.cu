@@ -1492,12 +1492,9 @@ static int enqueue_rebuild_device(tb_context *ctx, tb_nlist *nl, const double *d
                                                nl->cell_count.as<int>(), &plan->unwrapped);
   int rc = exclusive_scan(ctx, nl->cell_count.as<int>(), nl->cell_start.as<int>(), nl->ncell + 1);
   if (rc) return rc;
-  CK(cudaMemcpyAsync(nl->cell_count.p, nl->cell_start.p, sizeof(int) * (nl->ncell + 1),
-                     cudaMemcpyDeviceToDevice, st));
-  k_cell_fill<<<nblk(N, 256), 256, 0, st>>>(N, nl->atom_cell.as<int>(), nl->cell_count.as<int>(),
-                                              nl->cell_atoms.as<int>());
-  k_cell_gather<<<nblk(N, 256), 256, 0, st>>>(N, d_pos, nl->cell_atoms.as<int>(),
-                                                nl->cpos.as<double4>());
+  k_cell_fill_gather<<<nblk(N, 256), 256, 0, st>>>(
+      N, d_pos, nl->atom_cell.as<int>(), nl->cell_start.as<int>(), nl->cell_count.as<int>(),
+      nl->cell_atoms.as<int>(), nl->cpos.as<double4>(), nl->ref_pos.as<double>());
   const double bc2 = nl->bc * nl->bc;
   k_nl_cells<<<nblk(nl->ncell, 8), 256, 0, st>>>(
       (int)nl->ncell, N, nl->cpos.as<double4>(), g, bc2, nl->cell_start.as<int>(),
@@ -1514,7 +1511,6 @@ static int enqueue_rebuild_device(tb_context *ctx, tb_nlist *nl, const double *d
       N, nl->scratch.as<int>(), nl->row_count.as<int>(), nl->offsets.as<int>(), nl->nbr.as<int>(),
       nl->nl_row.as<int>(), &plan->list_overflow);
   CK(cudaGetLastError());
-  CK(cudaMemcpyAsync(nl->ref_pos.p, d_pos, sizeof(double) * 3 * N, cudaMemcpyDeviceToDevice, st));
   const int *row_len = nl->row_count.as<int>(), *loff = nl->offsets.as<int>();
   const int *cent = nullptr;
   if (filter) {
@@ -1544,11 +1540,17 @@ static int enqueue_rebuild_device(tb_context *ctx, tb_nlist *nl, const double *d
   if (scatter == TB_SCATTER_GATHER) {
     rc = radix_sort_rows(ctx, nl, row_len);  // stable: reproducible chunk layout
     if (rc) return rc;
+  } else if (!filter) {
+    // rows bucketed by length and written straight into their chunks (one pass)
+    k_bucket_fill<<<nblk(N, 256), 256, 0, st>>>(N, row_len, loff, nullptr, nl->nbr.as<int>(),
+                                                plan, nl->sorted_atoms.as<int>(),
+                                                nl->lanes.as<int4>());
   } else {
     k_bucket_rows<<<nblk(N, 256), 256, 0, st>>>(N, row_len, plan, nl->sorted_atoms.as<int>());
   }
-  k_fill_lanes_dev<<<(int)std::min<int64_t>(nblk(ccap, 8), 148 * 8), 256, 0, st>>>(plan, nl->sorted_atoms.as<int>(), loff, cent,
-                                          nl->nbr.as<int>(), nl->lanes.as<int4>());
+  if (scatter == TB_SCATTER_GATHER || filter)
+    k_fill_lanes_dev<<<(int)std::min<int64_t>(nblk(ccap, 8), 148 * 8), 256, 0, st>>>(
+        plan, nl->sorted_atoms.as<int>(), loff, cent, nl->nbr.as<int>(), nl->lanes.as<int4>());
   if (scatter == TB_SCATTER_GATHER)
     k_nl_reverse<<<nblk(N, 256), 256, 0, st>>>(N, nl->offsets.as<int>(), nl->nbr.as<int>(),
                                                  nl->rev.as<int>());

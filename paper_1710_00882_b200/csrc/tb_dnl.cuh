@@ -280,7 +280,9 @@ __global__ void __launch_bounds__(256) k_bucket_fill(int n, const int *__restric
   const int rpc = 32 / L, r = s % rpc;
   int4 *dst = lanes + 32 * (int64_t)(plan->chunk_base[L] + s / rpc);
   const int b = start[i];
-  for (int k = 0; k < L; ++k) dst[r * L + k] = make_int4(lrow[b + k], i, lrowj[b + k], L);
+  // lrow == nullptr: the rows are the list's own (entry = b + k, j = lrowj[b + k])
+  for (int k = 0; k < L; ++k)
+    dst[r * L + k] = make_int4(lrow ? lrow[b + k] : b + k, i, lrowj[b + k], L);
   const bool last_in_chunk = r == rpc - 1, last_in_bucket = s == plan->hist[L] - 1;
   if (last_in_chunk || last_in_bucket)
     for (int k = (r + 1) * L; k < 32; ++k) dst[k] = make_int4(-1, 0, 0, L);

@@ -198,6 +198,28 @@ __global__ void k_cell_fill(int n, const int *__restrict__ atom_cell, int *__res
   cell_atoms[slot] = i;
 }
 
+// device rebuild (tb_md_run): the counting-sort scatter and the cell-ordered
+// position copy in one pass, the per-cell counts (left by k_cell_index, already
+// scanned into cell_start) counted down as the cursor; the order inside a cell is
+// arbitrary either way (rows are rank-sorted by j in k_nl_compact)
+__global__ void k_cell_fill_gather(int n, const double *__restrict__ pos,
+                                   const int *__restrict__ atom_cell,
+                                   const int *__restrict__ cell_start, int *__restrict__ count,
+                                   int *__restrict__ cell_atoms, double4 *__restrict__ cpos,
+                                   double *__restrict__ ref) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int c = atom_cell[i];
+  const int slot = cell_start[c] + atomicSub(count + c, 1) - 1;
+  const double x = __ldg(pos + 3 * (int64_t)i), y = __ldg(pos + 3 * (int64_t)i + 1),
+               z = __ldg(pos + 3 * (int64_t)i + 2);
+  cell_atoms[slot] = i;
+  cpos[slot] = make_double4(x, y, z, __longlong_as_double((long long)i));
+  ref[3 * (int64_t)i] = x;  // the list's reference positions (needs_rebuild)
+  ref[3 * (int64_t)i + 1] = y;
+  ref[3 * (int64_t)i + 2] = z;
+}
+
 // ---------------------------------------------------------------------------
 // K2: full Verlet list at bc (neighbor.py:104-217)
 // ---------------------------------------------------------------------------
