@@ -208,7 +208,8 @@ __device__ __forceinline__ void chunk_body(const KArgs &a, const WArgs &w, const
   const int e = cur.x, i = cur.y, j = cur.z;
   const int L = LC > 0 ? LC : Ldyn;  // warp-uniform row length
   const bool valid = e >= 0;
-  const int pos = lane % L;
+  constexpr bool POW2 = LC > 0 && (LC & (LC - 1)) == 0;
+  const int pos = POW2 ? (lane & (LC - 1)) : lane % L;
   const int first = lane - pos;
 
   // ---- pack: displacement with min image, r2 < r_cut^2 ----
@@ -302,7 +303,8 @@ __device__ __forceinline__ void chunk_body(const KArgs &a, const WArgs &w, const
   for (int it = 1; LC > 0 ? (live && it < LC) : m != 0; ++it, ++q) {
     int src;
     if (LC > 0) {
-      src = first + (pos + it >= L ? pos + it - L : pos + it);
+      src = POW2 ? first + ((pos + it) & (LC - 1))
+                 : first + (pos + it >= L ? pos + it - L : pos + it);
     } else {
       src = __ffs(m) - 1;
       m &= m - 1;
@@ -376,7 +378,8 @@ __device__ __forceinline__ void chunk_body(const KArgs &a, const WArgs &w, const
   for (int it = 1; LC > 0 ? (live && it < LC) : m != 0; ++it, ++q) {
     int src;
     if (LC > 0) {
-      src = first + (pos + it >= L ? pos + it - L : pos + it);
+      src = POW2 ? first + ((pos + it) & (LC - 1))
+                 : first + (pos + it >= L ? pos + it - L : pos + it);
     } else {
       src = __ffs(m) - 1;
       m &= m - 1;
