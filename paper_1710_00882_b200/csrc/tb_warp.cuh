@@ -1,21 +1,24 @@
 // tb_warp.cuh -- warp-per-chunk Tersoff kernel (K4/K5 fast path).
 //
-// Chunks (built with the neighbour list, k_fill_lanes): rows of equal length L
-// packed floor(32/L) to a warp, so lane = one (i,j) skin-list entry, the L
-// lanes of atom i are contiguous and every lane runs the same L-1 iterations
-// of the k-loops.  What a lane needs from the other neighbours of i (unit
-// vector, r, f_C, dzeta) is pulled from the owning lane with __shfl_sync;
-// the angular values of phase 1 are kept in a per-warp shared cache for
-// phase 2.  No block barriers inside the loop.
+// Chunks (built with the neighbour list, k_fill_lanes / the device plan
+// kernels): rows of equal length L packed floor(32/L) to a warp, so lane = one
+// (i,j) skin-list entry, the L lanes of atom i are contiguous and every lane
+// runs the same L-1 iterations of the k-loops.  What a lane needs from the
+// other neighbours of i (unit vector, r, f_C, dzeta, V) it reads from a
+// per-warp shared table the owning lanes write; the angular values of phase 1
+// are cached (registers in the mixed kernel, shared memory in fp64) for
+// phase 2.  Positions/species of the next chunk are gathered with cp.async
+// while the current one computes.  No block barriers inside the loop.
 //
 //   pack   : r2 < r_cut^2 at current positions, min image (neighbor.py:330-360)
 //   phase 1: zeta_ij over k, then V, dV/dr, dzeta (kernels.py:279-299,
 //            potential.py:238-290)
 //   phase 2: the force on neighbour a from every term centred on i -- (i,a,b)
 //            with a as j and (i,b,a) with a as k -- along e_a and e_b
-//   scatter: F_a += f_a, F_i -= f_a (red.global.add.f64 into the context's
-//            accumulator) or the per-entry buffer (deterministic gather);
-//            e_i by a segmented warp reduction.
+//   scatter: F_a += f_a (red.global.add.f64 into the context's accumulator),
+//            F_i = -sum_a f_a by a segmented shuffle reduction over the row,
+//            or the per-entry buffer (deterministic gather); e_i, E and the
+//            virial by row / warp / block reductions.
 #pragma once
 #include "tb_kernels.cuh"
 
