@@ -90,6 +90,7 @@ struct tb_context {
   cudaStream_t side = nullptr;
   std::vector<int> last_species;  // host species of the last tb_compute (filter validity)
   const int *dplan = nullptr;  // tb_md_run capture: device {nchunks, n_empty}
+  bool md_fuse = false;  // tb_md_run capture (atomic): finalize folded into the kick kernels
   int last_blocks = 0;  // grid of the last Tersoff launch (partials to reduce)  // tb_set_option(TB_OPT_TILE_KERNEL): general tile kernel only
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_used, ev_free;
 };
@@ -1188,6 +1189,10 @@ static int enqueue_compute(tb_context *ctx, const tb_nlist *nl, const double *d_
                                      : launch_prec<float>(ctx, nl, a, C, scatter);
   }
   if (rc) return rc;
+  if (ctx->md_fuse && scatter == TB_SCATTER_ATOMIC) {
+    ctx->last_blocks = nparts;  // k_md_kick_ke<true> + k_md_tail do the finalize's work
+    return TB_OK;
+  }
   // finalize grid: block 0 reduces E/W; the rest move the forces (atomic: 16-byte
   // vectors, ~4 per thread; gather: one atom row per thread)
   int fb = 1 + std::min(scatter == TB_SCATTER_GATHER ? nblk(n, 256) : nblk(3 * (int64_t)n, 256 * 2 * 4),
@@ -1679,13 +1684,23 @@ static int md_capture(tb_context *ctx, tb_nlist *nl, const MdArgs &m, MdGraph *G
       rc = fail(ctx, TB_ERR_CUDA, "md capture: rebuild body: %s", cudaGetErrorString(e));
     if (rc) break;
     ctx->dplan = &plan->nchunks;
+    const bool fuse = m.scatter == TB_SCATTER_ATOMIC;
+    ctx->md_fuse = fuse;
     rc = enqueue_compute(ctx, nl, m.pos, m.species, m.r_cut, m.precision, m.scatter, m.forces,
                          nullptr, m.result, nullptr);
+    ctx->md_fuse = false;
     ctx->dplan = nullptr;
     if (rc) break;
-    k_md_kick_ke<<<kb, 256, 0, s0>>>(n, m.vel, m.forces, m.mass, half, ctx->ke_part.as<double>());
+    const int nparts = fuse ? ctx->last_blocks : 0;
+    if (fuse)
+      k_md_kick_ke<true><<<kb, 256, 0, s0>>>(n, m.vel, m.forces, m.mass, half,
+                                             ctx->ke_part.as<double>(), ctx->facc.as<double>());
+    else
+      k_md_kick_ke<false><<<kb, 256, 0, s0>>>(n, m.vel, m.forces, m.mass, half,
+                                              ctx->ke_part.as<double>(), nullptr);
     k_md_tail<<<1, 256, 0, s0>>>(kb, ctx->ke_part.as<double>(), 0.5 / m.accel, m.result, plan,
-                                 m.series, m.record_every, h_loop);
+                                 m.series, m.record_every, h_loop, nparts,
+                                 ctx->partials.as<double>());
     if (cudaGetLastError() != cudaSuccess) rc = fail(ctx, TB_ERR_CUDA, "md capture: launch failed");
   } while (false);
   cudaGraph_t tmp;

@@ -300,10 +300,16 @@ __global__ void k_len_hist_plan(int n, const int *__restrict__ len, DevPlan *__r
 }
 
 // second half-kick fused with the kinetic-energy block partials
+// FUSED (atomic scatter in tb_md_run): the forces come straight from the
+// Tersoff kernel's accumulator -- copied out to f (+0.0 flush) and re-zeroed
+// here, so the step needs no separate finalize pass (its E/W reduction moves
+// to k_md_tail)
+template <bool FUSED>
 __global__ void __launch_bounds__(256) k_md_kick_ke(int n, double *__restrict__ vel,
-                                                    const double *__restrict__ f,
+                                                    double *__restrict__ f,
                                                     const double *__restrict__ mass, double half,
-                                                    double *__restrict__ part) {
+                                                    double *__restrict__ part,
+                                                    double *__restrict__ facc) {
   __shared__ double s[8];
   double acc = 0.0;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
@@ -312,7 +318,15 @@ __global__ void __launch_bounds__(256) k_md_kick_ke(int n, double *__restrict__ 
 #pragma unroll
     for (int ax = 0; ax < 3; ++ax) {
       const int64_t k = 3 * (int64_t)i + ax;
-      v[ax] = __dadd_rn(vel[k], __ddiv_rn(__dmul_rn(half, f[k]), m));
+      double fk;
+      if (FUSED) {
+        fk = __ldcg(facc + k) + 0.0;
+        f[k] = fk;
+        facc[k] = 0.0;
+      } else {
+        fk = f[k];
+      }
+      v[ax] = __dadd_rn(vel[k], __ddiv_rn(__dmul_rn(half, fk), m));
       vel[k] = v[ax];
     }
     acc += m * ((v[0] * v[0] + v[1] * v[1]) + v[2] * v[2]);
@@ -329,15 +343,35 @@ __global__ void __launch_bounds__(256) k_md_kick_ke(int n, double *__restrict__ 
 
 // kinetic energy -> result[7]; [E_pot, E_kin] recorded every `every` steps;
 // the WHILE handle continues while steps remain and nothing overflowed
+// nparts > 0 (fused step): also E and the virial from the Tersoff kernel's
+// block partials (8 doubles per block), the finalize kernel's reduction
 __global__ void k_md_tail(int nb, const double *__restrict__ part, double scale,
                           double *__restrict__ result, DevPlan *__restrict__ plan,
                           double *__restrict__ series, int every,
-                          cudaGraphConditionalHandle h_loop) {
+                          cudaGraphConditionalHandle h_loop, int nparts,
+                          const double *__restrict__ tpart) {
   __shared__ double s[256];
+  __shared__ double sw[8][7];
   double acc = 0.0;
   for (int b = threadIdx.x; b < nb; b += 256) acc += part[b];
+  if (nparts > 0) {
+    double e[7] = {0, 0, 0, 0, 0, 0, 0};
+    for (int b = threadIdx.x; b < nparts; b += 256)
+#pragma unroll
+      for (int q = 0; q < 7; ++q) e[q] += __ldcg(tpart + 8 * (int64_t)b + q);
+#pragma unroll
+    for (int q = 0; q < 7; ++q) e[q] = warp_sum(e[q]);
+    if ((threadIdx.x & 31) == 0)
+#pragma unroll
+      for (int q = 0; q < 7; ++q) sw[threadIdx.x >> 5][q] = e[q];
+  }
   s[threadIdx.x] = acc;
   __syncthreads();
+  if (nparts > 0 && threadIdx.x < 7) {
+    double v = 0.0;
+    for (int w = 0; w < 8; ++w) v += sw[w][threadIdx.x];
+    result[threadIdx.x] = v + 0.0;
+  }
   for (int h = 128; h > 0; h >>= 1) {
     if (threadIdx.x < h) s[threadIdx.x] += s[threadIdx.x + h];
     __syncthreads();
