@@ -1041,7 +1041,10 @@ static int live_repack(tb_context *ctx, tb_nlist *nl, const double *d_pos, doubl
   }
   DevPlan *plan = nl->lplan.as<DevPlan>();
   const int *start = filtered ? nl->coff.as<int>() : nl->offsets.as<int>();
-  constexpr int G = 8;  // lanes per row
+#ifndef TB_LIVE_G
+#define TB_LIVE_G 2  // measured at c3: G = 1/2/4/8/16 -> step 364/347/353/370/416 us
+#endif
+  constexpr int G = TB_LIVE_G;  // lanes per row
   CK(cudaMemsetAsync(plan, 0, sizeof(DevPlan), ctx->stream));
   if (filtered)
     k_live_rows<true, G><<<nblk((int64_t)N * G, 256), 256, 0, ctx->stream>>>(
