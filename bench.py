@@ -297,6 +297,14 @@ def gpu_arm_decomposed(args):
             graph = None
             launch = f"eager (graph capture failed: {str(e)[:80]})"
             torch.cuda.synchronize()
+        # every rank must take the same path (their NCCL call sequences must match)
+        ok = torch.tensor([1 if graph is not None else 0], dtype=torch.int32, device=dev)
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+        if int(ok.item()) == 0 and graph is not None:
+            del graph
+            graph = None
+            step_fn = lambda: ff(dom)  # noqa: E731
+            launch = "eager (graph capture failed on another rank)"
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
     k = args.steps
     starts = [torch.cuda.Event(enable_timing=True) for _ in range(k)]
