@@ -298,7 +298,8 @@ def gpu_arm_decomposed(args):
             launch = f"eager (graph capture failed: {str(e)[:80]})"
             torch.cuda.synchronize()
         # every rank must take the same path (their NCCL call sequences must match)
-        ok = torch.tensor([1 if graph is not None else 0], dtype=torch.int32, device=dev)
+        ok = torch.tensor([1 if graph is not None else 0], dtype=torch.int32,
+                          device=dev if backend == "nccl" else "cpu")
         dist.all_reduce(ok, op=dist.ReduceOp.MIN)
         if int(ok.item()) == 0 and graph is not None:
             del graph
