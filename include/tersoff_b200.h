@@ -82,6 +82,12 @@ int tb_set_stream(tb_context *ctx, void *stream);
  * rows on the device, so that dead entries occupy no warp lanes.  Auto: on for
  * atomic scatter over species-filtered rows (multi-species tables). */
 #define TB_OPT_LIVE_PACK 3
+/* TB_OPT_MD_LOOSE_SKIN = h: tb_md_run (one species, atomic scatter) keeps a
+ * list with skin + h/100 A (default 30 = 0.3 A) that it rebuilds only when an
+ * atom moved more than half of that; the reference's own rebuilds are still
+ * decided, counted and their positions kept, and the exact list at the last of
+ * them is rebuilt when the run ends.  0 = rebuild the exact list every time. */
+#define TB_OPT_MD_LOOSE_SKIN 4
 int tb_set_option(tb_context *ctx, int option, int value);
 
 /* Synchronise the context's stream. */

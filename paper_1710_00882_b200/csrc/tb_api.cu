@@ -78,6 +78,10 @@ struct tb_context {
   bool profile = false;
   bool force_tile = false;
   int live_pack = 2;  // TB_OPT_LIVE_PACK: 0 off, 1 on, 2 auto
+#ifndef TB_MD_LOOSE_DEFAULT
+#define TB_MD_LOOSE_DEFAULT 0.3
+#endif
+  double md_loose = TB_MD_LOOSE_DEFAULT;  // TB_OPT_MD_LOOSE_SKIN: extra list skin (A) of tb_md_run, 0 = off
   double list_margin = 0.25;  // TB_OPT_LIST_MARGIN
   bool warp_per_chunk = getenv("TB_WARP_PER_CHUNK") != nullptr;
   bool no_filter = getenv("TB_NO_FILTER") != nullptr;  // disable the species-pair compute filter
@@ -125,6 +129,7 @@ struct tb_nlist {
   // the evaluation's positions (pack_adjacency, neighbor.py:330-360), re-chunked
   // on the device every evaluation
   DevBuf lplan, llen, lrow, lrowj, lsorted, llanes;
+  DevBuf ref_log;  // tb_md_run loose list: positions of the reference's last rebuild
   bool fnbr_ok = false;  // fnbr matches centry (written by every filter pass since)
   int64_t lcap = 0;  // chunk capacity of llanes
   struct MdGraph *md = nullptr;
@@ -136,6 +141,7 @@ struct MdKey {
   int64_t n, ecap, ccap, ncell;
   double dt, accel, skin, r_cut;
   int rebuild_every, precision, scatter, record_every, param_version, filtered, S, tile;
+  double loose;
 };
 
 struct MdGraph {
@@ -353,6 +359,11 @@ extern "C" int tb_set_option(tb_context *ctx, int option, int value) {
     ctx->live_pack = value;
     return TB_OK;
   }
+  if (option == TB_OPT_MD_LOOSE_SKIN) {
+    if (value < 0 || value > 300) return fail(ctx, TB_ERR_ARG, "loose skin %d out of range", value);
+    ctx->md_loose = value / 100.0;
+    return TB_OK;
+  }
   if (option == TB_OPT_LIST_MARGIN) {
     if (value < 0 || value > 1000) return fail(ctx, TB_ERR_ARG, "list margin %d%% out of range", value);
     ctx->list_margin = value / 100.0;
@@ -468,7 +479,7 @@ extern "C" void tb_nlist_destroy(tb_nlist *nl) {
                     &nl->maxrow, &nl->nl_row, &nl->sorted_atoms, &nl->sort_keys,
                     &nl->iota, &nl->lanes, &nl->hist, &nl->cpos, &nl->crow, &nl->coff,
                     &nl->centry, &nl->fnbr, &nl->fbuf, &nl->plan, &nl->scratch, &nl->lplan,
-                    &nl->llen, &nl->lrow, &nl->lrowj, &nl->lsorted, &nl->llanes};
+                    &nl->llen, &nl->lrow, &nl->lrowj, &nl->lsorted, &nl->llanes, &nl->ref_log};
   for (DevBuf *b : bufs) b->release();
   md_graph_release(nl);
   delete nl;
@@ -1575,6 +1586,8 @@ struct MdArgs {
   double dt, accel, r_cut, skin;
   int rebuild_every, precision, scatter, record_every;
   double *series, *result;
+  double loose = 0.0;         // > 0: the list carries skin + loose (see k_md_decide)
+  double *ref_log = nullptr;  // loose: positions of the reference's last rebuild
 };
 }  // namespace
 
@@ -1587,7 +1600,7 @@ static MdKey md_key(const tb_context *ctx, const tb_nlist *nl, const MdArgs &m) 
                      nl->row_count.p, nl->nl_row.p, nl->sorted_atoms.p, nl->sort_keys.p,
                      nl->iota.p, nl->lanes.p, nl->cpos.p, nl->crow.p, nl->coff.p, nl->centry.p,
                      nl->fbuf.p, ctx->facc.p, ctx->partials.p, ctx->ke_part.p, ctx->errf.p,
-                     ctx->cub_tmp.p, nl->scratch.p};
+                     ctx->cub_tmp.p, nl->scratch.p, m.ref_log};
   static_assert(sizeof(p) / sizeof(p[0]) <= 40, "MdKey::ptr too small");
   memcpy(k.ptr, p, sizeof(p));
   k.n = m.n;
@@ -1598,6 +1611,7 @@ static MdKey md_key(const tb_context *ctx, const tb_nlist *nl, const MdArgs &m) 
   k.accel = m.accel;
   k.skin = m.skin;
   k.r_cut = m.r_cut;
+  k.loose = m.loose;
   k.rebuild_every = m.rebuild_every;
   k.precision = m.precision;
   k.scatter = m.scatter;
@@ -1647,10 +1661,12 @@ static int md_capture(tb_context *ctx, tb_nlist *nl, const MdArgs &m, MdGraph *G
   ctx->stream = s0;
   int rc = TB_OK;
   do {
+    const double hl = 0.5 * (m.skin + m.loose);
     k_md_kick_drift<<<nblk(n, 256), 256, 0, s0>>>(n, m.pos, m.vel, m.forces, m.mass,
                                                    nl->ref_pos.as<double>(), half, m.dt, box,
-                                                   plan);
-    k_md_decide<<<1, 1, 0, s0>>>(plan, hs * hs, m.rebuild_every, h_reb);
+                                                   plan, m.loose > 0 ? m.ref_log : nullptr);
+    k_md_decide<<<1, 1, 0, s0>>>(plan, hs * hs, m.rebuild_every, h_reb, m.loose > 0 ? 1 : 0,
+                                 hl * hl);
     if (cudaGetLastError() != cudaSuccess) {
       rc = fail(ctx, TB_ERR_CUDA, "md capture: launch failed");
       break;
@@ -1697,10 +1713,12 @@ static int md_capture(tb_context *ctx, tb_nlist *nl, const MdArgs &m, MdGraph *G
     const int nparts = fuse ? ctx->last_blocks : 0;
     if (fuse)
       k_md_kick_ke<true><<<kb, 256, 0, s0>>>(n, m.vel, m.forces, m.mass, half,
-                                             ctx->ke_part.as<double>(), ctx->facc.as<double>());
+                                             ctx->ke_part.as<double>(), ctx->facc.as<double>(),
+                                             plan, m.pos, m.loose > 0 ? m.ref_log : nullptr);
     else
       k_md_kick_ke<false><<<kb, 256, 0, s0>>>(n, m.vel, m.forces, m.mass, half,
-                                              ctx->ke_part.as<double>(), nullptr);
+                                              ctx->ke_part.as<double>(), nullptr, plan, m.pos,
+                                              m.loose > 0 ? m.ref_log : nullptr);
     k_md_tail<<<1, 256, 0, s0>>>(kb, ctx->ke_part.as<double>(), 0.5 / m.accel, m.result, plan,
                                  m.series, m.record_every, h_loop, nparts,
                                  ctx->partials.as<double>());
@@ -1793,15 +1811,45 @@ extern "C" int tb_md_run(tb_context *ctx, tb_nlist *nl, int64_t n, double *d_pos
            rebuild_every, precision, scatter, record_every, d_series, d_result};
   const int N = (int)n;
   int64_t extra = 0;
-  CK(ctx->snap.ensure(sizeof(double) * 9 * (size_t)N + sizeof(double)));
+  // Loose list (one species, atomic scatter; TB_OPT_MD_LOOSE_SKIN): the run's
+  // list carries skin + loose and is rebuilt only when some atom moved more
+  // than (skin + loose)/2 since its build; the reference's rebuilds (skin/2
+  // trigger, fixed cadence) are still decided, counted and their positions
+  // kept (ref_log) -- and the exact list at the last of them is rebuilt when
+  // the run ends.  Pair terms are the same either way: every evaluation
+  // re-tests r < r_cut on a list that holds all such pairs.
+  const bool loose = ctx->md_loose > 0 && ctx->S == 1 && scatter == TB_SCATTER_ATOMIC;
+  const double skin_list = loose ? skin + ctx->md_loose : skin;
+  CK(ctx->snap.ensure(sizeof(double) * (loose ? 12 : 9) * (size_t)N + sizeof(double)));
   double *snap = ctx->snap.as<double>();
+  if (loose) {
+    CK(nl->ref_log.ensure(sizeof(double) * 3 * (size_t)N));
+    CK(cudaMemcpyAsync(nl->ref_log.p, nl->ref_pos.p, sizeof(double) * 3 * N,
+                       cudaMemcpyDeviceToDevice, ctx->stream));
+    CK(cudaMemcpyAsync(snap + 9 * N + 1, nl->ref_pos.p, sizeof(double) * 3 * N,
+                       cudaMemcpyDeviceToDevice, ctx->stream));
+    int rc = tb_build_neighbors(ctx, nl, n, d_positions, nl->L, nl->per, r_cut, skin_list);
+    if (rc) return rc;
+    if (nl->nchunks <= 0) {  // rows beyond the warp kernel: back to the exact list, per-step path
+      rc = tb_build_neighbors(ctx, nl, n, nl->ref_log.as<double>(), nl->L, nl->per, r_cut, skin);
+      return rc ? rc : fail(ctx, TB_ERR_UNSUPPORTED, "device-resident loop: rows exceed 32 entries");
+    }
+    m.loose = ctx->md_loose;
+    m.ref_log = nl->ref_log.as<double>();
+  }
+  // the exact list at the reference's last rebuild (loose runs, any exit)
+  auto finish = [&](int rc) -> int {
+    if (!loose) return rc;
+    int rc2 = tb_build_neighbors(ctx, nl, n, nl->ref_log.as<double>(), nl->L, nl->per, r_cut, skin);
+    return rc ? rc : rc2;
+  };
   CK(cudaMemcpyAsync(snap, d_positions, sizeof(double) * 3 * N, cudaMemcpyDeviceToDevice, ctx->stream));
   CK(cudaMemcpyAsync(snap + 3 * N, d_velocities, sizeof(double) * 3 * N, cudaMemcpyDeviceToDevice, ctx->stream));
   CK(cudaMemcpyAsync(snap + 6 * N, d_forces, sizeof(double) * 3 * N, cudaMemcpyDeviceToDevice, ctx->stream));
   CK(cudaMemcpyAsync(snap + 9 * N, d_result, sizeof(double), cudaMemcpyDeviceToDevice, ctx->stream));
   for (int attempt = 0;; ++attempt) {
     int rc0 = md_prepare(ctx, nl, d_species, scatter);
-    if (rc0) return rc0;
+    if (rc0) return finish(rc0);
     const bool filter_wanted = ctx->S > 1 && !ctx->no_filter;
     // ---- graph (re)capture when anything it holds changed ----
     const MdKey key = md_key(ctx, nl, m);
@@ -1812,7 +1860,7 @@ extern "C" int tb_md_run(tb_context *ctx, tb_nlist *nl, int64_t n, double *d_pos
       int rc = md_capture(ctx, nl, m, nl->md);
       if (rc) {
         md_graph_release(nl);
-        return rc;
+        return finish(rc);
       }
     }
     // ---- run ----
@@ -1836,24 +1884,27 @@ extern "C" int tb_md_run(tb_context *ctx, tb_nlist *nl, int64_t n, double *d_pos
       if (hp.rebuilds > 0 && scatter != TB_SCATTER_GATHER) nl->rev_valid = false;
       if (hp.rebuilds > 0 && filter_wanted) nl->fbuf_zero = scatter == TB_SCATTER_GATHER;
       if (rebuilds) *rebuilds = hp.rebuilds + extra;
-      return tb_check_errors(ctx);
+      return finish(tb_check_errors(ctx));
     }
     // ---- capacity overflow: back to the entry state, regrow, replay ----
     CK(cudaMemcpyAsync(d_positions, snap, sizeof(double) * 3 * N, cudaMemcpyDeviceToDevice, ctx->stream));
     CK(cudaMemcpyAsync(d_velocities, snap + 3 * N, sizeof(double) * 3 * N, cudaMemcpyDeviceToDevice, ctx->stream));
     CK(cudaMemcpyAsync(d_forces, snap + 6 * N, sizeof(double) * 3 * N, cudaMemcpyDeviceToDevice, ctx->stream));
     CK(cudaMemcpyAsync(d_result, snap + 9 * N, sizeof(double), cudaMemcpyDeviceToDevice, ctx->stream));
+    if (loose)
+      CK(cudaMemcpyAsync(nl->ref_log.p, snap + 9 * N + 1, sizeof(double) * 3 * N,
+                         cudaMemcpyDeviceToDevice, ctx->stream));
     if ((hp.overflow & OVF_ROW) || attempt >= 3)
-      return fail(ctx, TB_ERR_UNSUPPORTED,
-                  "device-resident loop: neighbour rows outgrew the warp kernel (overflow %d)",
-                  hp.overflow);
+      return finish(fail(ctx, TB_ERR_UNSUPPORTED,
+                         "device-resident loop: neighbour rows outgrew the warp kernel (overflow %d)",
+                         hp.overflow));
     nl->margin = std::max(2.0 * nl->margin, 0.25);
-    int rc = tb_build_neighbors(ctx, nl, n, d_positions, nl->L, nl->per, r_cut, skin);
-    if (rc) return rc;
+    int rc = tb_build_neighbors(ctx, nl, n, d_positions, nl->L, nl->per, r_cut, skin_list);
+    if (rc) return finish(rc);
     nl->filtered = false;
     extra += 1;
     if (nl->nchunks <= 0)
-      return fail(ctx, TB_ERR_UNSUPPORTED, "device-resident loop: rows exceed 32 entries");
+      return finish(fail(ctx, TB_ERR_UNSUPPORTED, "device-resident loop: rows exceed 32 entries"));
   }
 }
 

@@ -35,6 +35,11 @@ struct DevPlan {
   int unwrapped;          // k_cell_index: a periodic coordinate outside [0, L]
   int pad;
   unsigned long long drift_bits;  // max |x - x_ref|^2 of this step (bits; r^2 >= 0)
+  // loose-list runs (tb_md_run, TB_OPT_MD_LOOSE_SKIN): the reference's own
+  // trigger measured against the positions of its last (logical) rebuild
+  unsigned long long drift_log_bits;
+  int log_now;            // this step is one of the reference's rebuilds
+  int pad2;
   int hist[34];
   int bucket_start[34], chunk_base[34];
   int cursor[34];         // k_bucket_rows
@@ -48,9 +53,10 @@ __global__ void __launch_bounds__(256) k_md_kick_drift(int n, double *__restrict
                                                        const double *__restrict__ mass,
                                                        const double *__restrict__ ref, double half,
                                                        double dt, Box box,
-                                                       DevPlan *__restrict__ plan) {
+                                                       DevPlan *__restrict__ plan,
+                                                       const double *__restrict__ ref_log) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  unsigned long long best = 0;
+  unsigned long long best = 0, best_log = 0;
   if (i < n) {
     const double m = mass[i];
     double x[3];
@@ -67,24 +73,46 @@ __global__ void __launch_bounds__(256) k_md_kick_drift(int n, double *__restrict
     double r[3], d[3];
     load3(ref, i, r);
     best = __double_as_longlong(disp_r2(r, x, box, d));
+    if (ref_log) {
+      load3(ref_log, i, r);
+      best_log = __double_as_longlong(disp_r2(r, x, box, d));
+    }
   }
   for (int o = 16; o > 0; o >>= 1) {
     unsigned long long v = __shfl_down_sync(0xffffffffu, best, o);
     best = v > best ? v : best;
+    v = __shfl_down_sync(0xffffffffu, best_log, o);
+    best_log = v > best_log ? v : best_log;
   }
   if ((threadIdx.x & 31) == 0 && best) atomicMax(&plan->drift_bits, best);
+  if ((threadIdx.x & 31) == 0 && best_log) atomicMax(&plan->drift_log_bits, best_log);
 }
 
-// rebuild decision for this step (skin/2 trigger or the fixed cadence)
+// rebuild decision for this step (skin/2 trigger or the fixed cadence).
+// loose (> 0): the list was built with skin + delta; the reference's rebuild
+// (counted, and its positions kept as the trigger's new reference) follows its
+// own rule against ref_log, while the list itself is rebuilt only when some atom
+// moved more than (skin + delta)/2 since the list's build -- until then every
+// pair within r_cut is still in it, and the evaluation re-tests r < r_cut
 __global__ void k_md_decide(DevPlan *__restrict__ plan, double half_skin2, int rebuild_every,
-                            cudaGraphConditionalHandle h_rebuild) {
+                            cudaGraphConditionalHandle h_rebuild, int loose,
+                            double half_loose2) {
   const double d2 = __longlong_as_double((long long)plan->drift_bits);
   const int step = plan->step + 1;
-  const bool need = d2 > half_skin2 || (rebuild_every > 0 && step % rebuild_every == 0);
   plan->step = step;
   plan->drift_bits = 0ull;
-  if (need) plan->rebuilds += 1;
-  cudaGraphSetConditional(h_rebuild, need ? 1u : 0u);
+  if (!loose) {
+    const bool need = d2 > half_skin2 || (rebuild_every > 0 && step % rebuild_every == 0);
+    if (need) plan->rebuilds += 1;
+    cudaGraphSetConditional(h_rebuild, need ? 1u : 0u);
+    return;
+  }
+  const double dl2 = __longlong_as_double((long long)plan->drift_log_bits);
+  plan->drift_log_bits = 0ull;
+  const bool logical = dl2 > half_skin2 || (rebuild_every > 0 && step % rebuild_every == 0);
+  plan->log_now = logical ? 1 : 0;
+  if (logical) plan->rebuilds += 1;
+  cudaGraphSetConditional(h_rebuild, d2 > half_loose2 ? 1u : 0u);
 }
 
 // reset the per-build counters (full) or only the histogram (filter pass)
@@ -309,10 +337,19 @@ __global__ void __launch_bounds__(256) k_md_kick_ke(int n, double *__restrict__ 
                                                     double *__restrict__ f,
                                                     const double *__restrict__ mass, double half,
                                                     double *__restrict__ part,
-                                                    double *__restrict__ facc) {
+                                                    double *__restrict__ facc,
+                                                    const DevPlan *__restrict__ plan,
+                                                    const double *__restrict__ pos,
+                                                    double *__restrict__ ref_log) {
   __shared__ double s[8];
   double acc = 0.0;
+  // a loose-list run keeps the positions of the reference's rebuilds
+  const bool keep = ref_log && plan->log_now;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    if (keep) {
+#pragma unroll
+      for (int ax = 0; ax < 3; ++ax) ref_log[3 * (int64_t)i + ax] = pos[3 * (int64_t)i + ax];
+    }
     const double m = mass[i];
     double v[3];
 #pragma unroll
