@@ -138,3 +138,28 @@ def test_graph_loop_free_axis_falls_back():
     assert rec["loop"] == "step"
     with pytest.raises(RuntimeError):
         run_nve_device(st, t, RunConfig(dt=1.0, steps=5, skin=0.3), loop="graph")
+
+
+@pytest.mark.parametrize("precision", ["double", "single"])
+def test_loose_list_matches_exact_list(precision):
+    """tb_md_run with the loose list (skin + 0.3 A, rebuilt only for validity)
+    and with the exact list rebuilt at every reference rebuild: same rebuild
+    count and the same trajectory to round-off."""
+    from paper_1710_00882_b200 import _native
+    st, tname = structures.config(2, small=True)
+    t = builtin_params(tname)
+    cfg = RunConfig(dt=1.0, steps=200, skin=0.3, rebuild_every=10)
+    ctx = _native.default_context(0)
+    ctx.set_option(_native.OPT_MD_LOOSE_SKIN, 0)
+    try:
+        exact = run_nve_device(st.copy(), t, cfg, precision=precision, loop="graph",
+                               record_every=1)
+    finally:
+        ctx.set_option(_native.OPT_MD_LOOSE_SKIN, 30)
+    loose = run_nve_device(st.copy(), t, cfg, precision=precision, loop="graph", record_every=1)
+    assert loose["loop"] == exact["loop"] == "graph"
+    assert loose["rebuilds"] == exact["rebuilds"] > 20
+    scale = abs(exact["total"][0])
+    tol = 1e-9 if precision == "double" else 1e-6
+    assert np.max(np.abs(loose["total"] - exact["total"])) <= tol * scale
+    assert np.abs(loose["positions"] - exact["positions"]).max() <= (1e-7 if precision == "double" else 1e-4)
