@@ -44,6 +44,12 @@ namespace tb {
 #ifndef TB_FP64_REG
 #define TB_FP64_REG 0  // fp64 kernel: energy/virial + angular cache in registers too
 #endif
+#ifndef TB_FP64_REGACC
+// fp64 kernel, one species: energy/virial accumulators in registers (124 regs,
+// no spill since the constants moved to constant memory): c5 2.74 -> 2.62 ms,
+// c2 unchanged, c4 +1.5%
+#define TB_FP64_REGACC 1
+#endif
 constexpr int WNT = 128;  // threads per block of the warp kernel
 constexpr int WPB = WNT / 32;
 #ifndef TB_WNT64
@@ -205,7 +211,7 @@ template <class T, int S, bool LAM3, int MODE, bool ST, int LC>
 __device__ __forceinline__ void chunk_body(const KArgs &a, const WArgs &w, const Tables<T, S> &tab,
                                            T (*s_cache)[3][32], WTable<T> &tb, const int lane,
                                            const int4 cur, const WStage &stg, const int Ldyn,
-                                           WAcc<sizeof(T) == 4 || TB_FP64_REG> &A) {
+                                           WAcc<sizeof(T) == 4 || TB_FP64_REG || (S == 1 && TB_FP64_REGACC)> &A) {
   static_assert(S <= 2, "the warp kernel handles up to two species");
   using T2 = typename Vec2<T>::t;
   const int e = cur.x, i = cur.y, j = cur.z;
@@ -686,12 +692,12 @@ __global__ void __launch_bounds__(WarpCfg<T>::nt, WarpCfg<T>::minb)
     if (sm < 0 || sm >= S) atomicMin(&a.err->bad_species_atom, m);
   }
 
-  WAcc<sizeof(T) == 4 || TB_FP64_REG> A;
+  WAcc<sizeof(T) == 4 || TB_FP64_REG || (S == 1 && TB_FP64_REGACC)> A;
 #pragma unroll
   for (int q = 0; q < 7; ++q) s_acc[wid][q][lane] = 0.0;
   A.acc = &s_acc[wid][0][lane];
 #pragma unroll
-  for (int q = 0; q < (sizeof(T) == 4 || TB_FP64_REG ? 7 : 1); ++q) A.r[q] = 0.0;
+  for (int q = 0; q < (sizeof(T) == 4 || TB_FP64_REG || (S == 1 && TB_FP64_REGACC) ? 7 : 1); ++q) A.r[q] = 0.0;
 
   // software pipeline over this warp's chunks: lane records in registers two
   // chunks ahead; the position/species gathers of the next chunk are issued
