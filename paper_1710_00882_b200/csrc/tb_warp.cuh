@@ -44,6 +44,9 @@ namespace tb {
 #ifndef TB_FP64_REG
 #define TB_FP64_REG 0  // fp64 kernel: energy/virial + angular cache in registers too
 #endif
+#ifndef TB_FP64_SHUF_E
+#define TB_FP64_SHUF_E 1
+#endif
 #ifndef TB_FP64_REGACC
 // fp64 kernel, one species: energy/virial accumulators in registers (124 regs,
 // no spill since the constants moved to constant memory): c5 2.74 -> 2.62 ms,
@@ -376,7 +379,7 @@ __device__ __forceinline__ void chunk_body(const KArgs &a, const WArgs &w, const
   else
     tb.dz[lane] = dz;
   const double vd = (double)v;
-  if (sizeof(T) == 8) tb.v[lane] = vd;
+  if (!(sizeof(T) == 4 || (S == 1 && TB_FP64_REGACC && TB_FP64_SHUF_E))) tb.v[lane] = vd;
   __syncwarp();
 
   // ---- phase 2: force on this neighbour from the terms centred on i ----
@@ -474,7 +477,10 @@ __device__ __forceinline__ void chunk_body(const KArgs &a, const WArgs &w, const
   // (fp64 sums; the mixed kernel sums its fp32 force pieces in fp32 first --
   // fewer shuffles -- while fp64 keeps e_i as a row-order shared-memory sum)
   constexpr bool MIXED = sizeof(T) == 4;
-  double ev = MIXED ? vd : 0.0;
+  // e_i by shuffles (mixed; fp64 one species when its accumulators are in
+  // registers), else a row-order sum from the shared V table
+  constexpr bool SHUF_E = MIXED || (S == 1 && TB_FP64_REGACC && TB_FP64_SHUF_E);
+  double ev = SHUF_E ? vd : 0.0;
   T sx = tfx, sy = tfy, sz = tfz;
   double dsx = fx, dsy = fy, dsz = fz;
   if (LC > 0 && (LC & (LC - 1)) == 0) {
@@ -492,7 +498,7 @@ __device__ __forceinline__ void chunk_body(const KArgs &a, const WArgs &w, const
           dsz += __shfl_xor_sync(0xffffffffu, dsz, off);
         }
       }
-      if (MIXED) ev += __shfl_xor_sync(0xffffffffu, ev, off);
+      if (SHUF_E) ev += __shfl_xor_sync(0xffffffffu, ev, off);
     }
   } else {
 #pragma unroll
@@ -520,7 +526,7 @@ __device__ __forceinline__ void chunk_body(const KArgs &a, const WArgs &w, const
           }
         }
       }
-      if (MIXED) {
+      if (SHUF_E) {
         const double ov = __shfl_down_sync(0xffffffffu, ev, off);
         if (in) ev += ov;
       }
@@ -548,7 +554,7 @@ __device__ __forceinline__ void chunk_body(const KArgs &a, const WArgs &w, const
   // ---- e_i (the row's first lane) ----
   if (valid && pos == 0) {
     double se = ev;
-    if (!MIXED) {  // row order, from the shared table
+    if (!SHUF_E) {  // row order, from the shared table
       se = 0.0;
 #pragma unroll
       for (int q = 0; q < (LC > 0 ? LC : 1); ++q) se += tb.v[lane + q];
