@@ -44,6 +44,9 @@ namespace tb {
 #ifndef TB_FP64_REG
 #define TB_FP64_REG 0  // fp64 kernel: energy/virial + angular cache in registers too
 #endif
+#ifndef TB_FP64_RC2
+#define TB_FP64_RC2 1  // measured: c2 20.94 -> 20.69 us, c5 2.58 -> 2.51 ms, c4 470 -> 476 us (80 B spill)
+#endif
 #ifndef TB_FP64_SHUF_E
 #define TB_FP64_SHUF_E 1
 #endif
@@ -300,7 +303,10 @@ __device__ __forceinline__ void chunk_body(const KArgs &a, const WArgs &w, const
   // the cache of (cos, g, dg) per partner: registers for the unrolled mixed
   // kernel (compile-time indices), shared memory otherwise
   constexpr bool RC = LC > 0 && (sizeof(T) == 4 || TB_FP64_REG);
-  T rcos[RC ? QCAP : 1], rg[RC ? QCAP : 1], rdg[RC ? QCAP : 1];
+  // RC2 (fp64, one species, unrolled rows): g and dg in registers, cos
+  // recomputed in phase 2 from the partner's unit vector it loads anyway
+  constexpr bool RC2 = !RC && LC > 0 && S == 1 && TB_FP64_RC2;
+  T rcos[RC ? QCAP : 1], rg[RC || RC2 ? QCAP : 1], rdg[RC || RC2 ? QCAP : 1];
   T zeta = T(0);
   // only live partners of the row contribute (a dead b has f_C = dzeta = 0);
   // lanes iterate their own row's live mask (the table is in shared memory,
@@ -332,6 +338,9 @@ __device__ __forceinline__ void chunk_body(const KArgs &a, const WArgs &w, const
     if (q < QCAP) {
       if (RC) {
         rcos[q] = cost;
+        rg[q] = g;
+        rdg[q] = dg;
+      } else if (RC2) {
         rg[q] = g;
         rdg[q] = dg;
       } else {
@@ -414,6 +423,11 @@ __device__ __forceinline__ void chunk_body(const KArgs &a, const WArgs &w, const
     if (q < QCAP) {
       if (RC) {
         cost = rcos[q];
+        g = rg[q];
+        dg = rdg[q];
+      } else if (RC2) {
+        cost = ex * be.x + ey * be.y + ez * be.z;  // same bits as phase 1's
+        TB_CLAMP_COS(cost);
         g = rg[q];
         dg = rdg[q];
       } else {
