@@ -216,7 +216,7 @@ __global__ void __launch_bounds__(256) k_fill_lanes_dev(const DevPlan *__restric
       const int atom = sorted_atoms[s_start[L] + row];
       const int k = offsets[atom] + lane % L;
       const int e = centry ? centry[k] : k;
-      v = make_int4(e, atom, nbr[e], L);
+      v = make_int4(e, atom, nbr[e], L | ((lane % L) << 8));
     }
     lanes[32 * (int64_t)c + lane] = v;
   }
@@ -310,7 +310,7 @@ __global__ void __launch_bounds__(256) k_bucket_fill(int n, const int *__restric
   const int b = start[i];
   // lrow == nullptr: the rows are the list's own (entry = b + k, j = lrowj[b + k])
   for (int k = 0; k < L; ++k)
-    dst[r * L + k] = make_int4(lrow ? lrow[b + k] : b + k, i, lrowj[b + k], L);
+    dst[r * L + k] = make_int4(lrow ? lrow[b + k] : b + k, i, lrowj[b + k], L | (k << 8));
   const bool last_in_chunk = r == rpc - 1, last_in_bucket = s == plan->hist[L] - 1;
   if (last_in_chunk || last_in_bucket)
     for (int k = (r + 1) * L; k < 32; ++k) dst[k] = make_int4(-1, 0, 0, L);

@@ -88,7 +88,7 @@ __device__ __forceinline__ T pick(const T (&x)[S], int k) {
 }
 
 struct WArgs {
-  const int4 *__restrict__ lanes;      // [nchunks*32] {entry, i, j, L}; entry -1 = idle lane
+  const int4 *__restrict__ lanes;      // [nchunks*32] {entry, i, j, L | pos << 8}; entry -1 = idle lane
   const int *__restrict__ empty_atoms; // atoms with empty rows (per_atom = 0)
   int nchunks, n_empty;
   const int *__restrict__ dinfo;       // non-null: {nchunks, n_empty} in device memory (tb_md_run)
@@ -200,7 +200,7 @@ __device__ __forceinline__ void stage_chunk(WStage &st, const int4 rec, const in
     // HEAD (mixed kernel): x_i and s_i once per row (its first lane), read by
     // the row's lanes from that slot -- less staging traffic on the L1/shared
     // pipe that bounds the mixed kernel (fp64 measured faster per lane)
-    const bool head = !HEAD || lane % rec.w == 0;
+    const bool head = !HEAD || (rec.w >> 8) == 0;  // w = L | (position in the row << 8)
 #pragma unroll
     for (int q = 0; q < 3; ++q) {
       if (head) cp_async8(&st.xi[q][lane], pos + 3 * (int64_t)rec.y + q);
@@ -224,7 +224,9 @@ __device__ __forceinline__ void chunk_body(const KArgs &a, const WArgs &w, const
   const int L = LC > 0 ? LC : Ldyn;  // warp-uniform row length
   const bool valid = e >= 0;
   constexpr bool POW2 = LC > 0 && (LC & (LC - 1)) == 0;
-  const int pos = POW2 ? (lane & (LC - 1)) : lane % L;
+  // position in the row: by mask / constant modulo for unrolled rows, else
+  // from the lane record (w = L | pos << 8; no runtime division)
+  const int pos = POW2 ? (lane & (LC - 1)) : (LC > 0 ? lane % LC : (cur.w >> 8));
   const int first = lane - pos;
 
   // ---- pack: displacement with min image, r2 < r_cut^2 ----
@@ -754,7 +756,7 @@ __global__ void __launch_bounds__(WarpCfg<T>::nt, WarpCfg<T>::minb)
     cp_async_wait<1>();  // this lane's gathers for the current chunk have landed
     if (sizeof(T) == 4) __syncwarp();  // ... and the row heads' x_i / s_i are visible
     const WStage &stg = s_stage[wid][buf];
-    const int Ldyn = __shfl_sync(0xffffffffu, cur.w, 0);
+    const int Ldyn = __shfl_sync(0xffffffffu, cur.w, 0) & 0xff;
     // short rows (diamond: 4): fixed rotation, unrolled; longer rows: live masks
     switch (Ldyn) {
       case 4: chunk_body<T, S, LAM3, MODE, ST, 4>(a, w, tab, s_cache[wid], s_tb[wid], lane, cur, stg, Ldyn, A); break;
@@ -847,7 +849,7 @@ __global__ void k_fill_lanes(const ChunkPlan plan, const int *__restrict__ sorte
     const int atom = sorted_atoms[plan.bucket_start[L] + row];
     const int k = offsets[atom] + lane % L;
     const int e = centry ? centry[k] : k;
-    v = make_int4(e, atom, nbr[e], L);
+    v = make_int4(e, atom, nbr[e], L | ((lane % L) << 8));  // w = L | position << 8
   }
   lanes[32 * (int64_t)c + lane] = v;
 }
