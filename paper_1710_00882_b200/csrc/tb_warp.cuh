@@ -47,6 +47,9 @@ namespace tb {
 #ifndef TB_FP64_RC2
 #define TB_FP64_RC2 1  // measured: c2 20.94 -> 20.69 us, c5 2.58 -> 2.51 ms, c4 470 -> 476 us (80 B spill)
 #endif
+#ifndef TB_FP64_REGACC_S2
+#define TB_FP64_REGACC_S2 1  // two species too (c3 fp64 230 -> 226 us)
+#endif
 #ifndef TB_FP64_SHUF_E
 #define TB_FP64_SHUF_E 1
 #endif
@@ -217,7 +220,7 @@ template <class T, int S, bool LAM3, int MODE, bool ST, int LC>
 __device__ __forceinline__ void chunk_body(const KArgs &a, const WArgs &w, const Tables<T, S> &tab,
                                            T (*s_cache)[3][32], WTable<T> &tb, const int lane,
                                            const int4 cur, const WStage &stg, const int Ldyn,
-                                           WAcc<sizeof(T) == 4 || TB_FP64_REG || (S == 1 && TB_FP64_REGACC)> &A) {
+                                           WAcc<sizeof(T) == 4 || TB_FP64_REG || ((S == 1 || TB_FP64_REGACC_S2) && TB_FP64_REGACC)> &A) {
   static_assert(S <= 2, "the warp kernel handles up to two species");
   using T2 = typename Vec2<T>::t;
   const int e = cur.x, i = cur.y, j = cur.z;
@@ -390,7 +393,7 @@ __device__ __forceinline__ void chunk_body(const KArgs &a, const WArgs &w, const
   else
     tb.dz[lane] = dz;
   const double vd = (double)v;
-  if (!(sizeof(T) == 4 || (S == 1 && TB_FP64_REGACC && TB_FP64_SHUF_E))) tb.v[lane] = vd;
+  if (!(sizeof(T) == 4 || ((S == 1 || TB_FP64_REGACC_S2) && TB_FP64_REGACC && TB_FP64_SHUF_E))) tb.v[lane] = vd;
   __syncwarp();
 
   // ---- phase 2: force on this neighbour from the terms centred on i ----
@@ -495,7 +498,7 @@ __device__ __forceinline__ void chunk_body(const KArgs &a, const WArgs &w, const
   constexpr bool MIXED = sizeof(T) == 4;
   // e_i by shuffles (mixed; fp64 one species when its accumulators are in
   // registers), else a row-order sum from the shared V table
-  constexpr bool SHUF_E = MIXED || (S == 1 && TB_FP64_REGACC && TB_FP64_SHUF_E);
+  constexpr bool SHUF_E = MIXED || ((S == 1 || TB_FP64_REGACC_S2) && TB_FP64_REGACC && TB_FP64_SHUF_E);
   double ev = SHUF_E ? vd : 0.0;
   T sx = tfx, sy = tfy, sz = tfz;
   double dsx = fx, dsy = fy, dsz = fz;
@@ -714,12 +717,12 @@ __global__ void __launch_bounds__(WarpCfg<T>::nt, WarpCfg<T>::minb)
     if (sm < 0 || sm >= S) atomicMin(&a.err->bad_species_atom, m);
   }
 
-  WAcc<sizeof(T) == 4 || TB_FP64_REG || (S == 1 && TB_FP64_REGACC)> A;
+  WAcc<sizeof(T) == 4 || TB_FP64_REG || ((S == 1 || TB_FP64_REGACC_S2) && TB_FP64_REGACC)> A;
 #pragma unroll
   for (int q = 0; q < 7; ++q) s_acc[wid][q][lane] = 0.0;
   A.acc = &s_acc[wid][0][lane];
 #pragma unroll
-  for (int q = 0; q < (sizeof(T) == 4 || TB_FP64_REG || (S == 1 && TB_FP64_REGACC) ? 7 : 1); ++q) A.r[q] = 0.0;
+  for (int q = 0; q < (sizeof(T) == 4 || TB_FP64_REG || ((S == 1 || TB_FP64_REGACC_S2) && TB_FP64_REGACC) ? 7 : 1); ++q) A.r[q] = 0.0;
 
   // software pipeline over this warp's chunks: lane records in registers two
   // chunks ahead; the position/species gathers of the next chunk are issued
