@@ -9,6 +9,13 @@ __global__ void k_big(const __grid_constant__ Big b, int *p) { if (threadIdx.x =
 __global__ void k_fill(float *p, size_t n) {
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) p[i] = 0.f;
 }
+__global__ void k_readsum(const float4 *p, size_t n, float *out) {
+  float a = 0.f;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+    float4 v = __ldcs(p + i); a += v.x + v.y + v.z + v.w;
+  }
+  if (a == 12345.f) out[0] = a;
+}
 __global__ void k_load(const int4 *__restrict__ l, double *out) {
   int4 v = __ldg(l + blockIdx.x * blockDim.x + threadIdx.x);
   if (v.x == 12345) out[0] = v.y;
@@ -27,13 +34,15 @@ int main() {
   cudaGraphInstantiate(&ge, gr, 0);
   const char *names[] = {"empty_after_memset", "big_params_after_memset", "one_ldg_after_memset",
                          "empty_after_fill_kernel", "empty_no_flush", "graph_empty_after_fill_kernel",
-                         "fill_kernel_itself"};
-  for (int mode = 3; mode < 7; ++mode) {
+                         "fill_kernel_itself", "empty_after_fill_then_read"};
+  float *fl2; cudaMalloc(&fl2, fb);
+  for (int mode = 3; mode < 8; ++mode) {
     float tot = 0; int K = 200;
     for (int it = 0; it < K + 10; ++it) {
       if (mode != 4 && mode != 6) k_fill<<<148 * 8, 256, 0, st>>>(fl, fb / 4);
+      if (mode == 7) k_readsum<<<148 * 8, 256, 0, st>>>((const float4 *)fl2, fb / 16, (float *)d);
       cudaEventRecord(a, st);
-      if (mode == 3 || mode == 4) k_empty<<<592, 128, 0, st>>>(d);
+      if (mode == 3 || mode == 4 || mode == 7) k_empty<<<592, 128, 0, st>>>(d);
       else if (mode == 5) cudaGraphLaunch(ge, st);
       else k_fill<<<148 * 8, 256, 0, st>>>(fl, fb / 4);
       cudaEventRecord(b, st);
@@ -57,6 +66,21 @@ int main() {
       if (it >= 10) tot += ms;
     }
     printf("{\"mode\": \"%s\", \"us\": %.2f}\n", names[mode], 1e3 * tot / K);
+  }
+  // grid shape of the same resident thread count: 592x128 vs 296x256 vs 148x512
+  const int shp[4][2] = {{592, 128}, {296, 256}, {148, 512}, {148, 128}};
+  for (int m = 0; m < 4; ++m) {
+    float tot = 0; int K = 200;
+    for (int it = 0; it < K + 10; ++it) {
+      k_fill<<<148 * 8, 256, 0, st>>>(fl, fb / 4);
+      cudaEventRecord(a, st);
+      k_empty<<<shp[m][0], shp[m][1], 0, st>>>(d);
+      cudaEventRecord(b, st);
+      cudaEventSynchronize(b);
+      float ms; cudaEventElapsedTime(&ms, a, b);
+      if (it >= 10) tot += ms;
+    }
+    printf("{\"mode\": \"empty_%dx%d_after_fill\", \"us\": %.2f}\n", shp[m][0], shp[m][1], 1e3 * tot / K);
   }
   return 0;
 }
