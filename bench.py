@@ -278,7 +278,7 @@ def gpu_arm_decomposed(args):
     # the whole decomposed step (halo P2P, Tersoff kernel + finalize, reverse
     # forces, all-reduce) as one CUDA graph: NCCL ops are capturable
     # (tools/nccl_capture_probe.py); any capture error falls back to eager
-    launch = "eager (Python host loop, NCCL batch_isend_irecv)"
+    launch = f"eager (Python host loop, {backend} batch_isend_irecv)"
     graph = None
     step_fn = lambda: ff(dom)  # noqa: E731
     if backend == "nccl" and os.environ.get("BENCH_DD_GRAPH", "1") == "1":
@@ -384,7 +384,8 @@ def gpu_arm_decomposed(args):
         "dtype": "f64" if args.precision == "double" else "f32/f64", "data": "synthetic",
         "config": {"workload": f"config 2 per GPU, weak scaling: {cells[0]}x{cells[1]}x{cells[2]}"
                                f"-cell Si diamond ({n_total} atoms), slab decomposition along x, "
-                               f"NCCL P2P halo + reverse forces + all-reduce per step",
+                               f"{backend.upper()} P2P halo + reverse forces + all-reduce per step",
+                   "backend": backend,
                    "atoms": n_total, "atoms_per_gpu": n_total // ws,
                    "precision": args.precision, "scatter": args.scatter,
                    "parallelism": f"spatial slabs x{ws}",
