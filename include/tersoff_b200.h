@@ -120,6 +120,11 @@ int tb_build_neighbors_owned(tb_context *ctx, tb_nlist *nl, int64_t n, int64_t n
                              const double *positions, const double *box,
                              const int32_t *periodic, double r_cut, double skin);
 
+/* Forget the species-pair compute filter (multi-species tables): the next
+ * evaluation derives it again from the species it is given.  Needed only
+ * after changing a device species array in place (see tb_compute_device). */
+int tb_nlist_refilter(tb_context *ctx, tb_nlist *nl);
+
 /* number of list entries (sum of row lengths) and the longest row */
 int tb_nlist_info(const tb_nlist *nl, int64_t *n_atoms, int64_t *n_entries,
                   int64_t *max_row);
@@ -153,9 +158,13 @@ int tb_compute(tb_context *ctx, const tb_nlist *nl, const double *positions,
  * [energy, virial(6)] as 7 doubles; `dstats` TB_NSTATS uint64 (may be NULL).
  * Does not synchronise; validation errors are latched on the device and
  * reported by the next tb_check_errors().  With two or more species the
- * first call after a build derives a species-pair compute filter from
- * d_species (one host synchronisation); the species array must not change
- * in place while the list is in use (pass a different pointer instead). */
+ * first call after a build (or after tb_set_params, or with a different
+ * species pointer) derives a species-pair compute filter from d_species (one
+ * host synchronisation).  Species changed IN PLACE afterwards are detected on
+ * the device (a copy of the filter's species is compared every evaluation):
+ * tb_compute then rebuilds the filter and re-evaluates; here the next
+ * tb_check_errors() returns TB_ERR_INPUT -- call tb_nlist_refilter (or
+ * rebuild the list) and evaluate again. */
 int tb_compute_device(tb_context *ctx, const tb_nlist *nl, const double *d_positions,
                       const int32_t *d_species, double r_cut, int precision, int scatter,
                       double *d_forces, double *d_per_atom, double *d_result,

@@ -56,6 +56,7 @@ SIGNATURES = {
                        _P, _P, _P]),
     "tb_nlist_rebuild_device": (_I, [_P, _P, _P, _P, _I]),
     "tb_nlist_lanes": (_I, [_P, _P, _P]),
+    "tb_nlist_refilter": (_I, [_P, _P]),
     "tb_profile": (_I, [_P, _I]),
     "tb_profile_read": (_I, [_P, _P, _P]),
     "tb_measure_peak": (_I, [_P, _I, ctypes.POINTER(_D)]),

@@ -92,7 +92,6 @@ struct tb_context {
   unsigned long long *fin_err_dst = nullptr;
   cudaEvent_t ev_kernel_done = nullptr;
   cudaStream_t side = nullptr;
-  std::vector<int> last_species;  // host species of the last tb_compute (filter validity)
   const int *dplan = nullptr;  // tb_md_run capture: device {nchunks, n_empty}
   bool md_fuse = false;  // tb_md_run capture (atomic): finalize folded into the kick kernels
   int last_blocks = 0;  // grid of the last Tersoff launch (partials to reduce)  // tb_set_option(TB_OPT_TILE_KERNEL): general tile kernel only
@@ -114,6 +113,9 @@ struct tb_nlist {
   DevBuf fbuf;                           // gather mode: per-entry force pieces
   bool fbuf_zero = false;                // entries without lanes hold zeros
   const int *filter_species = nullptr;   // species array the filter was built for
+  int filter_param_version = -1;         // tb_set_params version the filter was built for
+  DevBuf fspecies;                       // copy of the species the filter was built for
+  std::vector<int> host_species;         // host species last staged for this list
   bool rev_valid = false;
   int nchunks = 0;  // > 0: warp-chunk fast path available (max_row <= 32)
   int n_empty = 0;  // atoms with empty rows: sorted_atoms[0, n_empty)
@@ -140,6 +142,8 @@ struct MdKey {
   const void *ptr[40];
   int64_t n, ecap, ccap, ncell;
   double dt, accel, skin, r_cut;
+  double L[3], width[3], origin[3];  // the graph bakes the box and cell grid in by value
+  int per[3], nc[3], stencil_image;
   int rebuild_every, precision, scatter, record_every, param_version, filtered, S, tile;
   double loose;
 };
@@ -479,7 +483,8 @@ extern "C" void tb_nlist_destroy(tb_nlist *nl) {
                     &nl->maxrow, &nl->nl_row, &nl->sorted_atoms, &nl->sort_keys,
                     &nl->iota, &nl->lanes, &nl->hist, &nl->cpos, &nl->crow, &nl->coff,
                     &nl->centry, &nl->fnbr, &nl->fbuf, &nl->plan, &nl->scratch, &nl->lplan,
-                    &nl->llen, &nl->lrow, &nl->lrowj, &nl->lsorted, &nl->llanes, &nl->ref_log};
+                    &nl->llen, &nl->lrow, &nl->lrowj, &nl->lsorted, &nl->llanes, &nl->ref_log,
+                    &nl->fspecies};
   for (DevBuf *b : bufs) b->release();
   md_graph_release(nl);
   delete nl;
@@ -603,8 +608,12 @@ static int build_filter(tb_context *ctx, tb_nlist *nl, const int *d_species) {
   memcpy(hist, hm, sizeof(hist));
   rc = build_chunks(ctx, nl, nl->crow.as<int>(), nl->coff.as<int>(), nl->centry.as<int>(), hist);
   if (rc) return rc;
+  CK(nl->fspecies.ensure(sizeof(int) * std::max(N, 1)));
+  CK(cudaMemcpyAsync(nl->fspecies.p, d_species, sizeof(int) * N, cudaMemcpyDeviceToDevice,
+                     ctx->stream));
   nl->filtered = true;
   nl->filter_species = d_species;
+  nl->filter_param_version = ctx->param_version;
   nl->fbuf_zero = false;
   return TB_OK;
 }
@@ -802,6 +811,12 @@ extern "C" int tb_build_neighbors_owned(tb_context *ctx, tb_nlist *nl, int64_t n
     nl->n_empty = 0;
   }
   nl->built = true;
+  return TB_OK;
+}
+
+extern "C" int tb_nlist_refilter(tb_context *ctx, tb_nlist *nl) {
+  if (!ctx || !nl) return fail(ctx, TB_ERR_ARG, "null argument");
+  nl->filtered = false;  // rebuilt for the current species at the next evaluation
   return TB_OK;
 }
 
@@ -1013,7 +1028,7 @@ static ErrFlags err_init() {
   e.bad_species_atom = INT_MAX;
   e.coinc_key = ~0ull;
   e.overflow = 0;
-  e.pad = 0;
+  e.stale_filter = 0;
   return e;
 }
 
@@ -1115,11 +1130,19 @@ static int enqueue_compute(tb_context *ctx, const tb_nlist *nl, const double *d_
   // warp-chunk kernel for rows <= 32 entries and <= 2 species; else the tile kernel
   const bool warp_path = nl->nchunks > 0 && !ctx->force_tile && ctx->S <= 2;
   if (warp_path && ctx->S > 1 && !ctx->no_filter &&
-      (!nl->filtered || nl->filter_species != d_species)) {
+      (!nl->filtered || nl->filter_species != d_species ||
+       nl->filter_param_version != ctx->param_version)) {
     int rc = build_filter(ctx, const_cast<tb_nlist *>(nl), d_species);
     if (rc) return rc;
   }
   const bool filtered = warp_path && nl->filtered;
+  if (filtered && !ctx->dplan && n > 0) {
+    // same pointer, changed contents: latch stale_filter (tb_compute rebuilds
+    // the filter and re-evaluates; tb_check_errors reports it)
+    k_species_guard<<<std::min(nblk(n, 256), 2 * 148), 256, 0, ctx->stream>>>(
+        n, d_species, nl->fspecies.as<int>(), ctx->errf.as<ErrFlags>());
+    CK(cudaGetLastError());
+  }
   if (scatter == TB_SCATTER_GATHER && filtered && !nl->fbuf_zero) {
     // entries the filter gave no lane are never written: zero them once per build
     CK(cudaMemsetAsync(nl->fbuf.p, 0, sizeof(double) * 3 * std::max<int64_t>(nl->entries, 1),
@@ -1238,6 +1261,10 @@ static int report_errors(tb_context *ctx, const tb_nlist *nl, const double *d_po
   int rc = TB_OK;
   if (e.overflow) {
     rc = fail(ctx, TB_ERR_CUDA, "internal error: tile staging overflow");
+  } else if (e.stale_filter) {
+    rc = fail(ctx, TB_ERR_INPUT,
+              "species changed since the neighbour list's species filter was built; "
+              "rebuild the list (tb_build_neighbors) or call tb_nlist_refilter");
   } else if (e.nonfinite_atom != INT_MAX) {
     // kernels.py:111-116
     rc = fail(ctx, TB_ERR_INPUT, "non-finite position for atom %d", e.nonfinite_atom);
@@ -1291,12 +1318,14 @@ extern "C" int tb_compute(tb_context *ctx, const tb_nlist *nl, const double *pos
   const int *d_sp = stage_in(ctx, species, (size_t)n, ctx->species, rc);
   if (rc) return rc;
   if (sp_host && ctx->S > 1) {
-    // host species go through one staging buffer: a content change must
-    // invalidate the species-pair compute filter built for the old values
-    if (ctx->last_species.size() != (size_t)n ||
-        memcmp(ctx->last_species.data(), species, sizeof(int) * n) != 0) {
-      ctx->last_species.assign(species, species + n);
-      const_cast<tb_nlist *>(nl)->filtered = false;
+    // host species go through one staging buffer: a content change (checked
+    // per list) invalidates the species-pair compute filter built for the old
+    // values (the device guard below catches in-place device changes)
+    tb_nlist *nlm = const_cast<tb_nlist *>(nl);
+    if (nlm->host_species.size() != (size_t)n ||
+        memcmp(nlm->host_species.data(), species, sizeof(int) * n) != 0) {
+      nlm->host_species.assign(species, species + n);
+      nlm->filtered = false;
     }
   }
   if (n == 0) {  // validation only (parameters, list, cutoff); empty results
@@ -1339,6 +1368,8 @@ extern "C" int tb_compute(tb_context *ctx, const tb_nlist *nl, const double *pos
     CK(cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking));
     CK(cudaEventCreateWithFlags(&ctx->ev_kernel_done, cudaEventDisableTiming));
   }
+  bool retried_stale = false;
+evaluate:
   ctx->fin_err_dst = reinterpret_cast<unsigned long long *>(hd);
   cudaEvent_t keep_ev = ctx->ev_kernel_done;
   if (!pa_async) ctx->ev_kernel_done = nullptr;
@@ -1362,6 +1393,15 @@ extern "C" int tb_compute(tb_context *ctx, const tb_nlist *nl, const double *pos
   if (pa_async) CK(spin_sync(ctx->side));
   ctx->err_unchecked = false;
   memcpy(ctx->h_err, h, sizeof(ErrFlags));
+  if (ctx->h_err->stale_filter && !retried_stale) {
+    // device species changed in place since the filter was built: rebuild it
+    // for the current species and evaluate again
+    const_cast<tb_nlist *>(nl)->filtered = false;
+    rc = reset_errors(ctx);
+    if (rc) return rc;
+    retried_stale = true;
+    goto evaluate;
+  }
   rc = report_errors(ctx, nl, d_pos, d_sp);
   if (rc) return rc;
   const double *hr = reinterpret_cast<const double *>(h + 64);
@@ -1400,6 +1440,10 @@ extern "C" int tb_check_errors(tb_context *ctx) {
   ErrFlags e = *ctx->h_err;
   int rc = TB_OK;
   if (e.overflow) rc = fail(ctx, TB_ERR_CUDA, "internal error: tile staging overflow");
+  else if (e.stale_filter)
+    rc = fail(ctx, TB_ERR_INPUT,
+              "species changed since the neighbour list's species filter was built; "
+              "rebuild the list (tb_build_neighbors) or call tb_nlist_refilter");
   else if (e.nonfinite_atom != INT_MAX)
     rc = fail(ctx, TB_ERR_INPUT, "non-finite position for atom %d", e.nonfinite_atom);
   else if (e.bad_species_atom != INT_MAX)
@@ -1607,6 +1651,14 @@ static MdKey md_key(const tb_context *ctx, const tb_nlist *nl, const MdArgs &m) 
   k.ecap = nl->ecap;
   k.ccap = nl->ccap;
   k.ncell = nl->ncell;
+  for (int ax = 0; ax < 3; ++ax) {
+    k.L[ax] = nl->L[ax];
+    k.per[ax] = nl->per[ax];
+    k.width[ax] = nl->grid.width[ax];
+    k.origin[ax] = nl->grid.origin[ax];
+    k.nc[ax] = nl->grid.nc[ax];
+  }
+  k.stencil_image = nl->grid.stencil_image;
   k.dt = m.dt;
   k.accel = m.accel;
   k.skin = m.skin;
@@ -1739,7 +1791,8 @@ static int md_capture(tb_context *ctx, tb_nlist *nl, const MdArgs &m, MdGraph *G
 static int md_prepare(tb_context *ctx, tb_nlist *nl, const int *d_species, int scatter) {
   const int N = (int)nl->n;
   const bool filter_wanted = ctx->S > 1 && !ctx->no_filter;
-  if (filter_wanted && (!nl->filtered || nl->filter_species != d_species)) {
+  if (filter_wanted && (!nl->filtered || nl->filter_species != d_species ||
+                        nl->filter_param_version != ctx->param_version)) {
     int rc = build_filter(ctx, nl, d_species);
     if (rc) return rc;
   }
@@ -1820,13 +1873,17 @@ extern "C" int tb_md_run(tb_context *ctx, tb_nlist *nl, int64_t n, double *d_pos
   // re-tests r < r_cut on a list that holds all such pairs.
   const bool loose = ctx->md_loose > 0 && ctx->S == 1 && scatter == TB_SCATTER_ATOMIC;
   const double skin_list = loose ? skin + ctx->md_loose : skin;
-  CK(ctx->snap.ensure(sizeof(double) * (loose ? 12 : 9) * (size_t)N + sizeof(double)));
+  // snapshot: x, v, F, E of the entry state and the entry list's reference
+  // positions (every failing exit rebuilds that exact list: the in-graph
+  // rebuilds may have left the list at a later trajectory point)
+  CK(ctx->snap.ensure(sizeof(double) * 12 * (size_t)N + sizeof(double)));
   double *snap = ctx->snap.as<double>();
+  double *snap_ref = snap + 9 * N + 1;
+  CK(cudaMemcpyAsync(snap_ref, nl->ref_pos.p, sizeof(double) * 3 * N, cudaMemcpyDeviceToDevice,
+                     ctx->stream));
   if (loose) {
     CK(nl->ref_log.ensure(sizeof(double) * 3 * (size_t)N));
     CK(cudaMemcpyAsync(nl->ref_log.p, nl->ref_pos.p, sizeof(double) * 3 * N,
-                       cudaMemcpyDeviceToDevice, ctx->stream));
-    CK(cudaMemcpyAsync(snap + 9 * N + 1, nl->ref_pos.p, sizeof(double) * 3 * N,
                        cudaMemcpyDeviceToDevice, ctx->stream));
     int rc = tb_build_neighbors(ctx, nl, n, d_positions, nl->L, nl->per, r_cut, skin_list);
     if (rc) return rc;
@@ -1842,6 +1899,15 @@ extern "C" int tb_md_run(tb_context *ctx, tb_nlist *nl, int64_t n, double *d_pos
     if (!loose) return rc;
     int rc2 = tb_build_neighbors(ctx, nl, n, nl->ref_log.as<double>(), nl->L, nl->per, r_cut, skin);
     return rc ? rc : rc2;
+  };
+  // failing exit after a graph launch (non-loose): the list back at its entry
+  // state, so a per-step fallback (tb_md_step) sees consistent lanes and drift
+  auto fail_restore = [&](int rc) -> int {
+    if (loose) return finish(rc);
+    const double *ref = snap_ref;
+    int rc2 = tb_build_neighbors(ctx, nl, n, ref, nl->L, nl->per, r_cut, skin);
+    if (rc2) nl->built = false;
+    return rc;
   };
   CK(cudaMemcpyAsync(snap, d_positions, sizeof(double) * 3 * N, cudaMemcpyDeviceToDevice, ctx->stream));
   CK(cudaMemcpyAsync(snap + 3 * N, d_velocities, sizeof(double) * 3 * N, cudaMemcpyDeviceToDevice, ctx->stream));
@@ -1892,19 +1958,19 @@ extern "C" int tb_md_run(tb_context *ctx, tb_nlist *nl, int64_t n, double *d_pos
     CK(cudaMemcpyAsync(d_forces, snap + 6 * N, sizeof(double) * 3 * N, cudaMemcpyDeviceToDevice, ctx->stream));
     CK(cudaMemcpyAsync(d_result, snap + 9 * N, sizeof(double), cudaMemcpyDeviceToDevice, ctx->stream));
     if (loose)
-      CK(cudaMemcpyAsync(nl->ref_log.p, snap + 9 * N + 1, sizeof(double) * 3 * N,
+      CK(cudaMemcpyAsync(nl->ref_log.p, snap_ref, sizeof(double) * 3 * N,
                          cudaMemcpyDeviceToDevice, ctx->stream));
     if ((hp.overflow & OVF_ROW) || attempt >= 3)
-      return finish(fail(ctx, TB_ERR_UNSUPPORTED,
-                         "device-resident loop: neighbour rows outgrew the warp kernel (overflow %d)",
-                         hp.overflow));
+      return fail_restore(fail(ctx, TB_ERR_UNSUPPORTED,
+                               "device-resident loop: neighbour rows outgrew the warp kernel "
+                               "(overflow %d)", hp.overflow));
     nl->margin = std::max(2.0 * nl->margin, 0.25);
     int rc = tb_build_neighbors(ctx, nl, n, d_positions, nl->L, nl->per, r_cut, skin_list);
     if (rc) return finish(rc);
     nl->filtered = false;
     extra += 1;
     if (nl->nchunks <= 0)
-      return finish(fail(ctx, TB_ERR_UNSUPPORTED, "device-resident loop: rows exceed 32 entries"));
+      return fail_restore(fail(ctx, TB_ERR_UNSUPPORTED, "device-resident loop: rows exceed 32 entries"));
   }
 }
 

@@ -3,11 +3,15 @@
 // are evaluated with Estrin's scheme (dependency depth ~log2(degree) instead of
 // Horner's ~degree), and there are no special-case branches.
 //
-// Domains (all the pair term ever feeds them; documented in DESIGN.md):
-//   tb_exp(x):    finite x in [-708, 709]         (exp(-lam r), exp(eta log t), ...)
-//   tb_log(x):    finite normal x > 0              (log(beta zeta), zeta >= 1e-30)
+// Fast domains (the built-in tables never leave them):
+//   tb_exp(x):    x in [-708, 709]                 (exp(-lam r), exp(eta log t), ...)
+//   tb_log(x):    normal finite x > 0              (log(beta zeta), zeta >= 1e-30)
 //   tb_log1p(u):  finite u >= 0                    (log(1 + (beta zeta)^eta))
 //   tb_rcp(y):    1e-30 < |y| < 1e30 (float-representable seed)
+// tb_exp / tb_log / tb_rcp_guarded fall back to libm / IEEE division outside
+// them (any valid .tersoff table may get there: a large eta at a tiny zeta
+// puts eta log(beta zeta) below -708), so the result is always the library
+// value; each guard is one compare + a branch never taken on the fast domain.
 // Accuracy (checked on the host against libm over the domains by
 // tests/test_fastmath.py): <= 2 ulp.
 //
@@ -71,6 +75,7 @@ static const double tbfm_kh[] = {TBFM_KLIST};
 // exp(x): x = k ln2 + r, |r| <= ln2/2; exp(r) by its degree-12 Taylor
 // polynomial (truncation < 2e-17 relative) in Estrin form; 2^k by exponent bits.
 TBFM_QUAL double tb_exp(double x) {
+  if (!(x >= -708.0 && x <= 709.0)) return exp(x);  // out of the fast domain, NaN: libm
   const double L2E = TBK(TBK_L2E);
   const double LN2HI = TBK(TBK_LN2HI);
   const double LN2LO = TBK(TBK_LN2LO);
@@ -105,6 +110,7 @@ TBFM_QUAL double tb_exp(double x) {
 // R by its degree-7 polynomial in z = s^2 (fdlibm coefficients) in Estrin form.
 TBFM_QUAL double tb_rcp(double y);
 TBFM_QUAL double tb_log(double x) {
+  if (!(x >= 2.2250738585072014e-308 && x <= 1.7976931348623157e308)) return log(x);  // libm
   uint64_t u = tbfm_bits(x);
   int e = (int)((u >> 52) & 0x7ff) - 1023;
   // mantissa in [1, 2); move to [sqrt(1/2), sqrt(2)) (compare on the high word)
@@ -149,6 +155,13 @@ TBFM_QUAL double tb_rcp(double y) {
   r = fma(r, e, r);
   e = fma(-y, r, 1.0);
   return fma(r, e, r);
+}
+
+// 1/y on any y: the fast path inside 1e-30 < |y| < 1e30, IEEE division outside
+TBFM_QUAL double tb_rcp_guarded(double y) {
+  const double a = fabs(y);
+  if (!(a > 1e-30 && a < 1e30)) return 1.0 / y;
+  return tb_rcp(y);
 }
 
 // r = sqrt(x) and 1/r together (the displacement norm and the unit-vector

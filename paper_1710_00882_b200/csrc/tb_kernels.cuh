@@ -34,7 +34,7 @@ struct ErrFlags {
   int bad_species_atom; // atomicMin, INT_MAX = none
   unsigned long long coinc_key;  // (r2 hi32 << 32) | entry, ~0 = none
   int overflow;         // tile staging overflow (internal error)
-  int pad;
+  int stale_filter;     // species differ from those the species-pair filter was built for
 };
 
 // ---------------------------------------------------------------------------
@@ -629,6 +629,18 @@ __global__ void k_export_i64(int m, const int *__restrict__ in, int64_t *__restr
 // ---------------------------------------------------------------------------
 // K3: skin/2 trigger (neighbor.py:220-229)
 // ---------------------------------------------------------------------------
+
+// Species guard of the species-pair compute filter: the filter decides which
+// entries get warp lanes from the species it was built for; species changed
+// since (in place, same pointer) latch stale_filter instead of silently
+// dropping live pairs.  4 B/atom read, coalesced.
+__global__ void k_species_guard(int n, const int *__restrict__ species,
+                                const int *__restrict__ built_for, ErrFlags *__restrict__ err) {
+  bool diff = false;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    diff |= __ldg(species + i) != __ldg(built_for + i);
+  if (__any_sync(0xffffffffu, diff) && (threadIdx.x & 31) == 0) err->stale_filter = 1;
+}
 
 __global__ void k_max_drift(int n, const double *__restrict__ pos, const double *__restrict__ ref,
                             Box box, unsigned long long *__restrict__ out) {

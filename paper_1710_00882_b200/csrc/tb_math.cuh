@@ -70,6 +70,9 @@ __device__ __forceinline__ float t_rcp(float x) {
   asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
   return r;
 }
+// 1/x for an unbounded x (zeta (1 + (beta zeta)^eta) of an arbitrary table)
+__device__ __forceinline__ double t_rcp_any(double x) { return tb_rcp_guarded(x); }
+__device__ __forceinline__ float t_rcp_any(float x) { return t_rcp(x); }
 
 // f_C and dF_C/dr with inclusive exact plateaus (potential.py:167-175).
 // Returns false when r >= R + D (exactly zero contribution).
@@ -138,7 +141,7 @@ __device__ __forceinline__ void pair_part_fc(T r, T zeta, const PairP<T> &p, T f
     const T lt = t_log(t);
     const T u = t_exp(p.eta * lt);
     const T w = T(1) + u;
-    const T rzw = t_rcp(zeta * w);
+    const T rzw = t_rcp_any(zeta * w);
     // log1p(u) = log(w) + (u - (w - 1)) / w, w = fl(1 + u)
     const T l1p = t_log(w) + (u - (w - T(1))) * (zeta * rzw);
     b = t_exp(p.neg_half_inv_eta * l1p);

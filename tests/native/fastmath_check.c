@@ -38,7 +38,17 @@ int main(int argc, char **argv) {
     e = ulp_err(sq, sqrt(q)); if (e > msq) msq = e;
     e = ulp_err(rs, 1.0 / sqrt(q)); if (e > mrs) mrs = e;
   }
-  printf("{\"exp_ulp\": %.3f, \"log_ulp\": %.3f, \"log1p_ulp\": %.3f, \"rcp_ulp\": %.3f, "
+  /* out of the fast domains: the guarded fallbacks must return the libm value */
+  int ood_ok = 1;
+  const double xs_ood[] = {-708.5, -720.0, -745.0, -745.2, -800.0, -1e300, 709.9, 710.0, 1e300};
+  for (int q = 0; q < 9; ++q) ood_ok &= tb_exp(xs_ood[q]) == exp(xs_ood[q]);
+  const double ys_ood[] = {1e-310, 4.9e-324, 0.0, 1e308 * 10.0};
+  for (int q = 0; q < 4; ++q) ood_ok &= tb_log(ys_ood[q]) == log(ys_ood[q]);
+  const double zs_ood[] = {1e-31, 1e31, 1e300, -1e40, 1e-300};
+  for (int q = 0; q < 5; ++q) ood_ok &= tb_rcp_guarded(zs_ood[q]) == 1.0 / zs_ood[q];
+  ood_ok &= isnan(tb_exp(NAN)) && isnan(tb_log(-1.0));
+  printf("{\"ood_ok\": %d, ", ood_ok);
+  printf("\"exp_ulp\": %.3f, \"log_ulp\": %.3f, \"log1p_ulp\": %.3f, \"rcp_ulp\": %.3f, "
          "\"sqrt_ulp\": %.3f, \"rsqrt_ulp\": %.3f, \"n\": %ld}\n", me, ml, m1, mr, msq, mrs, n);
   return 0;
 }

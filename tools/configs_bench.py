@@ -13,12 +13,13 @@ import bench
 
 cfgs = [int(c) for c in os.environ.get("CB_CONFIGS", "1,2,3,4,5").split(",")]
 steps = int(os.environ.get("CB_STEPS", "100"))
+scat = int(os.environ.get("CB_SCATTER", "0"))  # 0 atomic, 1 gather
 s = torch.cuda.Stream(); torch.cuda.set_stream(s)
 ctx = _native.default_context(0); ctx.set_stream(s.cuda_stream)
 peak64 = bench.measure_peak(ctx.lib, ctx, 0)["tflops"]
 peak32 = bench.measure_peak(ctx.lib, ctx, 1)["tflops"]
 flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")
-out = {"peaks_tflops": {"fp64": peak64, "fp32": peak32}, "configs": {}}
+out = {"peaks_tflops": {"fp64": peak64, "fp32": peak32}, "scatter": ["atomic", "gather"][scat], "configs": {}}
 for cfg in cfgs:
     t0 = time.time()
     st, tn = structures.config(cfg)
@@ -39,7 +40,7 @@ for cfg in cfgs:
            "nl_build_ms": nl_ms, "generate_s": gen_s}
     for prec in (0, 1):
         def step(with_stats=False):
-            ctx.check(ctx.lib.tb_compute_device(ctx.handle, nl._nl.handle, P(pos), P(sp), float(t.r_cut), prec, 0,
+            ctx.check(ctx.lib.tb_compute_device(ctx.handle, nl._nl.handle, P(pos), P(sp), float(t.r_cut), prec, scat,
                                                 P(f), None, P(res), P(stt) if with_stats else None))
         step(True); torch.cuda.synchronize()
         cnt = stt.cpu().numpy()
@@ -74,7 +75,7 @@ for cfg in cfgs:
     print(json.dumps({cfg: rec}), flush=True)
     del pos, sp, f, nl
     torch.cuda.empty_cache()
-if 2 in cfgs:
+if 2 in cfgs and os.environ.get("CB_MD", "1") == "1":
     st, tn = structures.config(2)
     t = B.builtin_params(tn)
     for prec in ("double", "single"):
