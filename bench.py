@@ -637,7 +637,7 @@ def md_measure(B, _native, ctx, state, table, dev, precision, scat, steps=1000, 
     import ctypes
 
     import torch
-    from paper_1710_00882_b200.system import ACCEL
+    from paper_1710_00882_b200.state import ACCEL
     n = state.natoms
     d = torch.device("cuda", dev)
     pos = torch.from_numpy(state.positions.copy()).to(d)

@@ -120,6 +120,20 @@ int tb_build_neighbors_owned(tb_context *ctx, tb_nlist *nl, int64_t n, int64_t n
                              const double *positions, const double *box,
                              const int32_t *periodic, double r_cut, double skin);
 
+/* Import a neighbour list built elsewhere -- the reference's NeighborList
+ * (neighbor.py:170-191: offsets[n+1] / neighbors int64 CSR, its
+ * reference_positions snapshot, build r_cut and skin) -- so the reference's
+ * own ForceField / run_nve / verify suites evaluate on the B200 kernels
+ * without rebuilding their list.  Rows are used as given
+ * (the evaluation re-tests r < r_cut at the current positions, as
+ * pack_adjacency does); tb_needs_rebuild works against ref_positions.
+ * Host or device pointers.  Imported lists have no cell grid, so
+ * tb_nlist_rebuild_device / tb_md_run return TB_ERR_UNSUPPORTED for them
+ * (tb_build_neighbors replaces them with a native list). */
+int tb_nlist_import(tb_context *ctx, tb_nlist *nl, int64_t n, const int64_t *offsets,
+                    const int64_t *neighbors, const double *ref_positions, const double *box,
+                    const int32_t *periodic, double r_cut, double skin);
+
 /* Forget the species-pair compute filter (multi-species tables): the next
  * evaluation derives it again from the species it is given.  Needed only
  * after changing a device species array in place (see tb_compute_device). */
@@ -227,6 +241,93 @@ int tb_md_run(tb_context *ctx, tb_nlist *nl, int64_t n, double *d_positions,
               const int32_t *d_species, double dt, double accel, double r_cut, double skin,
               int rebuild_every, int precision, int scatter, int64_t steps, int record_every,
               double *d_series, double *d_result, int64_t *rebuilds);
+
+/* ---- slab domain decomposition (north_star (4)) --------
+ *
+ * The reference has no decomposition; these entries replace no
+ * reference symbol -- they split the evaluation / NVE run above over ranks
+ * (one process per GPU) with results equal to the single-domain ones.  Each
+ * rank owns a slab of whole x cell columns of the neighbour grid (>= 2 per
+ * rank); ghosts are the atoms of the one column beyond each face (width >=
+ * r_cut + skin), kept at unshifted coordinates so every displacement and pair
+ * set equals the single-domain one; only owned atoms get list rows, so every
+ * energy term is evaluated exactly once, and forces landing on ghosts are
+ * returned to their owners (reverse halo).
+ *
+ * The caller owns the transport (NCCL / gloo P2P).  Message rows are float64,
+ * laid out [to-left | to-right] in the SEND buffer; incoming rows go to
+ * [from-left | from-right] of the RECV buffer (tb_dd_recv_buffer), or -- for
+ * the forward position halo -- straight into the ghost rows of POS.
+ *   rebuild:  tb_dd_migrate_pack -> send 9-double rows, exchange counts ->
+ *             tb_dd_recv_buffer -> recv -> tb_dd_migrate_unpack;
+ *             tb_dd_halo_pack -> send 2-double [id, species] rows ->
+ *             tb_dd_recv_buffer -> recv -> tb_dd_halo_unpack;
+ *             tb_dd_pack_positions -> positions halo -> tb_dd_build
+ *   evaluate: tb_dd_pack_positions -> positions halo (SEND -> ghost rows of
+ *             POS) -> tb_dd_compute -> ghost rows of FORCES to the
+ *             neighbours, theirs into RECV -> tb_dd_reverse_add -> sum the
+ *             [E, W6] result over ranks
+ *   NVE step: tb_dd_kick_drift (max drift^2 over ranks decides the rebuild:
+ *             skin/2 trigger, neighbor.py:220-229) -> [rebuild] -> evaluate
+ *             -> tb_dd_kick (E_kin in result[7], summed over ranks). */
+typedef struct tb_domain tb_domain;
+#define TB_DD_POS 0     /* (n_owned + ghosts, 3) float64 */
+#define TB_DD_VEL 1     /* (n_owned, 3) float64 */
+#define TB_DD_FORCES 2  /* (n_owned + ghosts, 3) float64 */
+#define TB_DD_MASS 3    /* (n_owned) float64 amu */
+#define TB_DD_SPECIES 4 /* (n_owned + ghosts) int32 */
+#define TB_DD_IDS 5     /* (n_owned + ghosts) int64 global atom ids */
+#define TB_DD_SEND 6    /* message rows to the neighbours */
+#define TB_DD_RECV 7    /* message rows from the neighbours */
+/* rank of nranks; box / periodic as tb_build_neighbors (x must be periodic) */
+int tb_dd_create(tb_context *ctx, int rank, int nranks, const double *box,
+                 const int32_t *periodic, double r_cut, double skin, tb_domain **out);
+void tb_dd_destroy(tb_domain *dd);
+/* this rank's owned atoms (host or device arrays): positions, velocities,
+ * per-atom masses, species, global ids */
+int tb_dd_load(tb_domain *dd, int64_t n, const double *pos, const double *vel,
+               const double *mass, const int32_t *species, const int64_t *ids);
+/* out[10] = n_owned, ghosts from left, ghosts from right, send-left rows,
+ * send-right rows, migrants to left, migrants to right, capacity, first and
+ * last owned column */
+int tb_dd_counts(const tb_domain *dd, int64_t *out);
+/* device pointer of a domain buffer (valid until the next call that may grow
+ * it: tb_dd_load, *_pack, *_unpack, tb_dd_recv_buffer) */
+int tb_dd_buffer(tb_domain *dd, int which, void **ptr);
+/* RECV buffer with room for rows x width doubles */
+int tb_dd_recv_buffer(tb_domain *dd, int64_t rows, int width, void **ptr);
+/* migration at a rebuild: owned atoms whose x column now belongs to the
+ * left / right rank are packed (9 doubles) into SEND; synchronises.
+ * TB_ERR_INPUT if an atom moved farther than one slab. */
+int tb_dd_migrate_pack(tb_domain *dd, int64_t *n_to_left, int64_t *n_to_right);
+/* kept atoms compacted in order, received rows [from-left | from-right]
+ * appended; ghosts cleared */
+int tb_dd_migrate_unpack(tb_domain *dd, int64_t n_from_left, int64_t n_from_right);
+/* halo send lists (owned atoms in the first / last column) and their
+ * [id, species] rows in SEND; synchronises */
+int tb_dd_halo_pack(tb_domain *dd, int64_t *n_send_left, int64_t *n_send_right);
+/* ghost ids / species from RECV; ghost rows follow the owned rows */
+int tb_dd_halo_unpack(tb_domain *dd, int64_t n_ghost_left, int64_t n_ghost_right);
+/* SEND <- positions of the send lists (3 doubles per row); asynchronous */
+int tb_dd_pack_positions(tb_domain *dd);
+/* owned-rows neighbour list over [owned | ghosts] (tb_build_neighbors_owned) */
+int tb_dd_build(tb_domain *dd, tb_nlist *nl);
+/* evaluation over the local atoms: FORCES on [owned | ghosts], d_result =
+ * [E, W6] of the owned rows (device, 7+ doubles), d_stats may be NULL;
+ * asynchronous */
+int tb_dd_compute(tb_domain *dd, const tb_nlist *nl, int precision, int scatter,
+                  double *d_result, uint64_t *d_stats);
+/* FORCES[send lists] += RECV rows (forces the neighbours computed on their
+ * ghosts); asynchronous, deterministic */
+int tb_dd_reverse_add(tb_domain *dd);
+/* v += dt/2 accel F/m, x += dt v, wrap (owned atoms); d_drift2 (device double)
+ * = max min-image drift^2 against nl's build positions; asynchronous */
+int tb_dd_kick_drift(tb_domain *dd, const tb_nlist *nl, double dt, double accel,
+                     double *d_drift2);
+/* v += dt/2 accel F/m (owned) and d_result[7] = this rank's kinetic energy */
+int tb_dd_kick(tb_domain *dd, double dt, double accel, double *d_result);
+/* owned atoms out (host or device pointers, each may be NULL) */
+int tb_dd_export(tb_domain *dd, int64_t *ids, double *pos, double *vel, double *forces);
 
 /* Diagnostic: measured FMA throughput of this GPU in TFLOP/s (2 flops per
  * FMA), precision TB_PREC_DOUBLE -> DFMA, TB_PREC_MIXED -> FFMA; the roofline

@@ -57,6 +57,24 @@ SIGNATURES = {
     "tb_nlist_rebuild_device": (_I, [_P, _P, _P, _P, _I]),
     "tb_nlist_lanes": (_I, [_P, _P, _P]),
     "tb_nlist_refilter": (_I, [_P, _P]),
+    "tb_nlist_import": (_I, [_P, _P, _I64, _P, _P, _P, _P, _P, _D, _D]),
+    "tb_dd_create": (_I, [_P, _I, _I, _P, _P, _D, _D, ctypes.POINTER(_P)]),
+    "tb_dd_destroy": (None, [_P]),
+    "tb_dd_load": (_I, [_P, _I64, _P, _P, _P, _P, _P]),
+    "tb_dd_counts": (_I, [_P, _P]),
+    "tb_dd_buffer": (_I, [_P, _I, ctypes.POINTER(_P)]),
+    "tb_dd_recv_buffer": (_I, [_P, _I64, _I, ctypes.POINTER(_P)]),
+    "tb_dd_migrate_pack": (_I, [_P, ctypes.POINTER(_I64), ctypes.POINTER(_I64)]),
+    "tb_dd_migrate_unpack": (_I, [_P, _I64, _I64]),
+    "tb_dd_halo_pack": (_I, [_P, ctypes.POINTER(_I64), ctypes.POINTER(_I64)]),
+    "tb_dd_halo_unpack": (_I, [_P, _I64, _I64]),
+    "tb_dd_pack_positions": (_I, [_P]),
+    "tb_dd_build": (_I, [_P, _P]),
+    "tb_dd_compute": (_I, [_P, _P, _I, _I, _P, _P]),
+    "tb_dd_reverse_add": (_I, [_P]),
+    "tb_dd_kick_drift": (_I, [_P, _P, _D, _D, _P]),
+    "tb_dd_kick": (_I, [_P, _D, _D, _P]),
+    "tb_dd_export": (_I, [_P, _P, _P, _P, _P]),
     "tb_profile": (_I, [_P, _I]),
     "tb_profile_read": (_I, [_P, _P, _P]),
     "tb_measure_peak": (_I, [_P, _I, ctypes.POINTER(_D)]),

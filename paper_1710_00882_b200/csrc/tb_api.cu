@@ -18,12 +18,12 @@
 #include <string>
 #include <vector>
 
-#include <cub/cub.cuh>
-
 #include "../../include/tersoff_b200.h"
 #include "tb_kernels.cuh"
+#include "tb_scan.cuh"
 #include "tb_warp.cuh"
 #include "tb_dnl.cuh"
+#include "tb_dd.cuh"
 
 #ifndef TB_VERSION_TAG
 #define TB_VERSION_TAG "dev"
@@ -69,7 +69,7 @@ struct tb_context {
   std::vector<double> pair_mat, trip_mat;
   // scratch
   DevBuf pos, species, forces, per_atom, result, stats, partials, errf, drift, bounds,
-      cub_tmp, facc, stats_acc, ke_part, snap;
+      scan_tmp, facc, stats_acc, ke_part, snap;
   cudaStream_t cap[2] = {nullptr, nullptr};  // tb_md_run graph capture
   int64_t facc_n = -1;
   ErrFlags *h_err = nullptr;      // pinned
@@ -134,6 +134,7 @@ struct tb_nlist {
   DevBuf ref_log;  // tb_md_run loose list: positions of the reference's last rebuild
   bool fnbr_ok = false;  // fnbr matches centry (written by every filter pass since)
   int64_t lcap = 0;  // chunk capacity of llanes
+  bool imported = false;  // rows from tb_nlist_import (no cell grid: no device rebuild)
   struct MdGraph *md = nullptr;
 };
 
@@ -325,7 +326,7 @@ extern "C" void tb_destroy(tb_context *ctx) {
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   DevBuf *bufs[] = {&ctx->pos, &ctx->species, &ctx->forces, &ctx->per_atom, &ctx->result,
                     &ctx->stats, &ctx->partials, &ctx->facc, &ctx->stats_acc, &ctx->ke_part, &ctx->errf,
-                    &ctx->drift, &ctx->bounds, &ctx->cub_tmp, &ctx->snap};
+                    &ctx->drift, &ctx->bounds, &ctx->scan_tmp, &ctx->snap};
   for (DevBuf *b : bufs) b->release();
   for (auto *v : {&ctx->ev_used, &ctx->ev_free})
     for (auto &ev : *v) {
@@ -490,11 +491,19 @@ extern "C" void tb_nlist_destroy(tb_nlist *nl) {
   delete nl;
 }
 
+// exclusive prefix sum (tb_scan.cuh); the tile-sum scratch is context-owned
+// and pre-sized by md_prepare before a graph capture
 static int exclusive_scan(tb_context *ctx, const int *in, int *out, int64_t count) {
-  size_t tmp = 0;
-  CK(cub::DeviceScan::ExclusiveSum(nullptr, tmp, in, out, (int)count, ctx->stream));
-  CK(ctx->cub_tmp.ensure(tmp));
-  CK(cub::DeviceScan::ExclusiveSum(ctx->cub_tmp.p, tmp, in, out, (int)count, ctx->stream));
+  CK(ctx->scan_tmp.ensure(sizeof(int) * (scan_tiles(count) + 4)));
+  CK(scan_exclusive(in, out, count, ctx->scan_tmp.as<int>(), ctx->stream));
+  return TB_OK;
+}
+
+// atoms sorted stably by row length into sorted_atoms (tb_scan.cuh)
+static int sort_rows_by_length(tb_context *ctx, tb_nlist *nl, const int *row_len) {
+  CK(ctx->scan_tmp.ensure(sizeof(int) * lsort_scratch((int)nl->n)));
+  CK(sort_by_length(row_len, (int)nl->n, nl->sorted_atoms.as<int>(), ctx->scan_tmp.as<int>(),
+                    ctx->stream));
   return TB_OK;
 }
 
@@ -516,18 +525,8 @@ static int build_chunks(tb_context *ctx, tb_nlist *nl, const int *row_len, const
                         const int *centry, const int *hist) {
   const int N = (int)nl->n;
   CK(nl->sorted_atoms.ensure(sizeof(int) * N));
-  CK(nl->sort_keys.ensure(sizeof(int) * N));
-  CK(nl->iota.ensure(sizeof(int) * N));
-  k_iota<<<nblk(N, 256), 256, 0, ctx->stream>>>(N, nl->iota.as<int>());
-  CK(cudaGetLastError());
-  size_t tmp = 0;
-  CK(cub::DeviceRadixSort::SortPairs(nullptr, tmp, row_len, nl->sort_keys.as<int>(),
-                                     nl->iota.as<int>(), nl->sorted_atoms.as<int>(), N, 0, 6,
-                                     ctx->stream));
-  CK(ctx->cub_tmp.ensure(tmp));
-  CK(cub::DeviceRadixSort::SortPairs(ctx->cub_tmp.p, tmp, row_len, nl->sort_keys.as<int>(),
-                                     nl->iota.as<int>(), nl->sorted_atoms.as<int>(), N, 0, 6,
-                                     ctx->stream));
+  int rcs = sort_rows_by_length(ctx, nl, row_len);  // stable -> deterministic chunks
+  if (rcs) return rcs;
   ChunkPlan plan;
   memset(&plan, 0, sizeof(plan));
   int start = hist[0], chunks = 0;
@@ -658,6 +657,7 @@ extern "C" int tb_build_neighbors_owned(tb_context *ctx, tb_nlist *nl, int64_t n
   nl->skin = skin;
   nl->bc = bc;
   nl->rev_valid = false;
+  nl->imported = false;
 
   // ---- grid geometry (CellList.__init__, neighbor.py:54-81) ----
   Grid g;
@@ -810,6 +810,105 @@ extern "C" int tb_build_neighbors_owned(tb_context *ctx, tb_nlist *nl, int64_t n
     nl->nchunks = 0;
     nl->n_empty = 0;
   }
+  nl->built = true;
+  return TB_OK;
+}
+
+// Import a CSR list built elsewhere (the reference's NeighborList:
+// offsets/neighbors int64, neighbor.py:170-191) so the reference's own callers
+// can run the B200 kernels on their list.  The rows are taken as given (the
+// evaluation re-tests r < r_cut, like pack_adjacency); warp chunks are built
+// from the row lengths.  Imported lists have no cell grid: the device rebuild
+// paths (tb_nlist_rebuild_device, tb_md_run) refuse them.
+extern "C" int tb_nlist_import(tb_context *ctx, tb_nlist *nl, int64_t n, const int64_t *offsets,
+                               const int64_t *neighbors, const double *ref_positions,
+                               const double *box, const int32_t *periodic, double r_cut,
+                               double skin) {
+  if (!ctx || !nl || !offsets || !box || !periodic || (n && !ref_positions))
+    return fail(ctx, TB_ERR_ARG, "null argument");
+  if (n < 0 || n > INT_MAX / 2) return fail(ctx, TB_ERR_ARG, "bad atom count %lld", (long long)n);
+  if (skin < 0) return fail(ctx, TB_ERR_CONFIG, "negative skin %s", fmt_g(skin).c_str());
+  CK(cudaSetDevice(ctx->device));
+  const int N = (int)n;
+  std::vector<int64_t> off(N + 1);
+  if (is_device_ptr(offsets))
+    CK(cudaMemcpy(off.data(), offsets, sizeof(int64_t) * (N + 1), cudaMemcpyDeviceToHost));
+  else
+    memcpy(off.data(), offsets, sizeof(int64_t) * (N + 1));
+  const int64_t m = off[N];
+  if (off[0] != 0 || m < 0 || m > INT_MAX)
+    return fail(ctx, TB_ERR_ARG, "offsets must start at 0 and end at the entry count");
+  std::vector<int> row(N + 1, 0), off32(N + 1, 0);
+  int hist[34] = {0};
+  int64_t max_row = 0;
+  for (int i = 0; i < N; ++i) {
+    const int64_t len = off[i + 1] - off[i];
+    if (len < 0) return fail(ctx, TB_ERR_ARG, "offsets decrease at row %d", i);
+    row[i] = (int)len;
+    off32[i] = (int)off[i];
+    max_row = std::max(max_row, len);
+    if (len <= 32) hist[len] += 1;
+  }
+  off32[N] = (int)m;
+  std::vector<int64_t> nb64(std::max<int64_t>(m, 1));
+  if (m) {
+    if (!neighbors) return fail(ctx, TB_ERR_ARG, "null neighbors");
+    if (is_device_ptr(neighbors))
+      CK(cudaMemcpy(nb64.data(), neighbors, sizeof(int64_t) * m, cudaMemcpyDeviceToHost));
+    else
+      memcpy(nb64.data(), neighbors, sizeof(int64_t) * m);
+  }
+  std::vector<int> nb(std::max<int64_t>(m, 1), 0);
+  for (int64_t e = 0; e < m; ++e) {
+    if (nb64[e] < 0 || nb64[e] >= n)
+      return fail(ctx, TB_ERR_ARG, "neighbour index %lld out of range", (long long)nb64[e]);
+    nb[e] = (int)nb64[e];
+  }
+  md_graph_release(nl);
+  nl->n = n;
+  for (int ax = 0; ax < 3; ++ax) {
+    if (!(box[ax] > 0))
+      return fail(ctx, TB_ERR_CONFIG, "box edge lengths must be positive, got %g", box[ax]);
+    nl->L[ax] = box[ax];
+    nl->per[ax] = periodic[ax] ? 1 : 0;
+  }
+  nl->r_cut = r_cut;
+  nl->skin = skin;
+  nl->bc = r_cut + skin;
+  nl->entries = m;
+  nl->max_row = max_row;
+  nl->margin = 0.0;
+  nl->ecap = std::max<int64_t>(m, 1);
+  nl->ncell = 0;
+  nl->imported = true;
+  nl->rev_valid = false;
+  nl->filtered = false;
+  nl->filter_species = nullptr;
+  nl->fbuf_zero = false;
+  CK(nl->offsets.ensure(sizeof(int) * (N + 1)));
+  CK(nl->row_count.ensure(sizeof(int) * (N + 1)));
+  CK(nl->nbr.ensure(sizeof(int) * nl->ecap));
+  CK(nl->ref_pos.ensure(sizeof(double) * 3 * std::max(N, 1)));
+  CK(nl->hist.ensure(sizeof(int) * 34));
+  CK(cudaMemcpyAsync(nl->offsets.p, off32.data(), sizeof(int) * (N + 1), cudaMemcpyHostToDevice,
+                     ctx->stream));
+  CK(cudaMemcpyAsync(nl->row_count.p, row.data(), sizeof(int) * (N + 1), cudaMemcpyHostToDevice,
+                     ctx->stream));
+  CK(cudaMemcpyAsync(nl->nbr.p, nb.data(), sizeof(int) * std::max<int64_t>(m, 1),
+                     cudaMemcpyHostToDevice, ctx->stream));
+  if (N)
+    CK(cudaMemcpyAsync(nl->ref_pos.p, ref_positions, sizeof(double) * 3 * N,
+                       is_device_ptr(ref_positions) ? cudaMemcpyDeviceToDevice
+                                                    : cudaMemcpyHostToDevice,
+                       ctx->stream));
+  if (max_row <= 32 && N > 0) {
+    int rc = build_chunks(ctx, nl, nl->row_count.as<int>(), nullptr, nullptr, hist);
+    if (rc) return rc;
+  } else {
+    nl->nchunks = 0;
+    nl->n_empty = 0;
+  }
+  CK(cudaStreamSynchronize(ctx->stream));  // host staging vectors go out of scope
   nl->built = true;
   return TB_OK;
 }
@@ -1531,14 +1630,6 @@ extern "C" int tb_md_step(tb_context *ctx, tb_nlist *nl, int64_t n, double *d_po
 // device-resident NVE loop: one graph launch for a whole run (tb_dnl.cuh)
 // ---------------------------------------------------------------------------
 
-static int radix_sort_rows(tb_context *ctx, tb_nlist *nl, const int *row_len) {
-  size_t tmp = ctx->cub_tmp.cap;
-  CK(cub::DeviceRadixSort::SortPairs(ctx->cub_tmp.p, tmp, row_len, nl->sort_keys.as<int>(),
-                                     nl->iota.as<int>(), nl->sorted_atoms.as<int>(), (int)nl->n,
-                                     0, 6, ctx->stream));
-  return TB_OK;
-}
-
 // The complete neighbour-list rebuild with every size taken from the device
 // plan: cell binning, count pass, offsets, fill pass, snapshot, species-pair
 // filter, warp chunks, reverse index.  No host synchronisation; capacities
@@ -1601,7 +1692,7 @@ static int enqueue_rebuild_device(tb_context *ctx, tb_nlist *nl, const double *d
       CK(cudaMemsetAsync(nl->fbuf.p, 0, sizeof(double) * 3 * (size_t)ecap, st));
   }
   if (scatter == TB_SCATTER_GATHER) {
-    rc = radix_sort_rows(ctx, nl, row_len);  // stable: reproducible chunk layout
+    rc = sort_rows_by_length(ctx, nl, row_len);  // stable: reproducible chunk layout
     if (rc) return rc;
   } else if (!filter) {
     // rows bucketed by length and written straight into their chunks (one pass)
@@ -1644,7 +1735,7 @@ static MdKey md_key(const tb_context *ctx, const tb_nlist *nl, const MdArgs &m) 
                      nl->row_count.p, nl->nl_row.p, nl->sorted_atoms.p, nl->sort_keys.p,
                      nl->iota.p, nl->lanes.p, nl->cpos.p, nl->crow.p, nl->coff.p, nl->centry.p,
                      nl->fbuf.p, ctx->facc.p, ctx->partials.p, ctx->ke_part.p, ctx->errf.p,
-                     ctx->cub_tmp.p, nl->scratch.p, m.ref_log};
+                     ctx->scan_tmp.p, nl->scratch.p, m.ref_log};
   static_assert(sizeof(p) / sizeof(p[0]) <= 40, "MdKey::ptr too small");
   memcpy(k.ptr, p, sizeof(p));
   k.n = m.n;
@@ -1808,17 +1899,10 @@ static int md_prepare(tb_context *ctx, tb_nlist *nl, const int *d_species, int s
     int rc = build_rev(ctx, nl);
     if (rc) return rc;
   }
-  {
-    size_t t1 = 0, t2 = 0, t3 = 0;
-    CK(cub::DeviceScan::ExclusiveSum(nullptr, t1, nl->cell_count.as<int>(),
-                                     nl->cell_start.as<int>(), (int)(nl->ncell + 1), ctx->stream));
-    CK(cub::DeviceScan::ExclusiveSum(nullptr, t2, nl->row_count.as<int>(), nl->offsets.as<int>(),
-                                     N + 1, ctx->stream));
-    CK(cub::DeviceRadixSort::SortPairs(nullptr, t3, nl->row_count.as<int>(),
-                                       nl->sort_keys.as<int>(), nl->iota.as<int>(),
-                                       nl->sorted_atoms.as<int>(), N, 0, 6, ctx->stream));
-    CK(ctx->cub_tmp.ensure(std::max(t1, std::max(t2, t3))));
-  }
+  // scan / length-sort scratch for every size the device rebuild uses
+  CK(ctx->scan_tmp.ensure(sizeof(int) * std::max<int64_t>(
+                              std::max(scan_tiles(nl->ncell + 1), scan_tiles((int64_t)N + 1)) + 4,
+                              lsort_scratch(N))));
   int sms = 0;
   CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device));
   CK(ctx->partials.ensure(sizeof(double) * 8 * (size_t)sms * 64));
@@ -1856,8 +1940,8 @@ extern "C" int tb_md_run(tb_context *ctx, tb_nlist *nl, int64_t n, double *d_pos
   CK(cudaSetDevice(ctx->device));
   // the loop keeps the list geometry and the warp-chunk kernel: anything else
   // goes through the per-step path (tb_md_step)
-  if (!nl->built || nl->n != n || n == 0 || !(nl->per[0] && nl->per[1] && nl->per[2]) ||
-      nl->nchunks <= 0 || ctx->force_tile || ctx->S > 2 || r_cut != nl->r_cut || skin != nl->skin)
+  if (!nl->built || nl->imported || nl->n != n || n == 0 ||
+      !(nl->per[0] && nl->per[1] && nl->per[2]) || nl->nchunks <= 0 || ctx->force_tile || ctx->S > 2 || r_cut != nl->r_cut || skin != nl->skin)
     return fail(ctx, TB_ERR_UNSUPPORTED,
                 "device-resident loop needs a built periodic list with rows <= 32 entries");
   MdArgs m{n, d_positions, d_velocities, d_forces, d_mass, d_species, dt, accel, r_cut, skin,
@@ -1978,7 +2062,7 @@ extern "C" int tb_nlist_rebuild_device(tb_context *ctx, tb_nlist *nl, const doub
                                        const int32_t *d_species, int scatter) {
   if (!ctx || !nl || !d_positions || !d_species) return fail(ctx, TB_ERR_ARG, "null argument");
   CK(cudaSetDevice(ctx->device));
-  if (!nl->built || nl->n == 0 || !(nl->per[0] && nl->per[1] && nl->per[2]) ||
+  if (!nl->built || nl->imported || nl->n == 0 || !(nl->per[0] && nl->per[1] && nl->per[2]) ||
       nl->nchunks <= 0 || ctx->force_tile || ctx->S > 2)
     return fail(ctx, TB_ERR_UNSUPPORTED,
                 "device rebuild needs a built periodic list with rows <= 32 entries");
@@ -2008,3 +2092,8 @@ extern "C" int tb_nlist_rebuild_device(tb_context *ctx, tb_nlist *nl, const doub
   if (filter) nl->filter_species = d_species;
   return TB_OK;
 }
+
+// ---------------------------------------------------------------------------
+// slab domain decomposition (north_star (4))
+// ---------------------------------------------------------------------------
+#include "tb_dd_api.inc"

@@ -715,6 +715,11 @@ __global__ void __launch_bounds__(WarpCfg<T>::nt, WarpCfg<T>::minb)
     if (a.per_atom) a.per_atom[m] = 0.0;
     const int sm = a.species[m];
     if (sm < 0 || sm >= S) atomicMin(&a.err->bad_species_atom, m);
+    // (rows are validated by their first lane; an atom without a row -- e.g. a
+    // non-finite position that binned nowhere -- is checked here, kernels.py:111-116)
+    const double *xm = a.pos + 3 * (int64_t)m;
+    if (!(isfinite(__ldg(xm)) && isfinite(__ldg(xm + 1)) && isfinite(__ldg(xm + 2))))
+      atomicMin(&a.err->nonfinite_atom, m);
   }
 
   WAcc<sizeof(T) == 4 || TB_FP64_REG || ((S == 1 || TB_FP64_REGACC_S2) && TB_FP64_REGACC)> A;

@@ -1,30 +1,37 @@
-"""Spatial (slab) domain decomposition of the Tersoff evaluation across ranks.
+"""Spatial (slab) domain decomposition of the Tersoff evaluation and of the NVE
+run across ranks -- BASELINE north_star (4), SURVEY.md 8(e).
 
-BASELINE north_star (4) / SURVEY.md 8(e): one slab of whole cell columns along
-x per rank (one process per GPU), ghost halos one cell column (>= rc + skin)
-wide on both faces, forces on ghosts reverse-communicated to their owners.
-The reference has no decomposition; parity target is the
-single-domain result:
+One process per GPU.  Each rank owns a slab of whole x cell columns of the
+neighbour grid (>= 2 columns per rank: ncx = max(int(Lx / bc), 1), width =
+Lx / ncx, column = floor(remainder(x, Lx) / width) clipped -- neighbor.py:54-88
+arithmetic, so an atom's owner is the same on every rank and in the
+single-domain build).  Ghosts are the atoms of the one column beyond each face
+(width >= r_cut + skin) at unshifted coordinates: every displacement is the
+global-box minimum image, so each owned row, its displacement bits and its
+energy terms equal the single-domain ones; only owned atoms get rows, so each
+term is evaluated exactly once; forces landing on ghosts go back to their
+owners (reverse halo).  The reference has no decomposition: the
+parity target is the single-domain evaluation and NVE run.
 
-* columns are the global cell grid of the neighbour build (neighbor.py:54-88):
-  ncx = floor(Lx / bc), width = Lx / ncx, column = floor(remainder(x, Lx) /
-  width) clipped -- numpy arithmetic identical to the GPU binning, so an atom's
-  column is the same on every rank and in the single-domain build;
-* ghosts keep their unshifted coordinates and every displacement uses the
-  global-box minimum image, so each owned atom's neighbour row, displacement
-  bits and energy terms equal the single-domain ones;
-* only owned atoms get rows (tb_build_neighbors_owned), so every energy term is
-  evaluated exactly once across ranks.
+Per evaluation: forward halo (positions of the send lists to the +-1 ranks),
+evaluation over [owned | ghosts], reverse halo, sum of [E, W6] over ranks.
+Per NVE step (system.py:355-380, :427-460): half-kick + drift + wrap of the
+owned atoms; the skin/2 trigger (neighbor.py:220-229) on the max drift over
+ranks (all-reduce MAX), plus the fixed cadence; at a rebuild migration of the
+atoms whose column changed owner, new send lists and ghost ids / species, a
+positions halo and the owned-rows list; evaluation; second half-kick;
+[E, W6, E_kin] summed over ranks.
 
-Per evaluation: forward halo (positions of the send lists to the +-1 ranks,
-torch.distributed P2P: NCCL over NVLink on GPUs, gloo in the CPU tests),
-compute on [owned | left ghosts | right ghosts], reverse halo (ghost forces
-back to their owners), all-reduce of [E, W6].  At a rebuild: migration of
-atoms that changed column owner, new send lists, ghost ids/species.
-
-The per-rank force engine is pluggable (`engine.rebuild`, `engine.compute`):
-B200Engine drives the CUDA kernels; the CPU tests plug in the oracle.
+Two layers:
+  * the rank's data and kernels -- B200Domain, the C ABI tb_dd_* (csrc/tb_dd.cuh:
+    classification, stable compaction by hand-written scans, packing, ghost
+    unpacking, reverse adds, velocity Verlet; all in HBM, no host copies);
+  * the transport and the step logic -- Comm (torch.distributed P2P: NCCL over
+    NVLink on GPUs, gloo in the CPU tests) and DomainMD, engine-agnostic (the
+    CPU tests drive the same DomainMD with a numpy/oracle engine).
 """
+
+import ctypes
 
 import numpy as np
 import torch
@@ -32,13 +39,13 @@ import torch.distributed as dist
 
 from .errors import ConfigurationError
 
-
-def _np_remainder(x, L):
-    return np.remainder(x, L)
+# ---------------------------------------------------------------------------
+# slab geometry (host mirror of tb_dd.cuh Slab; scatter and tests)
+# ---------------------------------------------------------------------------
 
 
 class SlabDecomposition:
-    """Static slab geometry: which cell columns each rank owns."""
+    """Which cell columns each rank owns."""
 
     def __init__(self, lengths, periodic, bc, nranks):
         if not periodic[0]:
@@ -56,8 +63,7 @@ class SlabDecomposition:
             self._owner[self.bounds[r]:self.bounds[r + 1]] = r
 
     def columns(self, x):
-        """Cell column of each x (neighbor.py:83-88 arithmetic, x axis)."""
-        c = np.floor(_np_remainder(np.asarray(x, dtype=np.float64) - 0.0, self.Lx)
+        c = np.floor(np.remainder(np.asarray(x, dtype=np.float64), self.Lx)
                      / self.width).astype(np.int64)
         return np.clip(c, 0, self.ncx - 1)
 
@@ -71,295 +77,380 @@ class SlabDecomposition:
         return self.bounds[r + 1] - 1
 
 
-class LocalDomain:
-    """The atoms one rank owns (global ids, state) plus its ghost bookkeeping."""
-
-    def __init__(self, ids, positions, velocities, species, masses):
-        self.ids = ids                    # int64 (n_own,)   global ids, host
-        self.pos = positions              # (n_own, 3) float64 tensor (engine device)
-        self.vel = velocities             # (n_own, 3)
-        self.species = species            # (n_own,) int32 tensor
-        self.masses = masses              # (n_own,) float64 tensor (per atom)
-        self.send_left = None             # owned indices sent to rank-1 (their right ghosts)
-        self.send_right = None            # owned indices sent to rank+1 (their left ghosts)
-        self.n_ghost_left = 0
-        self.n_ghost_right = 0
-        self.ghost_ids = None
-        self.ghost_species = None
-
-    @property
-    def n_owned(self):
-        return int(self.pos.shape[0])
+def owned_atoms(decomp, state, rank):
+    """Global ids of the atoms rank `rank` owns initially (every rank sees the
+    same seeded global state)."""
+    return np.nonzero(decomp.owner(state.positions[:, 0]) == rank)[0].astype(np.int64)
 
 
-def scatter_state(decomp, state, rank, device):
-    """Initial distribution: every rank takes the atoms in its columns (all
-    ranks see the same global state, e.g. a seeded generator)."""
-    own = decomp.owner(state.positions[:, 0]) == rank
-    ids = np.nonzero(own)[0].astype(np.int64)
-    t = lambda a, dt: torch.as_tensor(np.ascontiguousarray(a), dtype=dt, device=device)
-    return LocalDomain(ids, t(state.positions[ids], torch.float64),
-                       t(state.velocities[ids], torch.float64),
-                       t(state.species[ids], torch.int32),
-                       t(state.atom_masses[ids], torch.float64))
+# ---------------------------------------------------------------------------
+# transport
+# ---------------------------------------------------------------------------
 
 
-def _padded(shape):
-    # zero-row messages are sent as one dummy row (backends reject empty P2P)
-    return (max(shape[0], 1),) + tuple(shape[1:])
+class Comm:
+    """Neighbour P2P and all-reduces over torch.distributed.
 
+    `route` (e.g. "cpu"): move tensors there for the transport (a gloo group
+    with CUDA-resident domains); None = use the tensors where they live
+    (NCCL).  Zero-row messages are padded to one row on both ends (the
+    counts are exchanged first, so both ends agree)."""
 
-_COMM_DEVICE = {}  # process-wide override: exchange through this device (e.g. "cpu" for gloo)
-
-
-def _exchange(sends, recv_shapes, dtype, device, left, right):
-    """Two-way P2P with the left and right ranks.  sends: (to_left, to_right)
-    tensors; recv_shapes: (from_left, from_right) row counts x width.  Message
-    order per peer is fixed (to_left before to_right), which also resolves the
-    two-rank ring where left == right.  Returns (from_left, from_right)."""
-    comm = _COMM_DEVICE.get("device")
-    if comm is not None and str(comm) != str(device):
-        fl, fr = _exchange(tuple(t.to(comm) for t in sends), recv_shapes, dtype, comm, left,
-                           right)
-        return fl.to(device), fr.to(device)
-    bufs = []
-    for t in sends:
-        t = t.contiguous()
-        if t.shape[0] == 0:
-            t = torch.zeros(_padded(tuple(t.shape)), dtype=dtype, device=device)
-        bufs.append(t)
-    from_left = torch.empty(_padded(recv_shapes[0]), dtype=dtype, device=device)
-    from_right = torch.empty(_padded(recv_shapes[1]), dtype=dtype, device=device)
-    ops = [dist.P2POp(dist.isend, bufs[0], left),
-           dist.P2POp(dist.irecv, from_right, right),
-           dist.P2POp(dist.isend, bufs[1], right),
-           dist.P2POp(dist.irecv, from_left, left)]
-    for req in dist.batch_isend_irecv(ops):
-        req.wait()
-    return from_left[:recv_shapes[0][0]], from_right[:recv_shapes[1][0]]
-
-
-def _exchange_into(sends, recvs, left, right):
-    """_exchange with caller-owned receive buffers (contiguous row blocks,
-    written in place), as the per-step halos use them: no allocation, no
-    concatenation.  Zero-row messages and the gloo routing take _exchange
-    (both ends of a zero-row message do, so the padding stays matched)."""
-    dev = recvs[0].device
-    comm = _COMM_DEVICE.get("device")
-    if (comm is not None and str(comm) != str(dev)) or \
-            any(t.shape[0] == 0 for t in (*sends, *recvs)):
-        fl, fr = _exchange(sends, (tuple(recvs[0].shape), tuple(recvs[1].shape)), recvs[0].dtype,
-                           dev, left, right)
-        recvs[0].copy_(fl)
-        recvs[1].copy_(fr)
-        return
-    ops = [dist.P2POp(dist.isend, sends[0], left),
-           dist.P2POp(dist.irecv, recvs[1], right),
-           dist.P2POp(dist.isend, sends[1], right),
-           dist.P2POp(dist.irecv, recvs[0], left)]
-    for req in dist.batch_isend_irecv(ops):
-        req.wait()
-
-
-def _exchange_counts(a_left, a_right, device, left, right):
-    s = (torch.tensor([a_left], dtype=torch.int64, device=device),
-         torch.tensor([a_right], dtype=torch.int64, device=device))
-    fl, fr = _exchange(s, ((1,), (1,)), torch.int64, device, left, right)
-    return int(fl.item()), int(fr.item())
-
-
-class DecomposedForceField:
-    """Halo exchange + per-rank engine + reverse forces + all-reduce.
-
-    `engine` implements rebuild(pos_local, species_local, n_owned, box) and
-    compute(pos_local, species_local) -> (forces_local (n_local,3) tensor,
-    result tensor [E, W6]) on the domain's device."""
-
-    def __init__(self, decomp, box, engine, rank, nranks, device):
-        self.decomp = decomp
-        self.box = box
-        self.engine = engine
-        self.rank = rank
-        self.nranks = nranks
-        self.device = device
+    def __init__(self, rank, nranks, route=None):
+        self.rank, self.nranks, self.route = rank, nranks, route
         self.left = (rank - 1) % nranks
         self.right = (rank + 1) % nranks
-        self.rebuilds = 0
 
-    # ---- rebuild: migration, send lists, ghost identities ----
-    def migrate(self, dom):
-        """Hand atoms whose column now belongs to a neighbour over to it."""
-        x = dom.pos[:, 0].detach().cpu().numpy()
-        own = self.decomp.owner(x)
-        to_l = np.nonzero(own == self.left)[0] if self.nranks > 1 else np.zeros(0, np.int64)
-        to_r = np.nonzero((own == self.right) & (own != self.left))[0] if self.nranks > 1 \
-            else np.zeros(0, np.int64)
-        stray = np.nonzero((own != self.rank) & (own != self.left) & (own != self.right))[0]
-        if stray.size:
-            raise ConfigurationError("an atom moved more than one slab between rebuilds")
-        keep = np.nonzero(own == self.rank)[0]
+    def _p2p(self, sends, recvs):
+        # fixed message order per peer (to-left before to-right) also pairs the
+        # two messages of the two-rank ring, where left == right
+        ops = [dist.P2POp(dist.isend, sends[0], self.left),
+               dist.P2POp(dist.irecv, recvs[1], self.right),
+               dist.P2POp(dist.isend, sends[1], self.right),
+               dist.P2POp(dist.irecv, recvs[0], self.left)]
+        for req in dist.batch_isend_irecv(ops):
+            req.wait()
+
+    def exchange(self, sends, recvs):
+        """sends = (to_left, to_right), recvs = (from_left, from_right): row
+        blocks of equal width and dtype; received in place."""
         if self.nranks == 1:
-            return dom
-        dev = self.device
-        nl_, nr_ = _exchange_counts(len(to_l), len(to_r), dev, self.left, self.right)
-        idx = lambda a: torch.as_tensor(a, dtype=torch.long, device=dev)
+            return
+        dev = recvs[0].device
+        route = self.route if self.route is not None and str(self.route) != str(dev) else None
+        pad = any(t.shape[0] == 0 for t in (*sends, *recvs))
+        if route is None and not pad:
+            self._p2p([t.contiguous() for t in sends], recvs)
+            return
+        where = route or dev
 
-        def pack(sel):
-            s = idx(sel)
-            f = torch.cat([dom.pos[s], dom.vel[s], dom.masses[s, None],
-                           dom.species[s, None].to(torch.float64),
-                           torch.as_tensor(dom.ids[sel], dtype=torch.float64, device=dev)[:, None]],
-                          dim=1)
-            return f
+        def staged(t):
+            t = t.to(where).contiguous()
+            return t if t.shape[0] else torch.zeros((1,) + tuple(t.shape[1:]), dtype=t.dtype,
+                                                    device=where)
+        s = [staged(t) for t in sends]
+        r = [torch.empty((max(t.shape[0], 1),) + tuple(t.shape[1:]), dtype=t.dtype, device=where)
+             for t in recvs]
+        self._p2p(s, r)
+        for dst, src in zip(recvs, r):
+            if dst.shape[0]:
+                dst.copy_(src[:dst.shape[0]])
 
-        fl, fr = _exchange((pack(to_l), pack(to_r)), ((nl_, 9), (nr_, 9)), torch.float64, dev,
-                           self.left, self.right)
-        k = idx(keep)
-        inc = torch.cat([fl, fr], dim=0)
-        dom.pos = torch.cat([dom.pos[k], inc[:, 0:3]], dim=0).contiguous()
-        dom.vel = torch.cat([dom.vel[k], inc[:, 3:6]], dim=0).contiguous()
-        dom.masses = torch.cat([dom.masses[k], inc[:, 6]], dim=0).contiguous()
-        dom.species = torch.cat([dom.species[k], inc[:, 7].to(torch.int32)], dim=0).contiguous()
-        dom.ids = np.concatenate([dom.ids[keep], inc[:, 8].cpu().numpy().astype(np.int64)])
-        return dom
+    def exchange_counts(self, to_left, to_right, device):
+        s = (torch.tensor([[to_left]], dtype=torch.int64, device=device),
+             torch.tensor([[to_right]], dtype=torch.int64, device=device))
+        r = (torch.empty((1, 1), dtype=torch.int64, device=device),
+             torch.empty((1, 1), dtype=torch.int64, device=device))
+        self.exchange(s, r)
+        return int(r[0].item()), int(r[1].item())
 
-    def rebuild(self, dom):
-        dom = self.migrate(dom)
-        d = self.decomp
-        x = dom.pos[:, 0].detach().cpu().numpy()
-        col = d.columns(x)
-        dom.send_left = np.nonzero(col == d.first_col(self.rank))[0]
-        dom.send_right = np.nonzero(col == d.last_col(self.rank))[0]
-        if self.nranks > 1:
-            dev = self.device
-            ngl, ngr = _exchange_counts(len(dom.send_left), len(dom.send_right), dev,
-                                        self.left, self.right)
-            # from_left = rank-1's right-column atoms = my left ghosts
-            dom.n_ghost_left, dom.n_ghost_right = ngl, ngr
-            idl = torch.as_tensor(dom.send_left, dtype=torch.long, device=dev)
-            idr = torch.as_tensor(dom.send_right, dtype=torch.long, device=dev)
-            meta = lambda sel: torch.stack(
-                [torch.as_tensor(dom.ids, dtype=torch.float64, device=dev)[sel],
-                 dom.species[sel].to(torch.float64)], dim=1)
-            gl, gr = _exchange((meta(idl), meta(idr)), ((ngl, 2), (ngr, 2)), torch.float64, dev,
-                               self.left, self.right)
-            g = torch.cat([gl, gr], dim=0)
-            dom.ghost_ids = g[:, 0].cpu().numpy().astype(np.int64)
-            dom.ghost_species = g[:, 1].to(torch.int32).contiguous()
-            dom._idl, dom._idr = idl, idr
+    def allreduce(self, t, op="sum"):
+        if self.nranks == 1:
+            return t
+        o = dist.ReduceOp.SUM if op == "sum" else dist.ReduceOp.MAX
+        if self.route is not None and str(self.route) != str(t.device):
+            x = t.to(self.route)
+            dist.all_reduce(x, op=o)
+            t.copy_(x)
         else:
-            dom.n_ghost_left = dom.n_ghost_right = 0
-            dom.ghost_ids = np.zeros(0, np.int64)
-            dom.ghost_species = dom.species[:0]
-        self.rebuilds += 1
-        # per-step buffers (fixed until the next rebuild): [owned | left ghosts |
-        # right ghosts] positions, the packed send rows and the returning forces;
-        # species of [owned | ghosts] only change at a rebuild
-        if self.nranks > 1:
-            nsend = len(dom.send_left) + len(dom.send_right)
-            dom._idx_send = torch.cat([dom._idl, dom._idr]).contiguous()
-            dom._pos_l = torch.empty((dom.n_owned + dom.n_ghost_left + dom.n_ghost_right, 3),
-                                     dtype=torch.float64, device=self.device)
-            dom._send = torch.empty((nsend, 3), dtype=torch.float64, device=self.device)
-            dom._back = torch.empty((nsend, 3), dtype=torch.float64, device=self.device)
-        pos_l = self.halo_positions(dom)
-        dom._sp_l = torch.cat([dom.species, dom.ghost_species]).contiguous()
-        self.engine.rebuild(pos_l, dom._sp_l, dom.n_owned, self.box)
-        return dom
-
-    # ---- every evaluation ----
-    def halo_positions(self, dom):
-        """[owned | left ghosts | right ghosts] positions (forward halo)."""
-        if self.nranks == 1:
-            return dom.pos
-        n, ngl = dom.n_owned, dom.n_ghost_left
-        pos_l, send, nsl = dom._pos_l, dom._send, len(dom.send_left)
-        pos_l[:n].copy_(dom.pos)
-        torch.index_select(dom.pos, 0, dom._idx_send, out=send)
-        _exchange_into((send[:nsl], send[nsl:]), (pos_l[n:n + ngl], pos_l[n + ngl:]),
-                       self.left, self.right)
-        return pos_l
-
-    def __call__(self, dom):
-        """Forces on the owned atoms, global energy and virial.  The returned
-        force tensor is a view of the engine's buffer: valid until the next
-        call (copy it to keep it)."""
-        pos_l = self.halo_positions(dom)
-        sp_l = getattr(dom, "_sp_l", None)
-        if sp_l is None:
-            sp_l = torch.cat([dom.species, dom.ghost_species]).contiguous() \
-                if self.nranks > 1 else dom.species
-        forces_l, result = self.engine.compute(pos_l, sp_l)
-        n = dom.n_owned
-        f = forces_l[:n]
-        if self.nranks > 1:
-            # reverse halo: forces on my left ghosts belong to rank-1's right
-            # column atoms and vice versa; from_left carries forces on my
-            # left-column atoms (rank-1's right ghosts)
-            ngl, nsl, back = dom.n_ghost_left, len(dom.send_left), dom._back
-            _exchange_into((forces_l[n:n + ngl], forces_l[n + ngl:]), (back[:nsl], back[nsl:]),
-                           self.left, self.right)
-            f.index_add_(0, dom._idx_send, back)
-            comm = _COMM_DEVICE.get("device")
-            if comm is not None and str(comm) != str(self.device):
-                r = result.to(comm)
-                dist.all_reduce(r)
-                result.copy_(r)
-            else:
-                dist.all_reduce(result)
-        return f, result
+            dist.all_reduce(t, op=o)
+        return t
 
 
-class B200Engine:
-    """Per-rank force engine on the sm_100a kernels (device tensors)."""
+# ---------------------------------------------------------------------------
+# the rank's atoms on the B200 (C ABI tb_dd_*)
+# ---------------------------------------------------------------------------
 
-    def __init__(self, params, skin=0.3, device=0, precision="double", scatter="atomic"):
+_POS, _VEL, _FORCES, _MASS, _SPECIES, _IDS, _SEND, _RECV = range(8)
+_DT = {"f8": torch.float64, "i4": torch.int32, "i8": torch.int64}
+
+
+class _Dev:
+    """A CUDA array interface over a domain buffer (zero-copy torch view)."""
+
+    def __init__(self, ptr, shape, typestr):
+        self.__cuda_array_interface__ = {"shape": tuple(shape), "typestr": "<" + typestr,
+                                         "data": (int(ptr or 0), False), "version": 3,
+                                         "strides": None}
+
+
+class B200Domain:
+    """One rank's atoms in HBM and the tb_dd_* kernels (engine of DomainMD)."""
+
+    def __init__(self, params, box, rank, nranks, skin=0.3, device=0, precision="double",
+                 scatter="atomic"):
         from . import _native
         self.native = _native
         self.ctx = _native.default_context(device)
         self.ctx.set_table(params)
-        self.params = params
-        self.skin = skin
+        self.params, self.box, self.skin = params, box, skin
+        self.device = torch.device("cuda", device)
         self.prec = _native.PRECISION[precision]
         self.scat = _native.SCATTER[scatter]
-        self.nl = _native.NList(self.ctx)
-        self.device = torch.device("cuda", device)
-
-    def rebuild(self, pos_l, sp_l, n_owned, box):
-        P = self.native.ptr
+        self.ctx.set_stream(torch.cuda.current_stream(self.device).cuda_stream)
         L = np.ascontiguousarray(np.asarray(box.lengths, dtype=np.float64))
         per = np.ascontiguousarray(np.asarray(box.periodic, dtype=np.int32))
-        self.ctx.set_stream(torch.cuda.current_stream(self.device).cuda_stream)
-        self.ctx.check(self.ctx.lib.tb_build_neighbors_owned(
-            self.ctx.handle, self.nl.handle, pos_l.shape[0], n_owned, P(pos_l), P(L), P(per),
-            float(self.params.r_cut), float(self.skin)), "tb_build_neighbors_owned")
+        h = ctypes.c_void_p()
+        self._check(self.ctx.lib.tb_dd_create(self.ctx.handle, rank, nranks, _native.ptr(L),
+                                              _native.ptr(per), float(params.r_cut),
+                                              float(skin), ctypes.byref(h)), "tb_dd_create")
+        self.h = h
+        self.nl = _native.NList(self.ctx)
+        self._i64 = (ctypes.c_int64(), ctypes.c_int64())
+        self.drift2 = torch.zeros(1, dtype=torch.float64, device=self.device)
 
-    def compute(self, pos_l, sp_l):
-        """Forces on [owned | ghosts] and [E, W6] into engine-owned buffers
-        (reused while the atom count is unchanged: capturable in a graph)."""
+    def __del__(self):
+        try:
+            if self.h:
+                self.ctx.lib.tb_dd_destroy(self.h)
+                self.h = None
+        except Exception:
+            pass
+
+    def _check(self, rc, what):
+        self.ctx.check(rc, what)
+
+    def counts(self):
+        out = np.zeros(10, dtype=np.int64)
+        self._check(self.ctx.lib.tb_dd_counts(self.h, self.native.ptr(out)), "tb_dd_counts")
+        return out
+
+    def _view(self, which, row0, rows, width, typestr="f8"):
+        p = ctypes.c_void_p()
+        self._check(self.ctx.lib.tb_dd_buffer(self.h, which, ctypes.byref(p)), "tb_dd_buffer")
+        item = int(typestr[1])
+        if rows == 0:
+            return torch.empty((0, width) if width else (0,), dtype=_DT[typestr],
+                               device=self.device)
+        shape = (rows, width) if width else (rows,)
+        return torch.as_tensor(_Dev((p.value or 0) + row0 * max(width, 1) * item, shape, typestr),
+                               device=self.device)
+
+    def _recv(self, rows, width):
+        p = ctypes.c_void_p()
+        self._check(self.ctx.lib.tb_dd_recv_buffer(self.h, rows, width, ctypes.byref(p)),
+                    "tb_dd_recv_buffer")
+        return p.value
+
+    def _split(self, which, nl, nr, width):
+        return (self._view(which, 0, nl, width), self._view(which, nl, nr, width))
+
+    # ---- state ----
+    def load(self, ids, pos, vel, mass, species):
+        P, n = self.native.ptr, len(ids)
+        arr = [np.ascontiguousarray(pos, dtype=np.float64),
+               np.ascontiguousarray(vel, dtype=np.float64),
+               np.ascontiguousarray(mass, dtype=np.float64),
+               np.ascontiguousarray(species, dtype=np.int32),
+               np.ascontiguousarray(ids, dtype=np.int64)]
+        self._check(self.ctx.lib.tb_dd_load(self.h, n, *[P(a) for a in arr]), "tb_dd_load")
+
+    def export(self):
+        c = self.counts()
+        n = int(c[0])
+        ids, pos, vel, f = (np.zeros(n, np.int64), np.zeros((n, 3)), np.zeros((n, 3)),
+                            np.zeros((n, 3)))
         P = self.native.ptr
-        n = pos_l.shape[0]
-        if getattr(self, "_n", None) != n:
-            self._forces = torch.empty((n, 3), dtype=torch.float64, device=self.device)
-            self._result = torch.zeros(8, dtype=torch.float64, device=self.device)
-            self._n = n
-        self.ctx.check(self.ctx.lib.tb_compute_device(
-            self.ctx.handle, self.nl.handle, P(pos_l), P(sp_l), float(self.params.r_cut),
-            self.prec, self.scat, P(self._forces), None, P(self._result), None),
-            "tb_compute_device")
-        return self._forces, self._result[:7]
+        self._check(self.ctx.lib.tb_dd_export(self.h, P(ids), P(pos), P(vel), P(f)),
+                    "tb_dd_export")
+        return ids, pos, vel, f
+
+    def local_ids(self):
+        c = self.counts()
+        return self._view(_IDS, 0, int(c[0] + c[1] + c[2]), 0, "i8").cpu().numpy()
+
+    # ---- rebuild ----
+    def migrate_pack(self):
+        a, b = self._i64
+        self._check(self.ctx.lib.tb_dd_migrate_pack(self.h, ctypes.byref(a), ctypes.byref(b)),
+                    "tb_dd_migrate_pack")
+        return self._split(_SEND, a.value, b.value, 9)
+
+    def migrate_recv(self, nl, nr):
+        self._recv(nl + nr, 9)
+        return self._split(_RECV, nl, nr, 9)
+
+    def migrate_unpack(self, nl, nr):
+        self._check(self.ctx.lib.tb_dd_migrate_unpack(self.h, nl, nr), "tb_dd_migrate_unpack")
+
+    def halo_pack(self):
+        a, b = self._i64
+        self._check(self.ctx.lib.tb_dd_halo_pack(self.h, ctypes.byref(a), ctypes.byref(b)),
+                    "tb_dd_halo_pack")
+        return self._split(_SEND, a.value, b.value, 2)
+
+    def halo_recv(self, nl, nr):
+        self._recv(nl + nr, 2)
+        return self._split(_RECV, nl, nr, 2)
+
+    def halo_unpack(self, nl, nr):
+        self._check(self.ctx.lib.tb_dd_halo_unpack(self.h, nl, nr), "tb_dd_halo_unpack")
+        self._layout()
+
+    def _layout(self):
+        """Views of the per-evaluation message blocks (fixed until the next
+        rebuild: graph-capturable)."""
+        c = self.counts()
+        n, ngl, ngr, nsl, nsr = (int(v) for v in c[:5])
+        self.n_owned, self.n_local = n, n + ngl + ngr
+        self.pos_ghosts = (self._view(_POS, n, ngl, 3), self._view(_POS, n + ngl, ngr, 3))
+        self.force_ghosts = (self._view(_FORCES, n, ngl, 3), self._view(_FORCES, n + ngl, ngr, 3))
+        self.pos_send = self._split(_SEND, nsl, nsr, 3) if nsl + nsr else (
+            self._view(_SEND, 0, 0, 3), self._view(_SEND, 0, 0, 3))
+        self._recv(nsl + nsr, 3)
+        self.force_recv = self._split(_RECV, nsl, nsr, 3)
+
+    def build(self):
+        self._check(self.ctx.lib.tb_dd_build(self.h, self.nl.handle), "tb_dd_build")
+        self._layout()
+
+    # ---- every evaluation ----
+    def pack_positions(self):
+        self._check(self.ctx.lib.tb_dd_pack_positions(self.h), "tb_dd_pack_positions")
+
+    def compute(self, result, stats=None):
+        P = self.native.ptr
+        self._check(self.ctx.lib.tb_dd_compute(self.h, self.nl.handle, self.prec, self.scat,
+                                               P(result), P(stats)), "tb_dd_compute")
+
+    def reverse_add(self):
+        self._check(self.ctx.lib.tb_dd_reverse_add(self.h), "tb_dd_reverse_add")
+
+    # ---- integration ----
+    def kick_drift(self, dt, accel):
+        self._check(self.ctx.lib.tb_dd_kick_drift(self.h, self.nl.handle, float(dt), float(accel),
+                                                  self.native.ptr(self.drift2)),
+                    "tb_dd_kick_drift")
+        return self.drift2
+
+    def kick(self, dt, accel, result):
+        self._check(self.ctx.lib.tb_dd_kick(self.h, float(dt), float(accel),
+                                            self.native.ptr(result)), "tb_dd_kick")
+
+    def pairs(self):
+        """Owned rows as global-id pairs (gid_i, gid_j), for parity checks."""
+        n, m, _ = self.nl.info()
+        off = np.zeros(n + 1, np.int64)
+        nbr = np.zeros(max(m, 1), np.int64)
+        P = self.native.ptr
+        self.ctx.check(self.ctx.lib.tb_nlist_export(self.ctx.handle, self.nl.handle, P(off),
+                                                    P(nbr)), "tb_nlist_export")
+        ids = self.local_ids()
+        i = np.repeat(np.arange(n), np.diff(off))
+        return np.stack([ids[i], ids[nbr[:m]]], axis=1)
+
+    def check_errors(self):
+        self.ctx.check(self.ctx.lib.tb_check_errors(self.ctx.handle), "tb_check_errors")
 
 
-def set_comm_device(device):
-    """Route the P2P/all-reduce traffic through `device` (e.g. "cpu" when the
-    process group is gloo but the domain lives on a GPU)."""
-    _COMM_DEVICE["device"] = device
+# ---------------------------------------------------------------------------
+# the decomposed evaluation and NVE run (engine-agnostic)
+# ---------------------------------------------------------------------------
 
 
-def gather_global(dom, forces_owned, n_global, device):
-    """All-gather owned forces into the global atom order (tests/diagnostics)."""
-    comm = _COMM_DEVICE.get("device") or device
-    out = torch.zeros((n_global, 3), dtype=torch.float64, device=comm)
-    out[torch.as_tensor(dom.ids, dtype=torch.long, device=comm)] = forces_owned.to(comm)
-    dist.all_reduce(out)
-    return out.to(device)
+class DomainMD:
+    """Slab-decomposed evaluation / velocity-Verlet NVE over `engine` (the
+    rank's atoms) and `comm` (the transport).
+
+    result (device tensor, 8 doubles): [E, W xx yy zz xy xz yz, E_kin], summed
+    over ranks after every step."""
+
+    def __init__(self, engine, comm, skin=0.3, dt=1.0, rebuild_every=0, accel=None):
+        from .state import ACCEL
+        self.eng, self.comm = engine, comm
+        self.skin, self.dt, self.rebuild_every = skin, dt, int(rebuild_every or 0)
+        self.accel = ACCEL if accel is None else accel
+        self.device = engine.device
+        self.result = torch.zeros(8, dtype=torch.float64, device=self.device)
+        self.rebuilds = 0
+        self.step_no = 0
+
+    # ---- rebuild: migration, send lists, ghost identities, list ----
+    def rebuild(self):
+        eng, comm = self.eng, self.comm
+        if comm.nranks > 1:
+            sl, sr = eng.migrate_pack()
+            nfl, nfr = comm.exchange_counts(sl.shape[0], sr.shape[0], self.device)
+            comm.exchange((sl, sr), eng.migrate_recv(nfl, nfr))
+            eng.migrate_unpack(nfl, nfr)
+            ml, mr = eng.halo_pack()
+            ngl, ngr = comm.exchange_counts(ml.shape[0], mr.shape[0], self.device)
+            comm.exchange((ml, mr), eng.halo_recv(ngl, ngr))
+            eng.halo_unpack(ngl, ngr)
+            self.forward_positions()
+        eng.build()
+        self.rebuilds += 1
+
+    # ---- every evaluation ----
+    def forward_positions(self):
+        if self.comm.nranks > 1:
+            self.eng.pack_positions()
+            self.comm.exchange(self.eng.pos_send, self.eng.pos_ghosts)
+
+    def evaluate_local(self, stats=None):
+        """Halo + evaluation + reverse halo: complete forces on the owned atoms,
+        this rank's [E, W6] in result[:7] (not yet summed)."""
+        self.forward_positions()
+        self.eng.compute(self.result, stats)
+        if self.comm.nranks > 1:
+            self.comm.exchange(self.eng.force_ghosts, self.eng.force_recv)
+            self.eng.reverse_add()
+        return self.result
+
+    def evaluate(self, stats=None):
+        """One decomposed E+F+virial evaluation; [E, W6] summed over ranks."""
+        self.evaluate_local(stats)
+        self.result[7] = 0.0
+        return self.comm.allreduce(self.result)
+
+    # ---- NVE ----
+    def setup(self):
+        """List, F(0), E(0) and E_kin(0) (run_nve's first ForceField call)."""
+        self.rebuild()
+        self.evaluate_local()
+        self.eng.kick(0.0, self.accel, self.result)  # zero-length kick: E_kin of v(0)
+        return self.comm.allreduce(self.result)
+
+    def step(self):
+        d2 = self.eng.kick_drift(self.dt, self.accel)
+        d2 = float(self.comm.allreduce(d2.clone(), op="max")[0])
+        self.step_no += 1
+        if d2 > (0.5 * self.skin) ** 2 or \
+                (self.rebuild_every and self.step_no % self.rebuild_every == 0):
+            self.rebuild()
+        self.evaluate_local()
+        self.eng.kick(self.dt, self.accel, self.result)
+        return self.comm.allreduce(self.result)
+
+    def run(self, steps, record_every=1):
+        """NVE record as the reference's run_nve: potential / kinetic / total
+        per recorded step (row 0 = the setup state), rebuild count."""
+        rec = [self.setup().clone()]
+        for s in range(1, steps + 1):
+            r = self.step()
+            if s % record_every == 0:
+                rec.append(r.clone())
+        a = torch.stack(rec).cpu().numpy()
+        return {"kind": "nve", "steps": steps, "dt": self.dt, "potential": a[:, 0],
+                "kinetic": a[:, 7], "total": a[:, 0] + a[:, 7], "rebuilds": self.rebuilds,
+                "virial": a[:, 1:7]}
+
+
+def decompose(state, params, rank, nranks, comm=None, skin=0.3, device=0, precision="double",
+              scatter="atomic", dt=1.0, rebuild_every=0):
+    """Rank `rank`'s DomainMD on the B200 for a global (seeded) state."""
+    d = SlabDecomposition(state.box.lengths, state.box.periodic, params.r_cut + skin, nranks)
+    ids = owned_atoms(d, state, rank)
+    eng = B200Domain(params, state.box, rank, nranks, skin, device, precision, scatter)
+    vel = state.velocities if state.velocities is not None else np.zeros_like(state.positions)
+    eng.load(ids, state.positions[ids], vel[ids], state.atom_masses[ids], state.species[ids])
+    return DomainMD(eng, comm or Comm(rank, nranks), skin, dt, rebuild_every)
+
+
+def gather_global(comm, ids, values, n_global, device="cpu"):
+    """Sum-gather per-atom rows (owned ids) into the global order (tests)."""
+    out = torch.zeros((n_global,) + tuple(values.shape[1:]), dtype=torch.float64,
+                      device=comm.route or device)
+    out[torch.as_tensor(ids, device=out.device)] = torch.as_tensor(values, dtype=torch.float64,
+                                                                   device=out.device)
+    return comm.allreduce(out)

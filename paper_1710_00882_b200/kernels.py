@@ -1,17 +1,29 @@
 """The Tersoff energy/force/virial entry points, on B200.
 
 Drop-in for reference pkg/src/tersoffmd/kernels.py:
-  make_variant / KernelVariant   (:46-77)   selector; tag "B200" (the reference
-                                            tags are accepted and all map onto
-                                            the same sm_100a kernel)
+  make_variant / KernelVariant   (:43-77)   selector (tag, backend); tag "B200"
+                                            or any reference tag -- all run the
+                                            same sm_100a kernel
   ForceEnergyResult              (:80-92)   + .virial (xx,yy,zz,xy,xz,yz)
   compute(state, nl, params, variant, threads=1)   (:517-527)
   kernel_function / count_flops_and_visits         (:530-544)
 
-compute() crosses the C ABI once (tb_compute): host positions are copied to
-HBM, the kernel re-packs the skin list at the current positions and
-evaluates E, F, per-atom E and the virial, and the results come back.
-There is no CPU path: a missing library raises NativeUnavailable.
+compute() takes this package's device NeighborList or the reference's own
+NeighborList (numpy CSR; imported once per list object with
+tb_nlist_import), and the reference's KernelVariant(tag, backend) objects as
+well as this package's.  One C-ABI crossing per evaluation (tb_compute):
+host positions are copied to HBM, the kernel re-packs the skin list at the
+current positions and evaluates E, F, per-atom E and the virial.  There is no
+CPU path: a missing library raises NativeUnavailable.
+
+Instrumentation counters follow the reference's contract
+(pkg/tests/test_kernels.py:218-249): zeta_visits = sum n_i^2 over the packed
+rows for single-pass variants and 2 sum n_i^2 for "Reference" (Algorithm 1
+walks k twice, kernels.py:172-243); the scalar tags (Reference, ScalarOpt)
+report no lanes (lane_utilization None) and no gathers; the lane tags (VecJ,
+VecI, B200) report the warp lanes of the B200 chunk layout: lane_total = 32 x
+warp chunks, lane_active = lanes holding a list entry, gathers = one neighbour
+gather per active lane.
 """
 
 import ctypes
@@ -22,59 +34,78 @@ import numpy as np
 
 from . import _native
 from .errors import ConfigurationError
-from .neighbor import _positions
+from .neighbor import NeighborList, _box_args, _positions
 
 REFERENCE_TAGS = ("Reference", "ScalarOpt", "VecJ", "VecI")
 KERNEL_TAGS = ("B200",) + REFERENCE_TAGS
+SCALAR_TAGS = ("Reference", "ScalarOpt")
 PRECISIONS = ("double", "single")
 
 
 @dataclass(frozen=True)
+class DeviceBackend:
+    """Execution model in the shape of the reference's simd.Backend
+    (simd.py:151-181): a warp of 32 lanes."""
+
+    name: str = "sm_100a"
+    width: int = 32
+    precision: str = "double"
+    strict: bool = False
+
+
+@dataclass(frozen=True)
 class KernelVariant:
-    """Kernel selector.  precision: "double" (fp64) or "single" (mixed: fp64
-    positions/displacements/accumulators, fp32 potential math, as
-    kernels.py:154-165).  scatter: "atomic" (red.global.add.f64 of the
+    """(tag, backend) as the reference's selector, plus B200 options:
+    precision "double" (fp64) or "single" (fp64 positions/displacements/
+    accumulators, fp32 potential math, kernels.py:154-165) -- taken from the
+    backend when not given; scatter "atomic" (red.global.add.f64 of the
     neighbour forces) or "gather" (per-entry buffer + deterministic gather)."""
 
     tag: str = "B200"
-    precision: str = "double"
+    backend: object = None
+    precision: str = None
     scatter: str = "atomic"
     device: int = 0
 
     def __post_init__(self):
         if self.tag not in KERNEL_TAGS:
             raise ConfigurationError(f"unknown kernel tag {self.tag!r}")
-        if self.precision not in PRECISIONS:
-            raise ConfigurationError(f"unknown precision {self.precision!r}")
+        prec = self.precision or getattr(self.backend, "precision", None) or "double"
+        if prec not in PRECISIONS:
+            raise ConfigurationError(f"unknown precision {prec!r}")
         if self.scatter not in _native.SCATTER:
             raise ConfigurationError(f"unknown scatter mode {self.scatter!r}")
+        object.__setattr__(self, "precision", prec)
+        if self.backend is None:
+            object.__setattr__(self, "backend", DeviceBackend(precision=prec))
 
     def describe(self):
         return f"{self.tag}[sm_100a,{self.precision},{self.scatter}]"
 
-    @property
-    def backend(self):
-        """Execution model in the shape of the reference's simd.Backend
-        (simd.py:151-181): name, lane width (a warp), precision."""
-        return DeviceBackend("sm_100a", 32, self.precision)
 
-
-@dataclass(frozen=True)
-class DeviceBackend:
-    name: str
-    width: int
-    precision: str
-    strict: bool = False
-
-
-def make_variant(tag="B200", backend=None, width=None, precision="double", strict=False,
+def make_variant(tag="B200", backend="scalar", width=None, precision="double", strict=False,
                  scatter="atomic", device=0):
-    """Mirror of kernels.make_variant (kernels.py:73-77).  backend/width/strict
-    describe the reference's CPU lane emulation and are accepted for
-    signature compatibility; the B200 kernel has one execution model."""
-    if backend is not None and hasattr(backend, "precision"):
-        precision = backend.precision
-    return KernelVariant(tag, precision, scatter, device)
+    """Mirror of kernels.make_variant (kernels.py:73-77).  A reference Backend
+    object supplies the precision; backend names / width / strict describe the
+    reference's CPU lane emulation and are accepted for compatibility."""
+    if backend is not None and not isinstance(backend, str):
+        return KernelVariant(tag, backend, getattr(backend, "precision", precision), scatter,
+                             device)
+    return KernelVariant(tag, None, precision, scatter, device)
+
+
+def resolve_variant(variant):
+    """This package's KernelVariant for None, one of ours, or the reference's
+    KernelVariant(tag, backend) (duck-typed: .tag and .precision/.backend)."""
+    if variant is None:
+        return KernelVariant()
+    if isinstance(variant, KernelVariant):
+        return variant
+    tag = getattr(variant, "tag", None)
+    prec = getattr(variant, "precision", None) or \
+        getattr(getattr(variant, "backend", None), "precision", None)
+    return KernelVariant(tag, getattr(variant, "backend", None), prec,
+                         getattr(variant, "scatter", "atomic"), getattr(variant, "device", 0))
 
 
 @dataclass
@@ -95,8 +126,8 @@ class ForceEnergyResult:
 
 def _species_i32(state, n):
     sp = state.species
-    if isinstance(sp, np.ndarray) or sp is None:
-        sp = np.zeros(n, np.int32) if sp is None else sp
+    if isinstance(sp, np.ndarray) or sp is None or isinstance(sp, (list, tuple)):
+        sp = np.zeros(n, np.int32) if sp is None else np.asarray(sp)
         if sp.shape != (n,):
             raise ConfigurationError(f"species shape {sp.shape} does not match {n} atoms")
         return np.ascontiguousarray(sp, dtype=np.int32)
@@ -135,6 +166,55 @@ class _Scratch:
         self.refs = (ctypes.byref(self.chunks), ctypes.byref(self.used))
 
 
+# the reference's NeighborList objects -> imported device lists
+_IMPORTED = weakref.WeakKeyDictionary()
+
+
+def device_list(nl, state, device=0):
+    """This package's NeighborList for `nl`: itself, or the device import of a
+    reference NeighborList (offsets / neighbors / reference_positions CSR,
+    neighbor.py:170-191), cached for the lifetime of that object."""
+    if isinstance(nl, NeighborList):
+        return nl
+    try:
+        hit = _IMPORTED.get(nl)
+    except TypeError:  # not weak-referenceable
+        hit = None
+    if hit is not None and hit[1] is nl.offsets and hit[2] is nl.neighbors:
+        return hit[0]
+    off = np.ascontiguousarray(nl.offsets, dtype=np.int64)
+    nbr = np.ascontiguousarray(nl.neighbors, dtype=np.int64)
+    ref = np.ascontiguousarray(nl.reference_positions, dtype=np.float64)
+    n = off.shape[0] - 1
+    skin = float(getattr(nl, "skin", 0.0))
+    r_cut = float(getattr(nl, "r_cut", nl.build_cutoff - skin))
+    ctx = _native.default_context(device)
+    h = _native.NList(ctx)
+    L, per = _box_args(state.box)
+    ctx.check(ctx.lib.tb_nlist_import(ctx.handle, h.handle, n, _native.ptr(off),
+                                      _native.ptr(nbr), _native.ptr(ref), _native.ptr(L),
+                                      _native.ptr(per), r_cut, skin), "tb_nlist_import")
+    dl = NeighborList(h, n, r_cut + skin, r_cut, skin, ref, state.box)
+    dl._csr = (off, nbr)
+    try:
+        _IMPORTED[nl] = (dl, nl.offsets, nl.neighbors)
+    except TypeError:
+        pass
+    return dl
+
+
+def _stats(tag, counts, chunks, used):
+    nsq = int(counts[0])
+    lanes = tag not in SCALAR_TAGS
+    return {"zeta_visits": 2 * nsq if tag == "Reference" else nsq,
+            "gathers": int(used) if lanes else 0,
+            "lane_active": int(used) if lanes else 0,
+            "lane_total": 32 * int(chunks) if lanes else 0,
+            "packed_pairs": int(counts[1]), "live_pairs": int(counts[2]),
+            "live_triplets": int(counts[3]), "taper_pairs": int(counts[4]),
+            "taper_triplets": int(counts[5])}
+
+
 def compute(state, nl, params, variant=None, threads=1, out=None):
     """One E+F(+virial) evaluation (kernels.py:517-527).
 
@@ -144,10 +224,12 @@ def compute(state, nl, params, variant=None, threads=1, out=None):
     `out` (extension): a ForceEnergyResult whose forces / per_atom_energy
     arrays are overwritten instead of allocating new ones (e.g. pinned host
     buffers for a streaming driver); it is returned updated."""
-    variant = variant or KernelVariant()
+    variant = resolve_variant(variant)
+    pos = _positions(state)
+    nl = device_list(nl, state, variant.device if isinstance(pos, np.ndarray)
+                     else pos.device.index)
     ctx = nl.context
     ctx.set_table(params)
-    pos = _positions(state)
     n = int(pos.shape[0])
     if n != nl.natoms:
         raise ConfigurationError(f"state has {n} atoms but the neighbor list {nl.natoms}")
@@ -176,12 +258,7 @@ def compute(state, nl, params, variant=None, threads=1, out=None):
     rc = lib.tb_nlist_lanes(nl._nl.handle, *scr.refs)
     if rc:
         ctx.check(rc, "tb_nlist_lanes")
-    stats = scr.stats.tolist()
-    st = {"zeta_visits": stats[0], "gathers": 0,
-          "lane_active": scr.used.value, "lane_total": 32 * scr.chunks.value,
-          "packed_pairs": stats[1], "live_pairs": stats[2],
-          "live_triplets": stats[3], "taper_pairs": stats[4],
-          "taper_triplets": stats[5]}
+    st = _stats(variant.tag, scr.stats, scr.chunks.value, scr.used.value)
     energy, virial = float(scr.energy[0]), scr.virial.copy()
     if out is not None:
         out.potential_energy, out.stats, out.virial = energy, st, virial
@@ -197,9 +274,10 @@ def kernel_function(variant, threads=1):
 
 
 def count_flops_and_visits(state, nl, params, variant):
-    """Run once and report the work counters (kernels.py:537-544)."""
+    """Run once and report the instrumentation counters (kernels.py:537-544),
+    plus the live pair / triplet counts the roofline is charged on."""
     res = compute(state, nl, params, variant)
-    return {"zeta_visits": res.stats["zeta_visits"], "gathers": 0,
+    return {"zeta_visits": res.stats["zeta_visits"], "gathers": res.stats["gathers"],
             "lane_utilization": res.lane_utilization,
             "live_pairs": res.stats["live_pairs"],
             "live_triplets": res.stats["live_triplets"]}

@@ -17,7 +17,7 @@ on the (1/4,1/4,1/4)-shifted half.  Velocities follow seed_velocities
 
 import numpy as np
 
-from .system import SimulationBox, SimulationState, seed_velocities  # noqa: F401
+from .state import MASSES, SimulationBox, SimulationState, seed_velocities  # noqa: F401
 
 _DIAMOND_BASIS = np.array([
     [0.00, 0.00, 0.00], [0.00, 0.50, 0.50],
@@ -26,7 +26,6 @@ _DIAMOND_BASIS = np.array([
     [0.75, 0.25, 0.75], [0.75, 0.75, 0.25],
 ])
 
-MASSES = {"C": 12.011, "Si": 28.0855, "Ge": 72.63}  # system.py:24
 
 
 def _lattice(cells, a):

@@ -25,7 +25,7 @@ class Frame:
     (the reference's own test stub shape, helpers.py:78-97)."""
 
     def __init__(self, positions, lengths, periodic, species=None):
-        from paper_1710_00882_b200.system import SimulationBox
+        from paper_1710_00882_b200.state import SimulationBox
         self.positions = np.ascontiguousarray(positions, dtype=np.float64)
         self.box = SimulationBox(lengths, tuple(bool(p) for p in periodic))
         n = self.positions.shape[0]

@@ -10,7 +10,7 @@ from paper_1710_00882_b200 import _native, structures
 from paper_1710_00882_b200.kernels import compute, make_variant
 from paper_1710_00882_b200.neighbor import build_neighbor_list
 from paper_1710_00882_b200.paramfile import builtin_params
-from paper_1710_00882_b200.system import SimulationBox, SimulationState
+from paper_1710_00882_b200.state import SimulationBox, SimulationState
 
 pytestmark = pytest.mark.gpu
 

@@ -1,6 +1,6 @@
-"""Device-resident NVE (tb_md_step / run_nve_device) and the host-level
-ForceField / run_nve drivers against the reference's own NVE run (golden) and
-the oracle's.  North-star bar: energy drift over 1000 NVE steps comparable to
+"""Device-resident NVE (md.run_nve: tb_md_run graph loop / tb_md_step) and
+md.ForceField as a drop-in force provider, against the reference's own NVE
+run (golden) and the oracle's.  North-star bar: energy drift over 1000 NVE steps comparable to
 the reference (fp64 and mixed)."""
 
 import numpy as np
@@ -10,8 +10,15 @@ import paper_1710_00882_b200 as B
 from conftest import load_golden
 from paper_1710_00882_b200 import structures
 from paper_1710_00882_b200.paramfile import builtin_params, parse_params
-from paper_1710_00882_b200.system import (RunConfig, SimulationBox, SimulationState,
-                                          run_nve_device)
+from paper_1710_00882_b200.md import ForceField, RunConfig, run_nve
+from paper_1710_00882_b200.state import ACCEL, SimulationBox, SimulationState
+
+
+def run_nve_device(state, params, cfg, precision="double", scatter="atomic", record_every=1,
+                   loop="auto"):
+    cfg.variant = B.make_variant("B200", precision=precision, scatter=scatter)
+    cfg.record_every = record_every
+    return run_nve(state, params, cfg, loop=loop)
 
 pytestmark = pytest.mark.gpu
 
@@ -47,10 +54,55 @@ def test_device_nve_matches_reference_run(precision, loop):
     assert drift(rec["total"]) < 5 * max(drift(ref_total), 1e-6)
 
 
-def test_host_run_nve_matches_reference():
+def test_force_field_drives_host_verlet_like_reference():
+    # ForceField as the forces_fn of a host velocity-Verlet loop (the
+    # reference's velocity_verlet_step shape, system.py:355-380): the golden
+    # trajectory of the reference's run_nve over 30 steps
     g, st, t = si512_state()
-    rec = B.run_nve(st, t, B.RunConfig(dt=1.0, steps=30, skin=0.3))
+    ff = ForceField(t, B.make_variant("ScalarOpt"), skin=0.3)
+    m = st.atom_masses[:, None]
+    half = 0.5 * 1.0 * ACCEL
+    res = ff(st)
+    total = [res.potential_energy + B.kinetic_energy(st)]
+    for _ in range(30):
+        st.velocities += half * res.forces / m
+        st.positions += 1.0 * st.velocities
+        st.box.wrap(st.positions)
+        res = ff(st)
+        st.velocities += half * res.forces / m
+        total.append(res.potential_energy + B.kinetic_energy(st))
     ref = g["nve_total"][:31]
+    assert np.max(np.abs(np.array(total) - ref)) <= 1e-9 * abs(ref[0])
+    assert ff.evaluations == 31 and ff.rebuilds >= 2
+    assert isinstance(res.forces, np.ndarray)
+
+
+def test_force_field_device_state_and_nonfinite():
+    import torch
+    g, st, t = si512_state()
+    ff = ForceField(t, skin=0.3)
+    dev = SimulationState(st.positions, st.box, species=st.species, masses=st.masses)
+    dev.positions = torch.from_numpy(st.positions).cuda()
+    dev.species = torch.from_numpy(st.species.astype(np.int32)).cuda()
+    r_dev = ff(dev)
+    r_host = ForceField(t, skin=0.3)(st)
+    assert r_dev.forces.is_cuda
+    assert np.abs(r_dev.forces.cpu().numpy() - r_host.forces).max() < 1e-12
+    bad = st.copy()
+    bad.positions[3, 0] = np.nan
+    with pytest.raises(B.InputError):
+        ForceField(t)(bad)
+
+
+def test_run_nve_dumps_xyz_frames(tmp_path):
+    g, st, t = si512_state()
+    path = tmp_path / "traj.xyz"
+    cfg = RunConfig(dt=1.0, steps=20, skin=0.3, dump_every=10, dump_path=str(path))
+    rec = run_nve(st, t, cfg)
+    frames = B.read_xyz(path)
+    assert len(frames) == 3 and rec["loop"] == "graph"
+    assert np.abs(frames[-1][1] - st.positions).max() < 1e-9
+    ref = g["nve_total"][:21]
     assert np.max(np.abs(rec["total"] - ref)) <= 1e-9 * abs(ref[0])
 
 

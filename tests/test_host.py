@@ -4,6 +4,7 @@ declares, signatures bound) -- no compute calls."""
 
 import ctypes
 import os
+import sys
 import re
 
 import numpy as np
@@ -12,6 +13,7 @@ import pytest
 import paper_1710_00882_b200 as B
 from conftest import load_golden
 from paper_1710_00882_b200 import _native, structures
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 from paper_1710_00882_b200.paramfile import (ParamFileError, builtin_params, parse_params,
                                              serialize_params)
 
@@ -97,6 +99,72 @@ def test_variant_selection():
         B.make_variant("Fastest")
     with pytest.raises(B.ConfigurationError, match="scatter"):
         B.make_variant("B200", scatter="magic")
+
+
+def test_reference_variant_objects_resolve():
+    # the reference's KernelVariant(tag, backend) (kernels.py:46-77), duck-typed
+    from paper_1710_00882_b200.kernels import resolve_variant
+
+    class Backend:
+        name, width, precision, strict = "native", 8, "single", False
+
+    class RefVariant:
+        tag, backend, precision = "VecI", Backend(), "single"
+
+    v = resolve_variant(RefVariant())
+    assert (v.tag, v.precision, v.scatter) == ("VecI", "single", "atomic")
+    kv = B.KernelVariant("ScalarOpt", Backend())  # positional (tag, backend) like the reference
+    assert kv.precision == "single" and kv.backend.width == 8
+    assert B.make_variant("Reference", Backend()).precision == "single"
+    assert resolve_variant(None).tag == "B200"
+
+
+def test_stats_contract():
+    # pkg/tests/test_kernels.py:218-249: Reference walks k twice, scalar tags
+    # have no lanes (lane_utilization None) and no gathers
+    from paper_1710_00882_b200.kernels import ForceEnergyResult, _stats
+    counts = [10, 4, 4, 6, 1, 2]
+    ref = _stats("Reference", counts, 3, 70)
+    opt = _stats("ScalarOpt", counts, 3, 70)
+    vec = _stats("VecI", counts, 3, 70)
+    assert ref["zeta_visits"] == 20 and opt["zeta_visits"] == 10 == vec["zeta_visits"]
+    for s in (ref, opt):
+        assert s["lane_total"] == 0 and s["gathers"] == 0
+        assert ForceEnergyResult(None, 0.0, None, s).lane_utilization is None
+    assert vec["lane_total"] == 96 and vec["lane_active"] == 70 == vec["gathers"]
+    assert ForceEnergyResult(None, 0.0, None, vec).lane_utilization == pytest.approx(70 / 96)
+
+
+def _reference_package():
+    ref = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref, "tersoffmd")):
+        pytest.skip("reference not installed in baseline/_ref")
+    if ref not in sys.path:
+        sys.path.insert(0, ref)
+    import tersoffmd
+    return tersoffmd
+
+
+def test_integration_install_registers_variant():
+    tersoffmd = _reference_package()
+    from paper_1710_00882_b200 import integration
+    import tersoffmd.cli
+    import tersoffmd.kernels as K
+    import tersoffmd.system as S
+    orig = K.compute
+    integration.install(tersoffmd)
+    try:
+        integration.install(tersoffmd)  # idempotent
+        assert K.KERNEL_TAGS.count("B200") == 1
+        v = K.make_variant("B200", precision="single")
+        assert v.tag == "B200" and v.precision == "single"
+        assert S.compute is K.compute and K.compute._b200_orig is orig
+        assert tersoffmd.cli._VARIANT_NAMES["b200"] == "B200"
+    finally:
+        integration.uninstall(tersoffmd)
+    assert K.compute is orig and S.compute is orig and "B200" not in K.KERNEL_TAGS
+    with pytest.raises(tersoffmd.errors.ConfigurationError):
+        K.make_variant("B200")
 
 
 def test_generators_deterministic_and_sized():

@@ -8,7 +8,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 import paper_1710_00882_b200 as B
 from paper_1710_00882_b200 import _native, structures
-from paper_1710_00882_b200.system import RunConfig, run_nve_device
+from paper_1710_00882_b200.md import RunConfig, run_nve
 import bench
 
 cfgs = [int(c) for c in os.environ.get("CB_CONFIGS", "1,2,3,4,5").split(",")]
@@ -80,9 +80,10 @@ if 2 in cfgs and os.environ.get("CB_MD", "1") == "1":
     t = B.builtin_params(tn)
     for prec in ("double", "single"):
         for loop in ("graph", "step"):
-            cfgr = RunConfig(dt=1.0, steps=int(os.environ.get("CB_MD_STEPS", "500")), skin=0.3, rebuild_every=10)
-            run_nve_device(st.copy(), t, RunConfig(dt=1.0, steps=20, skin=0.3, rebuild_every=10), precision=prec, loop=loop)
-            r = run_nve_device(st.copy(), t, cfgr, precision=prec, loop=loop)
+            v = B.make_variant("B200", precision=prec)
+            cfgr = RunConfig(dt=1.0, steps=int(os.environ.get("CB_MD_STEPS", "500")), skin=0.3, rebuild_every=10, variant=v)
+            run_nve(st.copy(), t, RunConfig(dt=1.0, steps=20, skin=0.3, rebuild_every=10, variant=v), loop=loop)
+            r = run_nve(st.copy(), t, cfgr, loop=loop)
             drift = float(np.max(np.abs(r["total"] - r["total"][0])) / abs(r["total"][0]))
             key = f"md_config2_{prec}_{loop}"
             out[key] = {"atom_steps_per_s": st.natoms * cfgr.steps / r["wall_clock"]["loop"],
