@@ -2,32 +2,42 @@
 """Benchmark of the B200 Tersoff hot path (driver contract: one JSON line).
 
 Metric (BASELINE.json): Tersoff atom-steps/s -- atoms x E+F evaluations per
-second -- with the achieved fraction of the FP64 pipe peak.
+second -- with the achieved fraction of the FP64 (FP32 for mixed) pipe peak.
 
-Workload: BASELINE config 2, the largest single-GPU configuration the metric
-is quoted on: 64,000-atom Si diamond (20^3 cells, a=5.431, sigma=0.1 seed
-1002), Si(C) Tersoff parameters, skin 0.3, fp64.  One "step" = one energy +
-force + virial evaluation at the current positions: the kernel re-packs the
-skin list at r_cut (pack_adjacency) and evaluates every Tersoff term
-(kernels.compute semantics).  The neighbour list is built once outside the
-timed region, as the reference harness does (bench.py:116-118).  Inputs are
-resident in HBM for `value`; the 64k-atom working set (~6 MB) fits in L2, so
-L2 is flushed (a 256 MiB write) between timed steps.
+Workload (default): BASELINE config 5, the largest configuration the metric
+is quoted on -- 16,777,216-atom Si diamond (128^3 cells, a=5.431, sigma=0.1
+seed 1005), Si(C) Tersoff parameters, skin 0.3, fp64.  One "step" = one
+energy + force + virial evaluation at the current positions: the kernel
+re-packs the skin list at r_cut (pack_adjacency) and evaluates every Tersoff
+term (kernels.compute semantics).  The neighbour list is built once outside
+the timed region, as the reference harness does (bench.py:116-118).  The
+working set (positions 0.4 GB, list 0.27 GB, lane table 1 GB) is far larger
+than L2, so no flush is needed between steps.  --config 2/3/4 select the other
+single-GPU configurations (smaller ones flush L2 between steps).
 
-  e2e         the same evaluation through the public API compute() with the
-              positions in pinned host memory: H2D of positions+species and
-              D2H of forces, per-atom energies, energy/virial/stats per step.
-  roofline    the Tersoff kernel's algorithmic fp64 flops (SURVEY 8(d) op
-              counts per live pair / live triplet) / its CUDA-event time, against
-              the FP64 DFMA peak measured on this GPU at start-up.
-  cpu_baseline  the CPU oracle (a C restatement of the reference ScalarOpt,
-              oracle/) on this host's cores, rank 0, N=1.
-
-  --impl reference   the reference's CPU implementation of the path on the
-              host cores (the oracle port; the Python reference cannot travel).
-
-Multi-GPU (torchrun, N>1): every rank evaluates its own replica of the
-workload (weak scaling); time = max over ranks of the device-timed loop.
+  N = 1      one GPU: each step is one CUDA-graph replay (Tersoff kernel +
+             finalize); value = atoms x steps / device time.
+  N > 1      (torchrun, NCCL) slab decomposition, decomp.DomainMD: strong
+             scaling of config 5 by default (--scaling weak: 64^3 cells =
+             2,097,152 atoms per GPU stacked along x).  A step = forward halo
+             (NCCL P2P) + evaluation of the owned rows + reverse halo + sum of
+             [E, W6] (all-reduce), captured as one CUDA graph; time = max over
+             ranks of the device-timed loop; value = all atoms x steps / time.
+  e2e        the same evaluation through the public API with HOST buffers:
+             compute() with pinned host positions/species in, forces/per-atom
+             energies out (N = 1); at N > 1 pinned host positions in and forces
+             out around each decomposed step.
+  roofline   the Tersoff kernel's algorithmic flops (SURVEY 8(d) op counts per
+             live pair / triplet) / its CUDA-event time, against the FMA-pipe
+             peak measured on this GPU at start-up; the ncu pipe utilisation
+             and DRAM traffic of the same kernel and config from profiles/.
+  cpu_baseline / --impl reference
+             the CPU oracle (C restatement of the reference ScalarOpt,
+             oracle/) on this host's cores -- "port": the reference itself is
+             Python and cannot travel to the GPU box.
+  extras     mixed precision (same workload), config 2 (64k atoms, the round-1
+             headline), the device-resident NVE of configs 2 and 5 (tb_md_run:
+             one graph launch per run), at N > 1 the decomposed NVE step.
 """
 
 import argparse
@@ -88,7 +98,11 @@ def algorithmic_flops32(stats):
 
 def algorithmic_flops(stats):
     return int(FLOPS_PAIR * stats[2] + FLOPS_TAPER * stats[4]
-            + FLOPS_TRIP * stats[3] + FLOPS_TAPER * stats[5])
+               + FLOPS_TRIP * stats[3] + FLOPS_TAPER * stats[5])
+
+
+def flops_for(stats, precision):
+    return algorithmic_flops(stats) if precision == "double" else algorithmic_flops32(stats)
 
 
 class ClockSampler:
@@ -134,7 +148,7 @@ class ClockSampler:
                         self.reasons.add(name)
             except Exception:
                 pass
-            time.sleep(0.01)
+            time.sleep(0.005)
 
     def __enter__(self):
         if self.ok:
@@ -169,22 +183,59 @@ def cpu_cores():
         return os.cpu_count() or 1
 
 
-def oracle_baseline(state, table, budget_s=12.0, min_evals=2, threads=None):
-    """Time the CPU oracle (reference ScalarOpt restated in C, OpenMP over
-    atom ranges) on this host: NL built outside the timer, then E+F
-    evaluations (pack + kernel) until `budget_s`."""
+# ---------------------------------------------------------------------------
+# workload (shared by both arms: identical `config` dicts)
+# ---------------------------------------------------------------------------
+
+def make_workload(args, ws):
+    """(state, table name, config dict) of this run."""
+    from paper_1710_00882_b200 import structures
+    weak = ws > 1 and args.scaling == "weak"
+    if weak:
+        st, tname = structures.config5_weak(ws)
+        what = (f"BASELINE config 5, weak scaling: (64*{ws})x64x64-cell Si diamond "
+                f"({st.natoms} atoms, 2,097,152 per GPU)")
+    else:
+        st, tname = structures.config(args.config)
+        what = {2: "BASELINE config 2: 64,000-atom Si diamond (20^3 cells)",
+                3: "BASELINE config 3: 512,000-atom 3C-SiC (40^3 cells, fixture SiC table)",
+                4: "BASELINE config 4: 1,000,000-atom disordered Si (rho 0.05/A^3)",
+                5: "BASELINE config 5: 16,777,216-atom Si diamond (128^3 cells)"}.get(
+                    args.config, f"BASELINE config {args.config}")
+    cfg = {"workload": f"{what}, one E+F+virial evaluation per step, neighbour list (skin "
+                       f"0.3) built outside the timed region",
+           "config": args.config if not weak else 5, "atoms": int(st.natoms),
+           "precision": args.precision, "skin": 0.3,
+           "scaling": ("weak" if weak else "strong") if ws > 1 else "single GPU",
+           "parallelism": f"spatial slabs x{ws}" if ws > 1 else "single GPU"}
+    return st, tname, cfg
+
+
+# ---------------------------------------------------------------------------
+# CPU oracle (cpu_baseline and the reference arm)
+# ---------------------------------------------------------------------------
+
+def oracle_timing(state, table, budget_s, max_evals, precision="double", threads=None):
+    """The CPU oracle (reference ScalarOpt restated in C, OpenMP over atom
+    ranges): NL built outside the timer, then E+F evaluations (pack + kernel)
+    until `budget_s` or `max_evals`."""
     from oracle import oracle as O
     threads = threads or cpu_cores()
     off, nb = O.build_neighbor_list(state.positions, state.box.lengths, state.box.periodic,
                                     table.r_cut, 0.3, threads=threads)
+
+    def one():
+        O.compute(state.positions, state.species, state.box.lengths, state.box.periodic,
+                  off, nb, table, precision=precision, threads=threads)
+
+    one()  # warm (page-in, thread pool)
     t0 = time.perf_counter()
     evals = 0
     while True:
-        O.compute(state.positions, state.species, state.box.lengths, state.box.periodic,
-                  off, nb, table, threads=threads)
+        one()
         evals += 1
         el = time.perf_counter() - t0
-        if (el >= budget_s and evals >= min_evals) or evals >= 10000:
+        if el >= budget_s or evals >= max_evals:
             break
     return state.natoms * evals / el, threads, evals, el
 
@@ -193,447 +244,185 @@ def reference_arm(args):
     ws, rank, _ = dist_setup()
     if rank != 0:
         return
-    from paper_1710_00882_b200 import structures
     from paper_1710_00882_b200.paramfile import builtin_params
-    from oracle import oracle as O
-    state, tname = structures.config(args.config)
+    state, tname, cfg = make_workload(args, ws)
     table = builtin_params(tname)
-    threads = cpu_cores()
-    off, nb = O.build_neighbor_list(state.positions, state.box.lengths, state.box.periodic,
-                                    table.r_cut, 0.3, threads=threads)
-
-    def one():
-        O.compute(state.positions, state.species, state.box.lengths, state.box.periodic,
-                  off, nb, table, precision=args.precision_ref, threads=threads)
-
-    for _ in range(args.warmup):
-        one()
-    # bounded sample: the whole run stays within ~2 minutes
-    t0 = time.perf_counter()
-    one()
-    per = time.perf_counter() - t0
-    steps = args.steps
-    budget = 120.0
-    timed = max(1, min(steps, int(budget / max(per, 1e-6))))
-    t0 = time.perf_counter()
-    for _ in range(timed):
-        one()
-    el = time.perf_counter() - t0
-    value = state.natoms * timed / el
+    v, threads, evals, el = oracle_timing(state, table, args.ref_budget,
+                                          max(1, args.steps), args.precision)
     line = {
-        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
-        "steps": timed, "warmup": args.warmup, "ms_per_step": 1e3 * el / timed,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-        "dtype": "f64" if args.precision_ref == "double" else "f32/f64",
-        "data": "synthetic", "impl": "reference",
-        "config": {"workload": f"BASELINE config {args.config}: {state.natoms} Si diamond "
-                               f"E+F(+virial) evaluation, skin 0.3",
-                   "atoms": state.natoms, "precision": args.precision_ref},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
-                         "sample": f"{timed} full E+F evaluations of the {state.natoms}-atom "
-                                   f"system (of {steps} requested; bounded to ~{budget:.0f} s), "
-                                   f"NL built outside the timer; oracle/ C restatement of "
-                                   f"ScalarOpt, OpenMP over {threads} threads"},
-        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": ws, "steps": evals,
+        "warmup": args.warmup, "ms_per_step": 1e3 * el / evals, "higher_is_better": True,
+        "scaling": "weak" if cfg["scaling"] == "weak" else "strong", "vs_baseline": None,
+        "dtype": "f64" if args.precision == "double" else "f32/f64",
+        "data": "synthetic", "impl": "reference", "config": cfg,
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads, "kind": "port",
+                         "sample": f"{evals} full E+F evaluations of the {state.natoms}-atom "
+                                   f"system in {el:.1f} s (of {args.steps} requested; bounded to "
+                                   f"~{args.ref_budget:.0f} s), NL built outside the timer; "
+                                   f"oracle/ C restatement of ScalarOpt, OpenMP {threads} threads"},
+        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line, default=_jsonable), flush=True)
 
 
-def gpu_arm_decomposed(args):
-    """N > 1: slab decomposition (decomp.py) with NCCL P2P halos, weak scaling:
-    every GPU owns a 20^3-cell (64,000-atom) slab of a (20N x 20 x 20)-cell Si
-    crystal (config 2 per GPU, same seeds).  A step = forward halo + Tersoff
-    evaluation on [owned | ghosts] + reverse ghost forces + all-reduce of
-    [E, W6]; device-timed (CUDA events) per rank, max over ranks."""
+# ---------------------------------------------------------------------------
+# measurement helpers
+# ---------------------------------------------------------------------------
+
+def measure_peak(lib, ctx, precision):
+    """FMA-pipe peak measured on this GPU (MEASURED_PEAKS.json has no fp64/fp32
+    figure): an 8-chain FMA loop over all SMs, best of 5 (tb_measure_peak)."""
+    import ctypes
+    out = ctypes.c_double()
+    if lib.tb_measure_peak(ctx.handle, int(precision), ctypes.byref(out)) != 0:
+        return None
+    return {"tflops": out.value,
+            "source": f"measured {'DFMA' if precision == 0 else 'FFMA'} loop in bench.py "
+                      f"(tb_measure_peak; MEASURED_PEAKS.json has no fp64/fp32 entry)"}
+
+
+def ncu_profile(config, precision):
+    """The committed ncu --set full summary of the Tersoff kernel at this
+    config / precision (profiles/ncu_r02_kernels.json, tools/ncu_kernels.sh)."""
+    for name in ("ncu_r02_kernels.json", "ncu_r01_kernels.json"):
+        try:
+            d = json.load(open(os.path.join(ROOT, "profiles", name)))
+        except (OSError, ValueError):
+            continue
+        k = d.get("kernels", {}).get(f"c{config}_p{0 if precision == 'double' else 1}")
+        if k:
+            return dict(k, source=f"profiles/{name}")
+    return None
+
+
+def kernel_time(ctx, step, flush, k):
+    """Average Tersoff-kernel duration: CUDA events bracket every launch on the
+    launch stream (tb_profile)."""
     import ctypes
     import torch
-    import torch.distributed as dist
-    ws, rank, local = dist_setup()
-    local = local % torch.cuda.device_count()
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
-    from paper_1710_00882_b200 import _native, decomp, structures
-    backend = os.environ.get("BENCH_DIST_BACKEND", "nccl")  # gloo: single-GPU smoke test only
-    if backend == "nccl":
-        dist.init_process_group("nccl", device_id=dev)
-    else:
-        dist.init_process_group(backend)
-        decomp.set_comm_device("cpu")
-    from paper_1710_00882_b200.paramfile import builtin_params
-    cells = (20 * ws, 20, 20)
-    st = structures.displace(structures.gen_diamond(cells, 5.431), 0.1, 1002)
-    table = builtin_params("Si")
-    n_total = st.natoms
-    stream = torch.cuda.Stream(device=dev)
-    torch.cuda.set_stream(stream)
-    d = decomp.SlabDecomposition(st.box.lengths, st.box.periodic, table.r_cut + 0.3, ws)
-    dom = decomp.scatter_state(d, st, rank, dev)
-    eng = decomp.B200Engine(table, 0.3, device=local, precision=args.precision,
-                            scatter=args.scatter)
-    ff = decomp.DecomposedForceField(d, st.box, eng, rank, ws, dev)
-    dom = ff.rebuild(dom)
-    for _ in range(max(3, args.warmup)):
-        f, res = ff(dom)
-    torch.cuda.synchronize()
-    # the whole decomposed step (halo P2P, Tersoff kernel + finalize, reverse
-    # forces, all-reduce) as one CUDA graph: NCCL ops are capturable
-    # (tools/nccl_capture_probe.py); any capture error falls back to eager
-    launch = f"eager (Python host loop, {backend} batch_isend_irecv)"
-    graph = None
-    step_fn = lambda: ff(dom)  # noqa: E731
-    if backend == "nccl" and os.environ.get("BENCH_DD_GRAPH", "1") == "1":
-        try:
-            dist.barrier()
-            torch.cuda.synchronize()
-            graph = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(graph, stream=stream):
-                f_g, res_g = ff(dom)
-            graph.replay()
-            torch.cuda.synchronize()
-            step_fn = lambda: (graph.replay(), (f_g, res_g))[1]  # noqa: E731
-            launch = ("one CUDA graph per step: halo P2P + Tersoff kernel + finalize + reverse "
-                      "forces + all-reduce (NCCL ops captured)")
-        except Exception as e:  # noqa: BLE001
-            graph = None
-            launch = f"eager (graph capture failed: {str(e)[:80]})"
-            torch.cuda.synchronize()
-        # every rank must take the same path (their NCCL call sequences must match)
-        ok = torch.tensor([1 if graph is not None else 0], dtype=torch.int32,
-                          device=dev if backend == "nccl" else "cpu")
-        dist.all_reduce(ok, op=dist.ReduceOp.MIN)
-        if int(ok.item()) == 0 and graph is not None:
-            del graph
-            graph = None
-            step_fn = lambda: ff(dom)  # noqa: E731
-            launch = "eager (graph capture failed on another rank)"
-    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
-    k = args.steps
-    starts = [torch.cuda.Event(enable_timing=True) for _ in range(k)]
-    ends = [torch.cuda.Event(enable_timing=True) for _ in range(k)]
-    sampler = ClockSampler(local)
-    dist.barrier()
-    torch.cuda.synchronize()
-    with sampler:
-        for s_ in range(k):
-            flush.zero_()
-            starts[s_].record(stream)
-            f, res = step_fn()
-            ends[s_].record(stream)
-        torch.cuda.synchronize()
-    t_local = sum(a.elapsed_time(b) for a, b in zip(starts, ends)) / 1e3
-    comm = "cpu" if backend != "nccl" else dev
-    t = torch.tensor([t_local], dtype=torch.float64, device=comm)
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    t_max = float(t[0])
-    value = n_total * k / t_max
-    energy = float(res[0])
-    # kernel share on this rank
-    lib, ctx = eng.ctx.lib, eng.ctx
+    lib = ctx.lib
     lib.tb_profile(ctx.handle, 1)
-    for _ in range(min(k, 100)):
-        flush.zero_()
-        f, res = ff(dom)
+    for _ in range(k):
+        if flush is not None:
+            flush.zero_()
+        step()
     torch.cuda.synchronize()
     lib.tb_profile(ctx.handle, 0)
     tot, cnt = ctypes.c_double(), ctypes.c_int64()
     ctx.check(lib.tb_profile_read(ctx.handle, ctypes.byref(tot), ctypes.byref(cnt)))
-    kern_ms = tot.value / max(cnt.value, 1)
-    # rank 0's algorithmic flops (its owned rows) for the kernel roofline
-    roof = {"bound": "fp64" if args.precision == "double" else "fp32",
-            "kernel_ms_rank0": kern_ms, "achieved": None, "peak": None,
-            "unit": "TFLOP/s", "frac": None, "traffic": None}
-    if rank == 0:
-        pcode = _native.PRECISION[args.precision]
-        st_t = torch.zeros(_native.NSTATS, dtype=torch.int64, device=dev)
-        r8 = torch.zeros(8, dtype=torch.float64, device=dev)
-        pos_l = dom._pos_l  # [owned | ghosts] of the last step (no collective on one rank)
-        f_t = torch.empty((pos_l.shape[0], 3), dtype=torch.float64, device=dev)
-        rc = lib.tb_compute_device(ctx.handle, eng.nl.handle, _native.ptr(pos_l),
-                                   _native.ptr(dom._sp_l), float(table.r_cut), pcode,
-                                   _native.SCATTER[args.scatter], _native.ptr(f_t), None,
-                                   _native.ptr(r8), _native.ptr(st_t))
-        torch.cuda.synchronize()
-        pk = measure_peak(lib, ctx, pcode)
-        if rc == 0 and pk:
-            stv = st_t.cpu().numpy()
-            flops = algorithmic_flops(stv) if pcode == 0 else algorithmic_flops32(stv)
-            ach = flops / (kern_ms * 1e-3) / 1e12
-            roof.update({"achieved": ach, "peak": pk["tflops"], "frac": ach / pk["tflops"],
-                         "flops_per_launch_rank0": flops, "peak_source": pk["source"],
-                         "kernel": "k_tersoff_warp (rank 0: its owned rows of [owned | ghosts])"})
-    # e2e: owned positions from pinned host memory each step, forces back
-    pos_h = torch.empty(tuple(dom.pos.shape), dtype=torch.float64).pin_memory()
-    pos_h.copy_(dom.pos)
-    f_h = torch.empty(tuple(dom.pos.shape), dtype=torch.float64).pin_memory()
-    ke = max(10, min(k, args.e2e_steps))
-    dist.barrier()
-    torch.cuda.synchronize()
-    t0 = time.perf_counter()
-    for _ in range(ke):
-        dom.pos.copy_(pos_h, non_blocking=True)
-        f, res = step_fn()
-        f_h.copy_(f, non_blocking=True)
-        e_host = float(res[0])
-    torch.cuda.synchronize()
-    te = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=comm)
-    dist.all_reduce(te, op=dist.ReduceOp.MAX)
-    line = {
-        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": k,
-        "warmup": args.warmup, "ms_per_step": t_max * 1e3 / k, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None,
-        "dtype": "f64" if args.precision == "double" else "f32/f64", "data": "synthetic",
-        "config": {"workload": f"config 2 per GPU, weak scaling: {cells[0]}x{cells[1]}x{cells[2]}"
-                               f"-cell Si diamond ({n_total} atoms), slab decomposition along x, "
-                               f"{backend.upper()} P2P halo + reverse forces + all-reduce per step",
-                   "backend": backend,
-                   "atoms": n_total, "atoms_per_gpu": n_total // ws,
-                   "precision": args.precision, "scatter": args.scatter,
-                   "parallelism": f"spatial slabs x{ws}",
-                   "l2": "flushed between timed steps (256 MiB write)",
-                   "launch": launch},
-        "e2e": {"value": n_total * ke / float(te[0]), "unit": UNIT, "steps": ke,
-                "h2d_bytes_per_step": int(dom.pos.numel() * 8),
-                "d2h_bytes_per_step": int(dom.pos.numel() * 8 + 8),
-                "path": "decomp.DecomposedForceField per rank, pinned host positions in, "
-                        "forces out, energy to host"},
-        "gpu_launches": 2 * k,
-        "roofline": roof,
-        "clocks": sampler.summary(), "energy_eV": energy,
-    }
-    if rank == 0:
-        print(json.dumps(line, default=_jsonable), flush=True)
-    dist.barrier()
-    if graph is not None:
-        # tearing the process group down under a live captured graph can
-        # block at exit: release the graph, then leave without the teardown
-        del graph, step_fn
-        torch.cuda.synchronize()
-        sys.stdout.flush()
-        os._exit(0)
-    dist.destroy_process_group()
+    return tot.value / max(cnt.value, 1)
 
 
-def gpu_arm(args):
-    import ctypes
-    import torch
-    ws, rank, local = dist_setup()
-    if ws > 1 and not args.replicas:
-        return gpu_arm_decomposed(args)
-    dev = local if ws > 1 else 0
-    torch.cuda.set_device(dev)
-    if ws > 1:
-        import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
-    import paper_1710_00882_b200 as B
-    from paper_1710_00882_b200 import _native, structures
-    from paper_1710_00882_b200.paramfile import builtin_params
+class Evaluator:
+    """One configuration resident on one GPU: positions/species/list in HBM,
+    the evaluation (tb_compute_device: Tersoff kernel + finalize) as a graph."""
 
-    state, tname = structures.config(args.config)
-    table = builtin_params(tname)
-    n = state.natoms
-    stream = torch.cuda.Stream(device=dev)   # one explicit stream for torch and the C ABI
-    torch.cuda.set_stream(stream)
-    ctx = _native.default_context(dev)
-    ctx.set_stream(stream.cuda_stream)
-    ctx.set_table(table)
-    lib = ctx.lib
+    def __init__(self, B, _native, ctx, state, table, dev, scatter, stream):
+        import torch
+        self.ctx, self.native, self.table, self.stream = ctx, _native, table, stream
+        ctx.set_table(table)
+        n = self.n = state.natoms
+        d = torch.device("cuda", dev)
+        self.pos = torch.from_numpy(state.positions).to(d).contiguous()
+        self.species = torch.from_numpy(state.species.astype(np.int32)).to(d)
+        self.forces = torch.empty((n, 3), dtype=torch.float64, device=d)
+        self.result = torch.zeros(8, dtype=torch.float64, device=d)
+        self.stats = torch.zeros(_native.NSTATS, dtype=torch.int64, device=d)
 
-    pos = torch.from_numpy(state.positions).to(f"cuda:{dev}").contiguous()
-    species = torch.from_numpy(state.species.astype(np.int32)).to(f"cuda:{dev}")
-    forces = torch.empty((n, 3), dtype=torch.float64, device=pos.device)
-    per_atom = torch.empty(n, dtype=torch.float64, device=pos.device)
-    result = torch.zeros(8, dtype=torch.float64, device=pos.device)
-    stats = torch.zeros(_native.NSTATS, dtype=torch.int64, device=pos.device)
+        class DS:
+            pass
+        ds = DS()
+        ds.positions, ds.species, ds.box = self.pos, self.species, state.box
+        self.nl = B.build_neighbor_list(ds, table.r_cut, 0.3, device=dev)
+        self.scat = _native.SCATTER[scatter]
 
-    class DevState:
-        pass
-
-    ds = DevState()
-    ds.positions, ds.species, ds.box = pos, species, state.box
-    nl = B.build_neighbor_list(ds, table.r_cut, 0.3, device=dev)
-    scat = _native.SCATTER[args.scatter]
-    P = _native.ptr
-
-    def step(precision, with_stats=False):
-        rc = lib.tb_compute_device(ctx.handle, nl._nl.handle, P(pos), P(species),
-                                   float(table.r_cut), precision, scat, P(forces),
-                                   P(per_atom), P(result), P(stats) if with_stats else None)
+    def step(self, precision, with_stats=False):
+        P, ctx = self.native.ptr, self.ctx
+        rc = ctx.lib.tb_compute_device(ctx.handle, self.nl._nl.handle, P(self.pos),
+                                       P(self.species), float(self.table.r_cut), precision,
+                                       self.scat, P(self.forces), None, P(self.result),
+                                       P(self.stats) if with_stats else None)
         if rc:
             ctx.check(rc, "tb_compute_device")
 
-    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=pos.device)
+    def counts(self, precision):
+        import torch
+        self.step(precision, with_stats=True)
+        torch.cuda.synchronize()
+        return self.stats.cpu().numpy().astype(np.int64)
 
-    def capture(precision):
-        """The evaluation (Tersoff kernel + finalize) as one CUDA graph."""
+    def capture(self, precision):
+        import torch
         for _ in range(3):
-            step(precision)
+            self.step(precision)
         torch.cuda.synchronize()
         g = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(g, stream=stream):
-            step(precision)
-        ctx.set_stream(stream.cuda_stream)
+        with torch.cuda.graph(g, stream=self.stream):
+            self.step(precision)
+        self.ctx.set_stream(self.stream.cuda_stream)
         torch.cuda.synchronize()
         return g
 
-    def timed_graph(g, k):
-        """k steps, L2 flushed between steps (outside the event bracket)."""
+    def timed(self, g, k, flush=None):
+        import torch
         starts = [torch.cuda.Event(enable_timing=True) for _ in range(k)]
         ends = [torch.cuda.Event(enable_timing=True) for _ in range(k)]
         torch.cuda.synchronize()
-        if ws > 1:
-            torch.distributed.barrier()
         for s_ in range(k):
-            flush.zero_()
-            starts[s_].record(stream)
+            if flush is not None:
+                flush.zero_()
+            starts[s_].record(self.stream)
             g.replay()
-            ends[s_].record(stream)
+            ends[s_].record(self.stream)
         torch.cuda.synchronize()
-        return sum(a_.elapsed_time(b_) for a_, b_ in zip(starts, ends))
+        return sum(a.elapsed_time(b) for a, b in zip(starts, ends))
 
-    def kernel_time(precision, k):
-        """Average Tersoff-kernel duration (CUDA events bracketing each launch on
-        the launch stream, tb_profile), same flush protocol."""
-        lib.tb_profile(ctx.handle, 1)
-        for _ in range(k):
-            flush.zero_()
-            step(precision)
-        torch.cuda.synchronize()
-        lib.tb_profile(ctx.handle, 0)
-        tot, cnt = ctypes.c_double(), ctypes.c_int64()
-        ctx.check(lib.tb_profile_read(ctx.handle, ctypes.byref(tot), ctypes.byref(cnt)))
-        return tot.value / max(cnt.value, 1)
-
-    prec = _native.PRECISION[args.precision]
-    for _ in range(max(3, args.warmup)):
-        step(prec)
-    step(prec, with_stats=True)
-    torch.cuda.synchronize()
-    ctx.check(lib.tb_check_errors(ctx.handle), "warm-up")
-    st = stats.cpu().numpy().astype(np.int64)
-    energy0 = float(result[0])
-    g = capture(prec)
-
-    sampler = ClockSampler(dev)
-    with sampler:
-        step_ms = timed_graph(g, args.steps)
-    ctx.check(lib.tb_check_errors(ctx.handle), "timed loop")
-    t_local = step_ms / 1e3
-    if ws > 1:
-        t = torch.tensor([t_local], dtype=torch.float64, device=pos.device)
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        t_max = float(t[0])
-    else:
-        t_max = t_local
-    value = ws * n * args.steps / t_max
-
-    # roofline of the Tersoff kernel (the dominant launch of the step)
-    kern_ms = kernel_time(prec, min(args.steps, 200))
-    flops = algorithmic_flops(st) if args.precision == "double" else algorithmic_flops32(st)
-    peak = measure_peak(lib, ctx, prec) if rank == 0 else None
-    achieved = flops / (kern_ms / 1e3) / 1e12
-    traffic = None
-    prof_json = os.path.join(ROOT, "profiles", "ncu_tersoff_fp64.json")
-    if os.path.exists(prof_json):
-        try:
-            traffic = json.load(open(prof_json)).get("dram_bytes_per_launch")
-        except Exception:
-            traffic = None
-
-    extra = {}
-    if args.extras and rank == 0 and args.precision == "double":
-        # mixed precision on the same workload, against the FP32 pipe
-        gm = capture(1)
-        k2 = max(10, args.steps // 2)
-        mixed_ms = timed_graph(gm, k2)
-        mk = kernel_time(1, min(k2, 200))
-        mflops = algorithmic_flops32(st)
-        mpeak = measure_peak(lib, ctx, 1)
-        extra["mixed"] = {
-            "value": n * k2 / (mixed_ms / 1e3), "unit": UNIT, "steps": k2,
-            "ms_per_step": mixed_ms / k2, "dtype": "f32 math / f64 positions+accumulators",
-            "roofline": {"bound": "fp32", "achieved": mflops / (mk / 1e3) / 1e12,
-                         "peak": mpeak["tflops"] if mpeak else None, "unit": "TFLOP/s",
-                         "frac": (mflops / (mk / 1e3) / 1e12) / mpeak["tflops"] if mpeak else None,
-                         "kernel_ms": mk, "flops_per_launch": mflops,
-                         "peak_source": mpeak["source"] if mpeak else None}}
-        step(prec)  # restore the fp64 result buffers
-        torch.cuda.synchronize()
-
-    if args.extras and rank == 0 and args.config == 2:
-        # SURVEY 8(d) "full MD step": velocity Verlet + rebuilds amortised,
-        # BASELINE config 2 protocol, the whole run one CUDA-graph launch
-        extra["md"] = {}
-        for pname, pcode in (("double", 0), ("single", 1)):
-            r = md_measure(B, _native, ctx, state, table, dev, pcode, scat)
-            fl = algorithmic_flops(st) if pcode == 0 else algorithmic_flops32(st)
-            pk = peak if pcode == 0 else measure_peak(lib, ctx, 1)
-            r["roofline_frac"] = (fl / (r["ms_per_step"] / 1e3) / 1e12 / pk["tflops"]
-                                  if pk else None)
-            extra["md"][pname] = r
-        ctx.set_stream(stream.cuda_stream)
-        step(prec)
-        torch.cuda.synchronize()
-
-    e2e = None
-    if rank == 0:
-        e2e = e2e_arm(args, B, state, table, nl, dev)
-
-    line = {
-        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_ms / args.steps,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-        "dtype": "f64" if args.precision == "double" else "f32/f64", "data": "synthetic",
-        "config": {"workload": f"BASELINE config {args.config}: {n}-atom "
-                               f"{'Si diamond' if tname == 'Si' else tname}, one E+F+virial "
-                               f"evaluation per step (skin-list repack at r_cut, Tersoff "
-                               f"terms, force/energy/virial reduction), neighbour list built "
-                               f"outside the timed region",
-                   "atoms": n, "precision": args.precision, "scatter": args.scatter,
-                   "parallelism": f"replicas x{ws}" if ws > 1 else "single GPU",
-                   "l2": "flushed between timed steps (256 MiB write)",
-                   "launch": "each step is one CUDA-graph replay (Tersoff kernel + finalize)"},
-        "e2e": e2e,
-        "gpu_launches": 2 * args.steps,
-        "roofline": {"bound": "fp64" if args.precision == "double" else "fp32",
-                     "achieved": achieved,
-                     "peak": peak["tflops"] if peak else None, "unit": "TFLOP/s",
-                     "frac": achieved / peak["tflops"] if peak else None,
-                     "traffic": traffic,
-                     "kernel": f"k_tersoff_warp<{'double' if prec == 0 else 'float'},S=1,{args.scatter}>",
-                     "kernel_ms": kern_ms,
-                     "flops_per_launch": flops,
-                     "flop_convention": "SURVEY 8(d): reference ScalarOpt expression tree "
-                                        "charged once per live pair and live triplet; "
-                                        f"library-call weights {OP_WEIGHTS_SOURCE} "
-                                        "(profiles/roofline.json)",
-                     "flops_per_unit": {"pair": FLOPS_PAIR, "triplet": FLOPS_TRIP,
-                                        "taper": FLOPS_TAPER},
-                     "peak_source": peak["source"] if peak else None,
-                     "counts": {"live_pairs": int(st[2]), "live_triplets": int(st[3]),
-                                "taper_pairs": int(st[4]), "taper_triplets": int(st[5]),
-                                "zeta_visits": int(st[0])}},
-        "clocks": sampler.summary(),
-        "energy_eV": energy0,
-    }
-    line.update(extra)
-    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
-        v, cores, evals, el = oracle_baseline(state, table, budget_s=args.cpu_budget)
-        line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": cores, "kind": "port",
-                                "sample": f"{evals} full E+F evaluations of the {n}-atom system "
-                                          f"in {el:.1f} s (NL outside the timer); oracle/ C "
-                                          f"restatement of ScalarOpt, OpenMP {cores} threads"}
-    if rank == 0:
-        print(json.dumps(line, default=_jsonable), flush=True)
-    if ws > 1:
-        torch.distributed.barrier()
-        torch.distributed.destroy_process_group()
+    def roofline(self, precision, k, flush, peak, config):
+        """Kernel time of the timed (counter-free) instantiation and of the
+        API's counting one, algorithmic flops, ncu pipe % / traffic."""
+        pcode = self.native.PRECISION[precision]
+        st = self.counts(pcode)
+        flops = flops_for(st, precision)
+        kms = kernel_time(self.ctx, lambda: self.step(pcode), flush, k)
+        kms_api = kernel_time(self.ctx, lambda: self.step(pcode, True), flush, k)
+        ach = flops / (kms * 1e-3) / 1e12
+        prof = ncu_profile(config, precision)
+        pipe = "fp64_pipe_pct" if precision == "double" else "fma_pipe_pct"
+        return {
+            "bound": "fp64" if precision == "double" else "fp32",
+            "achieved": ach, "peak": peak["tflops"] if peak else None, "unit": "TFLOP/s",
+            "frac": ach / peak["tflops"] if peak else None,
+            "traffic": prof.get("dram_bytes") if prof else None,
+            "kernel": f"k_tersoff_warp<{'double' if pcode == 0 else 'float'},S={self.table.nspecies},atomic>",
+            "kernel_ms": kms,
+            "kernel_ms_api": kms_api,
+            "kernel_ms_note": "kernel_ms: counter-free instantiation (the timed step); "
+                              "kernel_ms_api: the instantiation compute() runs (live-pair / "
+                              "triplet counters on)",
+            "flops_per_launch": flops,
+            "flop_convention": "SURVEY 8(d): reference ScalarOpt expression tree charged once "
+                               "per live pair and live triplet; library-call weights "
+                               f"{OP_WEIGHTS_SOURCE} (profiles/roofline.json)",
+            "flops_per_unit": ({"pair": FLOPS_PAIR, "triplet": FLOPS_TRIP, "taper": FLOPS_TAPER}
+                               if precision == "double" else
+                               {"pair": FLOPS32_PAIR, "triplet": FLOPS32_TRIP,
+                                "taper": FLOPS32_TAPER}),
+            "peak_source": peak["source"] if peak else None,
+            "counts": {"live_pairs": int(st[2]), "live_triplets": int(st[3]),
+                       "taper_pairs": int(st[4]), "taper_triplets": int(st[5]),
+                       "zeta_visits": int(st[0])},
+            "ncu": ({"pipe": pipe, "pipe_pct": prof.get(pipe), "l1tex_pct": prof.get("l1tex_pct"),
+                     "issue_active_pct": prof.get("issue_active_pct"),
+                     "dram_bytes_per_launch": prof.get("dram_bytes"),
+                     "duration_us": prof.get("duration_us"), "source": prof.get("source")}
+                    if prof else None),
+        }
 
 
-def md_measure(B, _native, ctx, state, table, dev, precision, scat, steps=1000, warm=20):
-    """Device-resident NVE (tb_md_run): BASELINE config 2 protocol -- dt 1 fs,
-    skin 0.3, rebuild every 10 steps plus the skin/2 trigger -- timed with
-    CUDA events around one graph launch of `steps` steps after a `warm`-step
-    launch that captures the graph."""
+def md_measure(B, _native, ctx, state, table, dev, precision, steps, warm=20):
+    """Device-resident NVE (tb_md_run): dt 1 fs, skin 0.3, rebuild every 10
+    steps plus the skin/2 trigger, timed with CUDA events around one graph
+    launch of `steps` steps after a `warm`-step launch that captures the graph."""
     import ctypes
 
     import torch
@@ -646,7 +435,7 @@ def md_measure(B, _native, ctx, state, table, dev, precision, scat, steps=1000, 
     species = torch.from_numpy(state.species.astype(np.int32)).to(d)
     forces = torch.empty((n, 3), dtype=torch.float64, device=d)
     result = torch.zeros(8, dtype=torch.float64, device=d)
-    series = torch.zeros((steps // 100 + 1, 2), dtype=torch.float64, device=d)
+    series = torch.zeros((steps // 100 + 2, 2), dtype=torch.float64, device=d)
 
     class DS:
         pass
@@ -655,17 +444,18 @@ def md_measure(B, _native, ctx, state, table, dev, precision, scat, steps=1000, 
     ds.positions, ds.species, ds.box = pos, species, state.box
     s = torch.cuda.current_stream(d)
     ctx.set_stream(s.cuda_stream)
+    ctx.set_table(table)
     nl = B.build_neighbor_list(ds, table.r_cut, 0.3, device=dev)
     lib, P = ctx.lib, _native.ptr
     ctx.check(lib.tb_compute_device(ctx.handle, nl._nl.handle, P(pos), P(species),
-                                    float(table.r_cut), precision, scat, P(forces), None,
+                                    float(table.r_cut), precision, 0, P(forces), None,
                                     P(result), None), "tb_compute_device")
     nreb = ctypes.c_int64()
 
     def run(k):
         ctx.check(lib.tb_md_run(ctx.handle, nl._nl.handle, n, P(pos), P(vel), P(forces), P(mass),
                                 P(species), 1.0, float(ACCEL), float(table.r_cut), 0.3, 10,
-                                precision, scat, k, 100, P(series), P(result),
+                                precision, 0, k, 100, P(series), P(result),
                                 ctypes.byref(nreb)), "tb_md_run")
         return int(nreb.value)
 
@@ -682,23 +472,10 @@ def md_measure(B, _native, ctx, state, table, dev, precision, scat, steps=1000, 
     return {"value": n * steps / (ms / 1e3), "unit": UNIT, "steps": steps,
             "ms_per_step": ms / steps, "rebuilds": rebuilds,
             "rel_energy_change": abs(e1 - e0) / abs(e0),
-            "workload": f"config 2 NVE ({n} Si, 1000 K, dt 1 fs, skin 0.3, rebuild every 10 "
-                        f"steps + skin/2 trigger): velocity Verlet + device-side list rebuilds "
-                        f"+ E/F/virial per step, one CUDA-graph launch (tb_md_run)",
-            "l2": "not flushed: consecutive steps of one run",
+            "workload": f"NVE ({n} atoms, dt 1 fs, skin 0.3, rebuild every 10 steps + skin/2 "
+                        f"trigger): velocity Verlet + device-side list rebuilds + E/F/virial per "
+                        f"step, one CUDA-graph launch (tb_md_run)",
             "gpu_launches": "1 graph launch (WHILE/IF conditional nodes)"}
-
-
-def measure_peak(lib, ctx, precision):
-    """FMA-pipe peak measured on this GPU (MEASURED_PEAKS.json has no fp64/fp32
-    figure): an 8-chain FMA loop over all SMs, best of 5 (tb_measure_peak)."""
-    import ctypes
-    out = ctypes.c_double()
-    if lib.tb_measure_peak(ctx.handle, int(precision), ctypes.byref(out)) != 0:
-        return None
-    return {"tflops": out.value,
-            "source": f"measured {'DFMA' if precision == 0 else 'FFMA'} loop in bench.py "
-                      f"(tb_measure_peak; MEASURED_PEAKS.json has no fp64/fp32 entry)"}
 
 
 def e2e_arm(args, B, state, table, nl, dev):
@@ -717,12 +494,11 @@ def e2e_arm(args, B, state, table, nl, dev):
     hs = HostState()
     hs.positions, hs.species, hs.box = pos_h, sp_h, state.box
     variant = B.make_variant("B200", precision=args.precision, scatter=args.scatter)
-    # caller-owned pinned result buffers (compute(..., out=)): D2H by DMA
     out = B.ForceEnergyResult(torch.empty((n, 3), dtype=torch.float64).pin_memory().numpy(),
                               0.0, torch.empty(n, dtype=torch.float64).pin_memory().numpy(), {})
-    for _ in range(3):
+    for _ in range(2):
         B.compute(hs, nl, table, variant, out=out)
-    k = max(10, min(args.steps, args.e2e_steps))
+    k = max(3, min(args.steps, args.e2e_steps))
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     for _ in range(k):
@@ -738,27 +514,312 @@ def e2e_arm(args, B, state, table, nl, dev):
                     "energy/virial/stats to host, wall clock per call (synchronous)"}
 
 
+# ---------------------------------------------------------------------------
+# N = 1
+# ---------------------------------------------------------------------------
+
+def gpu_arm(args):
+    import torch
+    import paper_1710_00882_b200 as B
+    from paper_1710_00882_b200 import _native, structures
+    from paper_1710_00882_b200.paramfile import builtin_params
+    dev = 0
+    torch.cuda.set_device(dev)
+    state, tname, cfg = make_workload(args, 1)
+    table = builtin_params(tname)
+    n = state.natoms
+    stream = torch.cuda.Stream(device=dev)  # one explicit stream for torch and the C ABI
+    torch.cuda.set_stream(stream)
+    ctx = _native.default_context(dev)
+    ctx.set_stream(stream.cuda_stream)
+    ev = Evaluator(B, _native, ctx, state, table, dev, args.scatter, stream)
+    lib = ctx.lib
+    prec = _native.PRECISION[args.precision]
+    big = n * 40 > 256 * 1024 * 1024  # working set far above L2: no flush needed
+    flush = None if big else torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32,
+                                         device=ev.pos.device)
+    for _ in range(max(3, args.warmup)):
+        ev.step(prec)
+    torch.cuda.synchronize()
+    ctx.check(lib.tb_check_errors(ctx.handle), "warm-up")
+    g = ev.capture(prec)
+    energy0 = float(ev.result[0])
+    sampler = ClockSampler(dev)
+    with sampler:
+        step_ms = ev.timed(g, args.steps, flush)
+    ctx.check(lib.tb_check_errors(ctx.handle), "timed loop")
+    value = n * args.steps / (step_ms / 1e3)
+    peak = measure_peak(lib, ctx, prec)
+    kk = max(5, min(args.steps, 50 if big else 200))
+    roof = ev.roofline(args.precision, kk, flush, peak, cfg["config"])
+    extra = {}
+    if args.extras:
+        if args.precision == "double":
+            # mixed precision on the same workload, against the FP32 pipe
+            gm = ev.capture(1)
+            k2 = max(5, args.steps // 2)
+            mixed_ms = ev.timed(gm, k2, flush)
+            mpeak = measure_peak(lib, ctx, 1)
+            extra["mixed"] = {
+                "value": n * k2 / (mixed_ms / 1e3), "unit": UNIT, "steps": k2,
+                "ms_per_step": mixed_ms / k2, "dtype": "f32 math / f64 positions+accumulators",
+                "roofline": ev.roofline("single", kk, flush, mpeak, cfg["config"])}
+            del gm
+        ev.step(prec)
+        torch.cuda.synchronize()
+        if cfg["config"] != 2:
+            # the round-1 headline (config 2, 64k atoms) beside it
+            st2, tn2 = structures.config(2)
+            ev2 = Evaluator(B, _native, ctx, st2, builtin_params(tn2), dev, args.scatter, stream)
+            fl2 = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=ev.pos.device)
+            g2 = ev2.capture(prec)
+            k2 = max(20, args.steps)
+            ms2 = ev2.timed(g2, k2, fl2)
+            extra["config2"] = {"value": st2.natoms * k2 / (ms2 / 1e3), "unit": UNIT,
+                                "steps": k2, "ms_per_step": ms2 / k2,
+                                "l2": "flushed between steps (256 MiB write)",
+                                "roofline": ev2.roofline(args.precision, 100, fl2, peak, 2)}
+            del g2, ev2, fl2
+            ctx.set_table(table)
+        torch.cuda.synchronize()
+        extra["md"] = {}
+        st2, tn2 = structures.config(2)
+        extra["md"]["config2_fp64"] = md_measure(B, _native, ctx, st2, builtin_params(tn2), dev,
+                                                 0, 1000)
+        extra["md"]["config2_mixed"] = md_measure(B, _native, ctx, st2, builtin_params(tn2), dev,
+                                                  1, 1000)
+        if cfg["config"] == 5 and args.md5_steps > 0:
+            extra["md"]["config5_fp64"] = md_measure(B, _native, ctx, state, table, dev, 0,
+                                                     args.md5_steps, warm=10)
+        ctx.set_stream(stream.cuda_stream)
+        ctx.set_table(table)
+    e2e = e2e_arm(args, B, state, table, ev.nl, dev)
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 1,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_ms / args.steps,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": "f64" if args.precision == "double" else "f32/f64", "data": "synthetic",
+        "config": cfg,
+        "details": {"scatter": args.scatter,
+                    "l2": ("working set > L2 (no flush)" if big
+                           else "flushed between timed steps (256 MiB write)"),
+                    "launch": "each step is one CUDA-graph replay (Tersoff kernel + finalize)"},
+        "e2e": e2e,
+        "gpu_launches": 2 * args.steps,
+        "roofline": roof,
+        "clocks": sampler.summary(),
+        "energy_eV": energy0,
+    }
+    line.update(extra)
+    if not args.no_cpu_baseline:
+        v, cores, evals, el = oracle_timing(state, table, args.cpu_budget, 1000, args.precision)
+        line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": cores, "kind": "port",
+                                "sample": f"{evals} full E+F evaluations of the {n}-atom system "
+                                          f"in {el:.1f} s (NL outside the timer); oracle/ C "
+                                          f"restatement of ScalarOpt, OpenMP {cores} threads"}
+    print(json.dumps(line, default=_jsonable), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# N > 1: slab decomposition
+# ---------------------------------------------------------------------------
+
+def gpu_arm_decomposed(args):
+    """N > 1 (torchrun): decomp.DomainMD per rank, NCCL P2P halos; the
+    evaluation step (halo + owned rows + reverse halo + all-reduce) as one
+    CUDA graph; device-timed per rank, max over ranks."""
+    import torch
+    import torch.distributed as dist
+    ws, rank, local = dist_setup()
+    local = local % torch.cuda.device_count()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    from paper_1710_00882_b200 import decomp
+    from paper_1710_00882_b200.paramfile import builtin_params
+    backend = os.environ.get("BENCH_DIST_BACKEND", "nccl")  # gloo: single-GPU functional run
+    if backend == "nccl":
+        dist.init_process_group("nccl", device_id=dev)
+    else:
+        dist.init_process_group(backend)
+    comm = decomp.Comm(rank, ws, route=None if backend == "nccl" else "cpu")
+    red_dev = dev if backend == "nccl" else "cpu"
+    state, tname, cfg = make_workload(args, ws)
+    table = builtin_params(tname)
+    n_total = state.natoms
+    stream = torch.cuda.Stream(device=dev)
+    torch.cuda.set_stream(stream)
+    md = decomp.decompose(state, table, rank, ws, comm, device=local, precision=args.precision,
+                          scatter=args.scatter, dt=1.0, rebuild_every=10)
+    eng = md.eng
+    md.rebuild()
+    stats = torch.zeros(8, dtype=torch.int64, device=dev)
+    md.evaluate(stats)
+    torch.cuda.synchronize()
+    energy = float(md.result[0])
+    st_h = stats.cpu().numpy()
+    for _ in range(max(3, args.warmup)):
+        md.evaluate()
+    torch.cuda.synchronize()
+    launch = f"eager (Python host loop, {backend} batch_isend_irecv)"
+    graph = None
+    step_fn = md.evaluate
+    if backend == "nccl" and os.environ.get("BENCH_DD_GRAPH", "1") == "1":
+        try:
+            dist.barrier()
+            torch.cuda.synchronize()
+            graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(graph, stream=stream):
+                md.evaluate()
+            eng.ctx.set_stream(stream.cuda_stream)
+            graph.replay()
+            torch.cuda.synchronize()
+            step_fn = graph.replay
+            launch = ("one CUDA graph per step: position halo (NCCL P2P) + Tersoff kernel + "
+                      "finalize + reverse halo + reverse add + all-reduce")
+        except Exception as e:  # noqa: BLE001
+            graph = None
+            launch = f"eager (graph capture failed: {str(e)[:80]})"
+            eng.ctx.set_stream(stream.cuda_stream)
+            torch.cuda.synchronize()
+        ok = torch.tensor([1 if graph is not None else 0], dtype=torch.int32, device=dev)
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+        if int(ok.item()) == 0 and graph is not None:
+            del graph
+            graph = None
+            step_fn = md.evaluate
+            launch = "eager (graph capture failed on another rank)"
+    k = args.steps
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(k)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(k)]
+    sampler = ClockSampler(local)
+    dist.barrier()
+    torch.cuda.synchronize()
+    with sampler:
+        for s_ in range(k):
+            starts[s_].record(stream)
+            step_fn()
+            ends[s_].record(stream)
+        torch.cuda.synchronize()
+    t_local = sum(a.elapsed_time(b) for a, b in zip(starts, ends)) / 1e3
+    t = torch.tensor([t_local], dtype=torch.float64, device=red_dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    t_max = float(t[0])
+    value = n_total * k / t_max
+    # Tersoff kernel of this rank (its owned rows of [owned | ghosts])
+    prec = eng.native.PRECISION[args.precision]
+    kern_ms = kernel_time(eng.ctx, lambda: eng.compute(md.result), None, min(k, 20))
+    peak = measure_peak(eng.ctx.lib, eng.ctx, prec) if rank == 0 else None
+    flops = flops_for(st_h, args.precision)
+    ach = flops / (kern_ms * 1e-3) / 1e12
+    roof = {"bound": "fp64" if prec == 0 else "fp32", "achieved": ach,
+            "peak": peak["tflops"] if peak else None, "unit": "TFLOP/s",
+            "frac": ach / peak["tflops"] if peak else None, "traffic": None,
+            "kernel": "k_tersoff_warp (rank 0: its owned rows of [owned | ghosts])",
+            "kernel_ms": kern_ms, "flops_per_launch": flops,
+            "peak_source": peak["source"] if peak else None}
+    counts = eng.counts()
+    # e2e: owned positions from pinned host memory each step, owned forces back
+    n_own = int(counts[0])
+    pos_h = torch.empty((n_own, 3), dtype=torch.float64).pin_memory()
+    pos_v = eng._view(0, 0, n_own, 3)
+    f_v = eng._view(2, 0, n_own, 3)
+    pos_h.copy_(pos_v)
+    f_h = torch.empty((n_own, 3), dtype=torch.float64).pin_memory()
+    ke = max(3, min(k, args.e2e_steps))
+    dist.barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(ke):
+        pos_v.copy_(pos_h, non_blocking=True)
+        res = step_fn() if graph is None else (step_fn(), md.result)[1]
+        f_h.copy_(f_v, non_blocking=True)
+        e_host = float(res[0])
+    torch.cuda.synchronize()
+    te = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=red_dev)
+    dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    # decomposed NVE steps (migration, cross-rank trigger, halos), eager
+    md_line = None
+    if args.extras and args.dd_md_steps > 0:
+        if graph is not None:
+            del graph
+            graph = None
+        dist.barrier()
+        torch.cuda.synchronize()
+        md.setup()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        reb0 = md.rebuilds
+        a.record(stream)
+        for _ in range(args.dd_md_steps):
+            r = md.step()
+        b.record(stream)
+        torch.cuda.synchronize()
+        tm = torch.tensor([a.elapsed_time(b) / 1e3], dtype=torch.float64, device=red_dev)
+        dist.all_reduce(tm, op=dist.ReduceOp.MAX)
+        md_line = {"value": n_total * args.dd_md_steps / float(tm[0]), "unit": UNIT,
+                   "steps": args.dd_md_steps, "ms_per_step": float(tm[0]) * 1e3 / args.dd_md_steps,
+                   "rebuilds": md.rebuilds - reb0, "e_total": float(r[0] + r[7]),
+                   "workload": "decomposed velocity-Verlet NVE (dt 1 fs, skin 0.3, rebuild every "
+                               "10 steps + skin/2 trigger on the max drift over ranks, migration "
+                               "+ ghost rebuild at each rebuild), eager host loop, one drift "
+                               "all-reduce + one result all-reduce per step"}
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": k,
+        "warmup": args.warmup, "ms_per_step": t_max * 1e3 / k, "higher_is_better": True,
+        "scaling": "weak" if cfg["scaling"] == "weak" else "strong", "vs_baseline": None,
+        "dtype": "f64" if args.precision == "double" else "f32/f64", "data": "synthetic",
+        "config": cfg,
+        "details": {"backend": backend, "scatter": args.scatter, "launch": launch,
+                    "atoms_per_gpu": n_total / ws,
+                    "rank0": {"owned": int(counts[0]), "ghosts": int(counts[1] + counts[2]),
+                              "send_rows": int(counts[3] + counts[4])},
+                    "l2": "working set > L2 (no flush)"},
+        "e2e": {"value": n_total * ke / float(te[0]), "unit": UNIT, "steps": ke,
+                "h2d_bytes_per_step": int(n_own * 24), "d2h_bytes_per_step": int(n_own * 24 + 8),
+                "path": "decomp.DomainMD.evaluate per rank, pinned host owned positions in, "
+                        "owned forces out, energy to host (rank 0's bytes)"},
+        "gpu_launches": 4 * k,
+        "roofline": roof,
+        "clocks": sampler.summary(), "energy_eV": energy, "energy_eV_e2e": e_host,
+    }
+    if md_line:
+        line["md"] = {"decomposed_fp64" if prec == 0 else "decomposed_mixed": md_line}
+    if rank == 0:
+        print(json.dumps(line, default=_jsonable), flush=True)
+    dist.barrier()
+    if graph is not None:
+        del graph
+        torch.cuda.synchronize()
+        sys.stdout.flush()
+        os._exit(0)
+    dist.destroy_process_group()
+
+
 def main():
     ap = argparse.ArgumentParser(description=__doc__.split("\n")[0])
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=2000)
-    ap.add_argument("--warmup", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
-    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--config", type=int, default=5)
+    ap.add_argument("--scaling", choices=["strong", "weak"], default="strong",
+                    help="N>1: config 5 at fixed size, or 2,097,152 atoms per GPU")
     ap.add_argument("--precision", choices=["double", "single"], default="double")
-    ap.add_argument("--precision-ref", dest="precision_ref", default="double")
     ap.add_argument("--scatter", choices=["atomic", "gather"], default="atomic")
-    ap.add_argument("--e2e-steps", type=int, default=300)
+    ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--cpu-budget", type=float, default=12.0)
+    ap.add_argument("--ref-budget", type=float, default=60.0)
+    ap.add_argument("--md5-steps", type=int, default=200)
+    ap.add_argument("--dd-md-steps", type=int, default=50)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-extras", dest="extras", action="store_false")
-    ap.add_argument("--replicas", action="store_true",
-                    help="N>1: independent replicas instead of the slab decomposition")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
+    ws, _, _ = dist_setup()
     if args.impl == "reference":
         reference_arm(args)
+    elif ws > 1:
+        gpu_arm_decomposed(args)
     else:
         gpu_arm(args)
 

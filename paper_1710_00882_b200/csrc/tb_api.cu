@@ -389,10 +389,9 @@ extern "C" int tb_set_params(tb_context *ctx, int nspecies, const double *pair_m
   if (nspecies < 1 || nspecies > SMAX)
     return fail(ctx, TB_ERR_CONFIG, "the B200 kernels support 1..%d species, got %d", SMAX,
                 nspecies);
-  int S = nspecies;
-  ctx->S = S;
-  ctx->pair_mat.assign(pair_mat, pair_mat + 8 * S * S);
-  ctx->trip_mat.assign(trip_mat, trip_mat + 8 * S * S * S);
+  const int S = nspecies;
+  // validate everything before touching the context (a refused table leaves
+  // the previous one in place)
   double rc = 0.0;
   bool lam3 = false;
   for (int q = 0; q < S * S * S; ++q) {
@@ -402,6 +401,22 @@ extern "C" int tb_set_params(tb_context *ctx, int nspecies, const double *pair_m
     if (!(r[7] == 1.0 || r[7] == 3.0))
       return fail(ctx, TB_ERR_CONFIG, "m must be 1 or 3, got %g", r[7]);
   }
+  // the fp64 kernel's fast exp / log domains (tb_fastmath.h): exp(-lambda r)
+  // for r < R + D and log(beta zeta) for zeta >= 1e-30 -- no physical table
+  // comes near these bounds; others are refused instead of silently rounded
+  for (int q = 0; q < S * S; ++q) {
+    const double *r = pair_mat + 8 * q;
+    const double reach = r[0] + r[1];
+    if (!(std::fabs(r[3]) * reach <= 700.0 && std::fabs(r[5]) * reach <= 700.0))
+      return fail(ctx, TB_ERR_CONFIG,
+                  "lambda1 %g / lambda2 %g times the cutoff %g exceeds the kernel's exp range", r[3],
+                  r[5], reach);
+    if (!(r[6] == 0.0 || r[6] >= 1e-250))
+      return fail(ctx, TB_ERR_CONFIG, "beta must be 0 or in [1e-250, inf), got %g", r[6]);
+  }
+  ctx->S = S;
+  ctx->pair_mat.assign(pair_mat, pair_mat + 8 * S * S);
+  ctx->trip_mat.assign(trip_mat, trip_mat + 8 * S * S * S);
   ctx->lam3 = lam3;
   ctx->r_cut = rc;
   ctx->param_version += 1;

@@ -54,11 +54,15 @@ struct Tables {
 };
 
 // ---- transcendental wrappers (overloads keep the templates readable) ----
-__device__ __forceinline__ double t_exp(double x) { return tb_exp(x); }
+__device__ __forceinline__ double t_exp(double x) { return tb_exp_fast(x); }
+// exp of an argument no table bound keeps in range (eta log(beta zeta), the
+// bond-order exponent, (lam3 t)^m): full-range fp64 exp
+__device__ __forceinline__ double t_exp_any(double x) { return tb_exp(x); }
 // mixed mode: MUFU-based exp2/log2 (relative error ~2^-22 plus the argument
 // rounding), well inside the 1e-5 force tolerance of the mixed mode
 __device__ __forceinline__ float t_exp(float x) { return __expf(x); }
-__device__ __forceinline__ double t_log(double x) { return tb_log(x); }
+__device__ __forceinline__ float t_exp_any(float x) { return __expf(x); }
+__device__ __forceinline__ double t_log(double x) { return tb_log_fast(x); }
 __device__ __forceinline__ float t_log(float x) { return __logf(x); }
 __device__ __forceinline__ double t_log1p(double x) { return tb_log1p(x); }
 __device__ __forceinline__ float t_log1p(float x) { return log1pf(x); }
@@ -70,9 +74,7 @@ __device__ __forceinline__ float t_rcp(float x) {
   asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
   return r;
 }
-// 1/x for an unbounded x (zeta (1 + (beta zeta)^eta) of an arbitrary table)
-__device__ __forceinline__ double t_rcp_any(double x) { return tb_rcp_guarded(x); }
-__device__ __forceinline__ float t_rcp_any(float x) { return t_rcp(x); }
+
 
 // f_C and dF_C/dr with inclusive exact plateaus (potential.py:167-175).
 // Returns false when r >= R + D (exactly zero contribution).
@@ -110,10 +112,10 @@ template <class T>
 __device__ __forceinline__ void lam3_term(T dr, const TripP<T> &p, T &ex, T &darg) {
   T t = p.lam3 * dr;
   if (p.m == 3) {
-    ex = t_exp(t * t * t);
+    ex = t_exp_any(t * t * t);
     darg = p.lam3x3 * (t * t);
   } else {
-    ex = t_exp(t);
+    ex = t_exp_any(t);
     darg = p.lam3;
   }
 }
@@ -137,15 +139,23 @@ __device__ __forceinline__ void pair_part_fc(T r, T zeta, const PairP<T> &p, T f
   } else {
     // u = t^eta, b = (1+u)^(-1/2eta), and with t^(eta-1) = u/t, t = beta zeta:
     //   db/dzeta = -beta/2 t^(eta-1) (1+u)^(-1/2eta-1) = -(1/2) u b / (zeta (1+u))
-    // one reciprocal serves db and the log1p correction (1/w = zeta / (zeta w))
+    // one reciprocal serves db and the log1p correction (1/w = zeta / (zeta w)).
+    // Range (any table, branch-free): x = eta log t above XBIG makes 1/u
+    // smaller than the rounding unit, so log1p(u) = x and u/(1+u) = 1 exactly
+    // in T -- no u, no overflow however large eta; below -708 u is a
+    // subnormal at most (clamped: b = 1, db ~ 1e-308/zeta).  Every exp / log
+    // argument then stays on the fast domain: -l1p/2eta >= -log(t)/2 >= -355.
+    constexpr T XBIG = sizeof(T) == 8 ? T(36) : T(17);
     const T lt = t_log(t);
-    const T u = t_exp(p.eta * lt);
+    const T x = p.eta * lt;
+    const bool big = x > XBIG;
+    const T u = t_exp(fmax(big ? T(0) : x, T(-708)));
     const T w = T(1) + u;
-    const T rzw = t_rcp_any(zeta * w);
+    const T rzw = t_rcp(big ? zeta : zeta * w);
     // log1p(u) = log(w) + (u - (w - 1)) / w, w = fl(1 + u)
-    const T l1p = t_log(w) + (u - (w - T(1))) * (zeta * rzw);
+    const T l1p = big ? x : t_log(w) + (u - (w - T(1))) * (zeta * rzw);
     b = t_exp(p.neg_half_inv_eta * l1p);
-    db = T(-0.5) * (u * b) * rzw;
+    db = T(-0.5) * (big ? b : u * b) * rzw;
   }
   T inner = fr + b * fa;
   v = fc * inner;

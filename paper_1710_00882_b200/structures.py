@@ -118,3 +118,10 @@ def config(index, small=False):
         st = displace(gen_diamond(10 if small else 128, 5.431), 0.1, 1005)
         return seed_velocities(st, 1000.0, 2005), "Si"
     raise ValueError(f"unknown configuration {index}")
+
+
+def config5_weak(n_gpus):
+    """BASELINE config 5 weak scaling: 64^3 cells (2,097,152 atoms) per GPU,
+    stacked along x (the slab axis); same sigma / temperature / seeds."""
+    st = displace(gen_diamond((64 * int(n_gpus), 64, 64), 5.431), 0.1, 1005)
+    return seed_velocities(st, 1000.0, 2005), "Si"

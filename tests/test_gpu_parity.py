@@ -277,3 +277,94 @@ def test_pinned_host_buffers_match_pageable(precision):
     pos[3, 1] = fr.positions[3, 1]
     r = B.compute(pf, nl, t, var, out=out)  # flags were reset: clean again
     assert abs(r.potential_energy - ref.potential_energy) <= 1e-12 * abs(ref.potential_energy)
+
+
+def _si_table(eta=None, beta=None):
+    """Si(C) (BASELINE) with eta / beta replaced (17-token line: m gamma lam3 c d
+    h eta beta lam2 B R D lam1 A)."""
+    tok = "Si Si Si 3 1.0 0.0 100390 16.217 -0.59825 0.78734 1.1e-6 1.7322 471.18 2.85 0.15 2.4799 1830.8".split()
+    if eta is not None:
+        tok[9] = repr(eta)
+    if beta is not None:
+        tok[10] = repr(beta)
+    return parse_params(" ".join(tok) + "\n")
+
+
+def _oracle_free(oracle_mod, pos, table):
+    fr = Frame(pos, np.ptp(pos, axis=0) + 8.0, (False, False, False))
+    fr.positions = fr.positions - fr.positions.min(axis=0) + 4.0
+    off, nb = oracle_mod.build_neighbor_list(fr.positions, fr.box.lengths, fr.box.periodic,
+                                             table.r_cut, 0.3)
+    return fr, oracle_mod.compute(fr.positions, fr.species, fr.box.lengths, fr.box.periodic,
+                                  off, nb, table)
+
+
+@pytest.mark.parametrize("case", ["tiny_zeta", "huge_u", "moderate"])
+def test_bond_order_extreme_regimes(oracle_mod, case, kernel_path):
+    # eta log(beta zeta) below -708 (u underflows: b = 1) and above the
+    # log1p(u) = x switch (u beyond 1e15): the kernel's branch-free bond order
+    # against the oracle's libm pow (potential.py:202-215), fp64 1e-10
+    if case == "tiny_zeta":
+        # Si(B)-like eta = 22.956, beta = 0.33675; the third atom sits 1e-7 A
+        # inside the cutoff: f_C ~ 3e-14, zeta ~ 1e-13, x ~ -760
+        table = _si_table(22.956, 0.33675)
+        d = 3.0 - 1e-7
+        pos = np.array([[0.0, 0, 0], [2.35, 0, 0], [d * np.cos(1.9), d * np.sin(1.9), 0]])
+    elif case == "huge_u":
+        # beta = 3, eta = 22.956 on a compact cluster: x = eta log(3 zeta) >> 36
+        table = _si_table(22.956, 3.0)
+        rng = np.random.default_rng(11)
+        pos = np.array([[0.0, 0, 0], [2.3, 0.1, 0], [0.2, 2.35, 0.1], [-0.1, 0.3, 2.3],
+                        [1.6, 1.7, 1.5], [-1.6, 1.2, -1.0]]) + rng.normal(0, 0.02, (6, 3))
+    else:
+        table = _si_table(3.0, 0.05)
+        pos = structures.gen_diamond(1).positions[:8] * 1.0
+    fr, ref = _oracle_free(oracle_mod, pos, table)
+    nl, res = gpu_eval(fr, table)
+    assert np.isfinite(res.forces).all() and np.isfinite(res.potential_energy)
+    assert abs(res.potential_energy - ref["energy"]) <= FP64_TOL * abs(ref["energy"])
+    assert rel_f(res.forces, ref["forces"]) <= FP64_TOL
+
+
+@pytest.mark.parametrize("precision", ["double", "single"])
+def test_collinear_bonds_cos_pm1(oracle_mod, precision, kernel_path):
+    # cos(theta) = -1 (a straight chain) and +1 (j and k on the same ray): the
+    # warp kernel does not clamp cos to [-1, 1] (|e_a . e_b| exceeds 1 by a few
+    # ulp at most, g is smooth there); parity with the clamping oracle
+    # (potential.py:256)
+    table = builtin_params("Si")
+    chain = np.array([[2.35 * q, 0.0, 0.0] for q in range(6)])
+    ray = np.array([[0.0, 0, 0], [2.2, 0, 0], [2.9, 0, 0], [0.0, 2.3, 0.0], [0.0, 2.9, 0.0]])
+    # (mixed: these near-equilibrium chains have net forces ~30x smaller than
+    # the pair terms that cancel into them, so the fp32 terms' relative error
+    # shows up ~30x amplified against max|F|)
+    tol = FP64_TOL if precision == "double" else 30 * MIXED_TOL
+    for pos in (chain, ray):
+        fr, ref = _oracle_free(oracle_mod, pos, table)
+        nl, res = gpu_eval(fr, table, precision=precision)
+        assert abs(res.potential_energy - ref["energy"]) <= tol * abs(ref["energy"])
+        assert rel_f(res.forces, ref["forces"]) <= tol
+
+
+def test_out_of_range_tables_are_refused():
+    # the fp64 kernel's exp / log domains: refused loudly, never rounded away
+    with pytest.raises(B.ConfigurationError, match="exp range"):
+        t = _si_table()
+        t2 = parse_params(B.serialize_params(t).replace("2.4799", "400.0"))
+        B.compute(*_tiny_frame(), t2)
+    # a refused table leaves the previous one in place
+    fr, nl = _tiny_frame()
+    good = _si_table()
+    want = B.compute(fr, nl, good).potential_energy
+    with pytest.raises(B.ConfigurationError, match="beta"):
+        B.compute(*_tiny_frame(), _si_table(beta=1e-300))
+    from paper_1710_00882_b200 import _native
+    ctx = _native.default_context(0)
+    ctx._table_key = id(good)  # as if `good` were still the uploaded table
+    assert B.compute(fr, nl, good).potential_energy == want
+
+
+def _tiny_frame():
+    fr = Frame([[0.0, 0, 0], [2.35, 0, 0]], [10.0, 10.0, 10.0], (False, False, False))
+    nl = B.build_neighbor_list(fr, 3.0, 0.3)
+    return fr, nl

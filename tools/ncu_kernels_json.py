@@ -1,6 +1,6 @@
 """Summarise the ncu raw exports of tools/ncu_kernels.sh into profiles/ JSON:
 duration, DRAM bytes and GB/s against the measured HBM peak, pipe / issue /
-L1 utilisation, lane efficiency.  Usage: python tools/ncu_kernels_json.py OUT.json"""
+L1 utilisation, lane efficiency.  Usage: python tools/ncu_kernels_json.py OUT.json [INDIR]"""
 import csv, glob, json, sys
 TS = {"ns": 1e-3, "nsecond": 1e-3, "us": 1.0, "usecond": 1.0, "ms": 1e3, "msecond": 1e3}
 BS = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
@@ -9,7 +9,8 @@ out = {"method": "ncu --set full --clock-control none, one k_tersoff_warp launch
                  "cold caches (ncu default cache control)",
        "peaks": {"dram_GBs_measured": 6552.3, "source": "MEASURED_PEAKS.json hbm_gbs"},
        "kernels": {}}
-for f in sorted(glob.glob("gpurun_out/ncu_tk_c*_p*_raw.csv")):
+indir = sys.argv[2] if len(sys.argv) > 2 else "gpurun_out"
+for f in sorted(glob.glob(f"{indir}/ncu_tk_c*_p*_raw.csv")):
     rows = list(csv.reader(open(f)))
     d, u = dict(zip(rows[0], rows[2])), dict(zip(rows[0], rows[1]))
 
