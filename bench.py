@@ -532,6 +532,8 @@ def gpu_arm(args):
     torch.cuda.set_stream(stream)
     ctx = _native.default_context(dev)
     ctx.set_stream(stream.cuda_stream)
+    if os.environ.get("TB_REPACK_MARGIN_MA"):  # experiments: live-repack margin (1/1000 A)
+        ctx.set_option(_native.OPT_REPACK_MARGIN, int(os.environ["TB_REPACK_MARGIN_MA"]))
     ev = Evaluator(B, _native, ctx, state, table, dev, args.scatter, stream)
     lib = ctx.lib
     prec = _native.PRECISION[args.precision]

@@ -88,6 +88,13 @@ int tb_set_stream(tb_context *ctx, void *stream);
  * decided, counted and their positions kept, and the exact list at the last of
  * them is rebuilt when the run ends.  0 = rebuild the exact list every time. */
 #define TB_OPT_MD_LOOSE_SKIN 4
+/* TB_OPT_REPACK_MARGIN = d: the live repack (TB_OPT_LIVE_PACK) cuts rows to
+ * r < r_cut + d/1000 A (default 1 = 0.001 A) and is redone only when some atom
+ * moved more than half of that since the last repack (decided on the device);
+ * the kernel's exact r < r_cut test keeps every term identical.  0 = repack
+ * exactly at every evaluation.  (Wider margins keep the repack across MD steps
+ * but add dead lanes: config 3 step 261 / 276 / 331 us at 1 / 10 / 50 mA.) */
+#define TB_OPT_REPACK_MARGIN 5
 int tb_set_option(tb_context *ctx, int option, int value);
 
 /* Synchronise the context's stream. */

@@ -83,6 +83,10 @@ struct tb_context {
 #endif
   double md_loose = TB_MD_LOOSE_DEFAULT;  // TB_OPT_MD_LOOSE_SKIN: extra list skin (A) of tb_md_run, 0 = off
   double list_margin = 0.25;  // TB_OPT_LIST_MARGIN
+#ifndef TB_REPACK_MARGIN_DEFAULT
+#define TB_REPACK_MARGIN_DEFAULT 0.001  // c3 step (A): 0 -> 333 us, 1e-3 -> 261, 5e-3 -> 268, 0.01 -> 276, 0.05 -> 331
+#endif
+  double repack_margin = TB_REPACK_MARGIN_DEFAULT;  // TB_OPT_REPACK_MARGIN (A)
   bool warp_per_chunk = getenv("TB_WARP_PER_CHUNK") != nullptr;
   bool no_filter = getenv("TB_NO_FILTER") != nullptr;  // disable the species-pair compute filter
   bool err_unchecked = false;     // kernels may have raised error flags nobody read yet
@@ -132,6 +136,11 @@ struct tb_nlist {
   // on the device every evaluation
   DevBuf lplan, llen, lrow, lrowj, lsorted, llanes;
   DevBuf ref_log;  // tb_md_run loose list: positions of the reference's last rebuild
+  // margin repack (TB_OPT_REPACK_MARGIN): positions of the last repack, the
+  // gate's drift word and flag; valid until the list or its filter changes
+  DevBuf lref, lgate;
+  bool lvalid = false, lfilt = false;
+  double lmargin = -1.0;
   bool fnbr_ok = false;  // fnbr matches centry (written by every filter pass since)
   int64_t lcap = 0;  // chunk capacity of llanes
   bool imported = false;  // rows from tb_nlist_import (no cell grid: no device rebuild)
@@ -273,6 +282,14 @@ static Tables<T, S> make_tables(const tb_context *ctx) {
               x.h == y.h && x.lam3 == y.lam3 && x.lam3x3 == y.lam3x3 && x.m == y.m))
           tab.gsym = 0;
       }
+  tab.ang_i = 1;
+  for (int i = 0; i < S; ++i)
+    for (int q = 0; q < S * S; ++q) {
+      const TripP<T> &x = tab.trip[i * S * S + q], &y = tab.trip[i * S * S];
+      if (!(x.gamma == y.gamma && x.gc2d2 == y.gc2d2 && x.m2gc2 == y.m2gc2 && x.d2 == y.d2 &&
+            x.h == y.h))
+        tab.ang_i = 0;
+    }
   tab.fc_same = S == 1 && ctx->pair_mat[0] == ctx->trip_mat[0] && ctx->pair_mat[1] == ctx->trip_mat[1];
   for (int q = 0; q < S * S; ++q) {
     const double *r = &ctx->pair_mat[8 * q];
@@ -367,6 +384,12 @@ extern "C" int tb_set_option(tb_context *ctx, int option, int value) {
   if (option == TB_OPT_MD_LOOSE_SKIN) {
     if (value < 0 || value > 300) return fail(ctx, TB_ERR_ARG, "loose skin %d out of range", value);
     ctx->md_loose = value / 100.0;
+    return TB_OK;
+  }
+  if (option == TB_OPT_REPACK_MARGIN) {
+    if (value < 0 || value > 1000)
+      return fail(ctx, TB_ERR_ARG, "repack margin %d mA out of range", value);
+    ctx->repack_margin = value / 1000.0;
     return TB_OK;
   }
   if (option == TB_OPT_LIST_MARGIN) {
@@ -500,7 +523,7 @@ extern "C" void tb_nlist_destroy(tb_nlist *nl) {
                     &nl->iota, &nl->lanes, &nl->hist, &nl->cpos, &nl->crow, &nl->coff,
                     &nl->centry, &nl->fnbr, &nl->fbuf, &nl->plan, &nl->scratch, &nl->lplan,
                     &nl->llen, &nl->lrow, &nl->lrowj, &nl->lsorted, &nl->llanes, &nl->ref_log,
-                    &nl->fspecies};
+                    &nl->fspecies, &nl->lref, &nl->lgate};
   for (DevBuf *b : bufs) b->release();
   md_graph_release(nl);
   delete nl;
@@ -626,6 +649,7 @@ static int build_filter(tb_context *ctx, tb_nlist *nl, const int *d_species) {
   CK(cudaMemcpyAsync(nl->fspecies.p, d_species, sizeof(int) * N, cudaMemcpyDeviceToDevice,
                      ctx->stream));
   nl->filtered = true;
+  nl->lvalid = false;
   nl->filter_species = d_species;
   nl->filter_param_version = ctx->param_version;
   nl->fbuf_zero = false;
@@ -673,6 +697,7 @@ extern "C" int tb_build_neighbors_owned(tb_context *ctx, tb_nlist *nl, int64_t n
   nl->bc = bc;
   nl->rev_valid = false;
   nl->imported = false;
+  nl->lvalid = false;
 
   // ---- grid geometry (CellList.__init__, neighbor.py:54-81) ----
   Grid g;
@@ -896,6 +921,7 @@ extern "C" int tb_nlist_import(tb_context *ctx, tb_nlist *nl, int64_t n, const i
   nl->ecap = std::max<int64_t>(m, 1);
   nl->ncell = 0;
   nl->imported = true;
+  nl->lvalid = false;
   nl->rev_valid = false;
   nl->filtered = false;
   nl->filter_species = nullptr;
@@ -1178,6 +1204,7 @@ static int live_repack(tb_context *ctx, tb_nlist *nl, const double *d_pos, doubl
   if (nl->lcap < cap) {
     CK(nl->llanes.ensure(sizeof(int4) * 32 * cap));
     nl->lcap = cap;
+    nl->lvalid = false;
   }
   DevPlan *plan = nl->lplan.as<DevPlan>();
   const int *start = filtered ? nl->coff.as<int>() : nl->offsets.as<int>();
@@ -1185,23 +1212,55 @@ static int live_repack(tb_context *ctx, tb_nlist *nl, const double *d_pos, doubl
 #define TB_LIVE_G 2  // measured at c3: G = 1/2/4/8/16 -> step 364/347/353/370/416 us
 #endif
   constexpr int G = TB_LIVE_G;  // lanes per row
-  CK(cudaMemsetAsync(plan, 0, sizeof(DevPlan), ctx->stream));
+  // Margin repack (TB_OPT_REPACK_MARGIN = delta): rows cut to r < r_cut + delta,
+  // redone only when some atom moved more than delta/2 since the last repack
+  // (a two-level Verlet list: every pair with r < r_cut now was within
+  // r_cut + delta then).  The kernel's own exact r < r_cut test picks the live
+  // set, so the terms are those of an exact repack (dead lanes add exact
+  // zeros).  The decision is made on the device (no host round trip).
+  const double margin = ctx->repack_margin;
+  const int *go = nullptr;
+  double *lref = nullptr;
+  if (margin > 0) {
+    CK(nl->lref.ensure(sizeof(double) * 3 * std::max(N, 1)));
+    CK(nl->lgate.ensure(16));
+    unsigned long long *dbits = nl->lgate.as<unsigned long long>();
+    int *gop = reinterpret_cast<int *>(dbits + 1);
+    const bool force = !nl->lvalid || nl->lmargin != margin || nl->lfilt != filtered;
+    CK(cudaMemsetAsync(dbits, 0, sizeof(unsigned long long), ctx->stream));
+    if (!force && N)
+      k_max_drift<<<std::min(nblk(N, 256), 4 * 148), 256, 0, ctx->stream>>>(
+          N, d_pos, nl->lref.as<double>(), box, dbits);
+    k_repack_gate<<<1, 128, 0, ctx->stream>>>(dbits, 0.25 * margin * margin, force ? 1 : 0, gop,
+                                               plan);
+    CK(cudaGetLastError());
+    go = gop;
+    lref = nl->lref.as<double>();
+  } else {
+    CK(cudaMemsetAsync(plan, 0, sizeof(DevPlan), ctx->stream));
+  }
+  const double cut = r_cut + std::max(margin, 0.0);
   if (filtered)
     k_live_rows<true, G><<<nblk((int64_t)N * G, 256), 256, 0, ctx->stream>>>(
-        N, d_pos, box, r_cut * r_cut, start, nl->crow.as<int>(), nl->centry.as<int>(),
-        nl->fnbr.as<int>(), nl->llen.as<int>(), nl->lrow.as<int>(), nl->lrowj.as<int>(), err);
+        N, d_pos, box, cut * cut, start, nl->crow.as<int>(), nl->centry.as<int>(),
+        nl->fnbr.as<int>(), nl->llen.as<int>(), nl->lrow.as<int>(), nl->lrowj.as<int>(), err, go,
+        lref);
   else
     k_live_rows<false, G><<<nblk((int64_t)N * G, 256), 256, 0, ctx->stream>>>(
-        N, d_pos, box, r_cut * r_cut, start, nullptr, nullptr, nl->nbr.as<int>(),
-        nl->llen.as<int>(), nl->lrow.as<int>(), nl->lrowj.as<int>(), err);
+        N, d_pos, box, cut * cut, start, nullptr, nullptr, nl->nbr.as<int>(), nl->llen.as<int>(),
+        nl->lrow.as<int>(), nl->lrowj.as<int>(), err, go, lref);
   CK(cudaGetLastError());
-  k_len_hist_plan<<<std::min(nblk(N, 256), 296), 256, 0, ctx->stream>>>(N, nl->llen.as<int>(), plan);
-  k_plan<<<1, 32, 0, ctx->stream>>>(plan, nullptr, N, 0, (int)nl->lcap);
+  k_len_hist_plan<<<std::min(nblk(N, 256), 296), 256, 0, ctx->stream>>>(N, nl->llen.as<int>(), plan,
+                                                                          go);
+  k_plan<<<1, 32, 0, ctx->stream>>>(plan, nullptr, N, 0, (int)nl->lcap, go);
   k_bucket_fill<<<nblk(N, 256), 256, 0, ctx->stream>>>(N, nl->llen.as<int>(), start,
                                                        nl->lrow.as<int>(), nl->lrowj.as<int>(),
                                                        plan, nl->lsorted.as<int>(),
-                                                       nl->llanes.as<int4>());
+                                                       nl->llanes.as<int4>(), go);
   CK(cudaGetLastError());
+  nl->lvalid = true;
+  nl->lmargin = margin;
+  nl->lfilt = filtered;
   return TB_OK;
 }
 
@@ -2047,6 +2106,7 @@ extern "C" int tb_md_run(tb_context *ctx, tb_nlist *nl, int64_t n, double *d_pos
       nl->n_empty = hp.n_empty;
       nl->lanes_used = hp.lanes_used;
       if (hp.rebuilds > 0 && scatter != TB_SCATTER_GATHER) nl->rev_valid = false;
+      nl->lvalid = false;  // the margin repack refers to the entry list
       if (hp.rebuilds > 0 && filter_wanted) nl->fbuf_zero = scatter == TB_SCATTER_GATHER;
       if (rebuilds) *rebuilds = hp.rebuilds + extra;
       return finish(tb_check_errors(ctx));
@@ -2102,6 +2162,7 @@ extern "C" int tb_nlist_rebuild_device(tb_context *ctx, tb_nlist *nl, const doub
   nl->nchunks = hp.nchunks;
   nl->n_empty = hp.n_empty;
   nl->lanes_used = hp.lanes_used;
+  nl->lvalid = false;
   nl->rev_valid = scatter == TB_SCATTER_GATHER;
   nl->fbuf_zero = filter && scatter == TB_SCATTER_GATHER;
   if (filter) nl->filter_species = d_species;

@@ -133,8 +133,8 @@ __global__ void k_plan_reset(DevPlan *__restrict__ plan, int full) {
 // (offsets = the list's CSR offsets: entries checked against the capacity;
 //  nullptr for the filtered rows, which are a subset of the list)
 __global__ void k_plan(DevPlan *__restrict__ plan, const int *__restrict__ offsets, int n,
-                       int entries_cap, int chunks_cap) {
-  if (threadIdx.x != 0) return;
+                       int entries_cap, int chunks_cap, const int *__restrict__ go = nullptr) {
+  if (threadIdx.x != 0 || (go && !*go)) return;
   int ovf = plan->overflow;
   if (offsets) {
     const int entries = offsets[n];
@@ -236,8 +236,11 @@ __global__ void __launch_bounds__(256) k_live_rows(int n, const double *__restri
                                                    const int *__restrict__ jlist,
                                                    int *__restrict__ llen, int *__restrict__ lrow,
                                                    int *__restrict__ lrowj,
-                                                   ErrFlags *__restrict__ err) {
+                                                   ErrFlags *__restrict__ err,
+                                                   const int *__restrict__ go = nullptr,
+                                                   double *__restrict__ lref = nullptr) {
   static_assert(G > 0 && G < 32 && (32 % G) == 0, "row groups tile the warp");
+  if (go && !*go) return;  // margin repack still valid (live_repack)
   const int i = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / G);
   const int lane = threadIdx.x & 31, sub = lane % G, g0 = lane - sub;
   const bool act = i < n;
@@ -249,6 +252,11 @@ __global__ void __launch_bounds__(256) k_live_rows(int n, const double *__restri
     load3(pos, i, xi);
     if (sub == 0 && !(isfinite(xi[0]) && isfinite(xi[1]) && isfinite(xi[2])))
       atomicMin(&err->nonfinite_atom, i);
+    if (lref && sub == 0) {  // positions of this repack (the next gate's drift origin)
+      lref[3 * (int64_t)i] = xi[0];
+      lref[3 * (int64_t)i + 1] = xi[1];
+      lref[3 * (int64_t)i + 2] = xi[2];
+    }
   }
   int q = 0;
   for (int k0 = b; __any_sync(0xffffffffu, act && k0 < end); k0 += G) {
@@ -285,7 +293,9 @@ __global__ void __launch_bounds__(256) k_bucket_fill(int n, const int *__restric
                                                      const int *__restrict__ lrowj,
                                                      DevPlan *__restrict__ plan,
                                                      int *__restrict__ empty_atoms,
-                                                     int4 *__restrict__ lanes) {
+                                                     int4 *__restrict__ lanes,
+                                                     const int *__restrict__ go = nullptr) {
+  if (go && !*go) return;
   __shared__ int s_cnt[34], s_base[34];
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (threadIdx.x < 34) s_cnt[threadIdx.x] = 0;
@@ -316,8 +326,25 @@ __global__ void __launch_bounds__(256) k_bucket_fill(int n, const int *__restric
     for (int k = (r + 1) * L; k < 32; ++k) dst[k] = make_int4(-1, 0, 0, L);
 }
 
+// margin repack gate (live_repack): repack when forced (new list / filter) or
+// when some atom moved more than margin/2 since the last repack; a repack
+// starts from a zeroed plan (what the ungated path's memset does)
+__global__ void k_repack_gate(const unsigned long long *__restrict__ drift_bits, double thr2,
+                              int force, int *__restrict__ go, DevPlan *__restrict__ plan) {
+  __shared__ int need;
+  if (threadIdx.x == 0) need = force || __longlong_as_double((long long)*drift_bits) > thr2;
+  __syncthreads();
+  if (threadIdx.x == 0) *go = need;
+  if (need) {
+    int *p = reinterpret_cast<int *>(plan);
+    for (int k = threadIdx.x; k < (int)(sizeof(DevPlan) / sizeof(int)); k += blockDim.x) p[k] = 0;
+  }
+}
+
 // histogram of row lengths into the device plan (block-private bins)
-__global__ void k_len_hist_plan(int n, const int *__restrict__ len, DevPlan *__restrict__ plan) {
+__global__ void k_len_hist_plan(int n, const int *__restrict__ len, DevPlan *__restrict__ plan,
+                                const int *__restrict__ go = nullptr) {
+  if (go && !*go) return;
   __shared__ int h[34];
   if (threadIdx.x < 34) h[threadIdx.x] = 0;
   __syncthreads();

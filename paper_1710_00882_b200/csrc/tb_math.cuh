@@ -48,6 +48,11 @@ struct Tables {
   // (gamma, c, d, h, lam3, m depend on i only, as in the Tersoff-1989 tables):
   // the (i,b,a) term then reuses the (i,a,b) angular values
   int gsym;
+  // 1 when g(cos) of entry (i,j,k) depends on i only (gamma, c, d, h equal
+  // for all j, k): the kernel keeps atom i's angular constants in registers
+  // instead of indexing the table per partner (the SiC fixture, Tersoff-1989
+  // tables)
+  int ang_i;
   // 1 when the pair cutoff (R, D of entry (i,j,j)) equals the k-role cutoff of
   // entry (i,j,j) -- one species: the pair term reuses the lane's f_C
   int fc_same;
@@ -97,9 +102,26 @@ __device__ __forceinline__ bool cutoff(T r, const P &p, T &fc, T &dfc) {
   return true;
 }
 
-// g(cos) and dg/dcos (potential.py:190-199), cancellation-free.
+// g(cos) constants of one entry, held in registers (Tables::ang_i)
 template <class T>
-__device__ __forceinline__ void angular(T cost, const TripP<T> &p, T &g, T &dg) {
+struct AngP {
+  T gamma, gc2d2, m2gc2, d2, h;
+};
+
+template <class T>
+__device__ __forceinline__ AngP<T> ang_of(const TripP<T> &p) {
+  AngP<T> a;
+  a.gamma = p.gamma;
+  a.gc2d2 = p.gc2d2;
+  a.m2gc2 = p.m2gc2;
+  a.d2 = p.d2;
+  a.h = p.h;
+  return a;
+}
+
+// g(cos) and dg/dcos (potential.py:190-199), cancellation-free.
+template <class T, class P>
+__device__ __forceinline__ void angular(T cost, const P &p, T &g, T &dg) {
   T x = p.h - cost;
   T x2 = x * x;
   T inv = t_rcp(p.d2 + x2);

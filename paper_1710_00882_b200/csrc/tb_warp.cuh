@@ -75,6 +75,9 @@ struct WarpCfg {
   static constexpr int minb = sizeof(T) == 8 ? TB_WARP_MINB64 : TB_WARP_MINB_F;
 };
 constexpr int QCAP = 4;   // k-iterations whose angular values are cached
+#ifndef TB_MIXED_LC8
+#define TB_MIXED_LC8 0  // measured: c4 mixed -2%, c3 mixed +19%, c5 mixed +14% (code size / registers)
+#endif
 
 template <class V>
 __device__ __forceinline__ V shfl(V v, int src) {
@@ -313,6 +316,9 @@ __device__ __forceinline__ void chunk_body(const KArgs &a, const WArgs &w, const
   constexpr bool RC2 = !RC && LC > 0 && S == 1 && TB_FP64_RC2;
   T rcos[RC ? QCAP : 1], rg[RC || RC2 ? QCAP : 1], rdg[RC || RC2 ? QCAP : 1];
   T zeta = T(0);
+  // two species with i-only angular constants: in registers for the row
+  const bool ang_i = S > 1 && tab.ang_i;
+  const AngP<T> ai = ang_of(tab.trip[si * S * S]);
   // only live partners of the row contribute (a dead b has f_C = dzeta = 0);
   // lanes iterate their own row's live mask (the table is in shared memory,
   // so no warp-uniform trip count is needed)
@@ -339,7 +345,10 @@ __device__ __forceinline__ void chunk_body(const KArgs &a, const WArgs &w, const
     T cost = ex * be.x + ey * be.y + ez * be.z;
     TB_CLAMP_COS(cost);
     T g, dg;
-    angular(cost, tp, g, dg);
+    if (S > 1 && ang_i)
+      angular(cost, ai, g, dg);
+    else
+      angular(cost, tp, g, dg);
     if (q < QCAP) {
       if (RC) {
         rcos[q] = cost;
@@ -443,7 +452,10 @@ __device__ __forceinline__ void chunk_body(const KArgs &a, const WArgs &w, const
     } else {
       cost = ex * be.x + ey * be.y + ez * be.z;
       TB_CLAMP_COS(cost);
-      angular(cost, tab.trip[(si * S + sj) * S + sb], g, dg);
+      if (S > 1 && ang_i)
+        angular(cost, ai, g, dg);
+      else
+        angular(cost, tab.trip[(si * S + sj) * S + sb], g, dg);
     }
     T alpha, beta;
     if (S == 1 && !LAM3) {
@@ -461,7 +473,7 @@ __device__ __forceinline__ void chunk_body(const KArgs &a, const WArgs &w, const
       if (t2) {  // (i,b,a): entry (si, sb, sa)
         const TripP<T> &tp = tab.trip[(si * S + sb) * S + sj];
         T g2 = g, dg2 = dg, exv = T(1), darg = T(0);
-        if (S > 1 && !tab.gsym) angular(cost, tp, g2, dg2);
+        if (S > 1 && !tab.gsym && !ang_i) angular(cost, tp, g2, dg2);
         if (LAM3) lam3_term(rb - ra, tp, exv, darg);
         alpha += dzb * (df_a * g2 * exv - f_a * g2 * exv * darg);
         beta += dzb * (f_a * dg2 * exv);
@@ -769,6 +781,14 @@ __global__ void __launch_bounds__(WarpCfg<T>::nt, WarpCfg<T>::minb)
     switch (Ldyn) {
       case 4: chunk_body<T, S, LAM3, MODE, ST, 4>(a, w, tab, s_cache[wid], s_tb[wid], lane, cur, stg, Ldyn, A); break;
       case 5: chunk_body<T, S, LAM3, MODE, ST, 5>(a, w, tab, s_cache[wid], s_tb[wid], lane, cur, stg, Ldyn, A); break;
+#if TB_MIXED_LC8
+      // mixed kernel: rows of 6-8 entries unrolled too (angular cache in
+      // registers; fp64 spills with them)
+      case 6: if (sizeof(T) == 4) { chunk_body<T, S, LAM3, MODE, ST, sizeof(T) == 4 ? 6 : 0>(a, w, tab, s_cache[wid], s_tb[wid], lane, cur, stg, Ldyn, A); break; }
+      case 7: if (sizeof(T) == 4) { chunk_body<T, S, LAM3, MODE, ST, sizeof(T) == 4 ? 7 : 0>(a, w, tab, s_cache[wid], s_tb[wid], lane, cur, stg, Ldyn, A); break; }
+      case 8: if (sizeof(T) == 4) { chunk_body<T, S, LAM3, MODE, ST, sizeof(T) == 4 ? 8 : 0>(a, w, tab, s_cache[wid], s_tb[wid], lane, cur, stg, Ldyn, A); break; }
+      // fall through (fp64)
+#endif
       default: chunk_body<T, S, LAM3, MODE, ST, 0>(a, w, tab, s_cache[wid], s_tb[wid], lane, cur, stg, Ldyn, A);
     }
     __syncwarp();  // the stage and the lane table are rewritten next iteration

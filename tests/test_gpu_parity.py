@@ -368,3 +368,44 @@ def _tiny_frame():
     fr = Frame([[0.0, 0, 0], [2.35, 0, 0]], [10.0, 10.0, 10.0], (False, False, False))
     nl = B.build_neighbor_list(fr, 3.0, 0.3)
     return fr, nl
+
+
+@pytest.mark.parametrize("margin", [1, 50])
+@pytest.mark.parametrize("precision", ["double", "single"])
+def test_margin_repack_tracks_moving_atoms(oracle_mod, precision, margin):
+    """TB_OPT_REPACK_MARGIN (rows cut at r_cut + delta, re-cut only after a
+    delta/2 drift, decided on the device): a sequence of evaluations at moving
+    positions -- small moves that keep the repack, larger ones that force it --
+    equals the oracle at every step, and equals the exact (margin 0) repack."""
+    from paper_1710_00882_b200 import _native
+    st, tname = structures.config(3, small=True)
+    t = builtin_params(tname)
+    ctx = _native.default_context(0)
+    rng = np.random.default_rng(5)
+    fr = Frame(st.positions.copy(), st.box.lengths, st.box.periodic, st.species)
+    nl = B.build_neighbor_list(fr, t.r_cut, 0.3)
+    nl0 = B.build_neighbor_list(fr, t.r_cut, 0.3)  # the exact-repack twin
+    var = B.make_variant("B200", precision=precision)
+    tol = FP64_TOL if precision == "double" else MIXED_TOL
+    ctx.set_option(_native.OPT_REPACK_MARGIN, margin)
+    moves = [0.0, 0.0, 0.0002, 0.004, 0.004, 0.03, 0.002, 0.05, 0.001]  # A per component (sigma)
+    base = st.positions.copy()
+    for k, s in enumerate(moves):
+        base = base + rng.normal(0.0, s, base.shape)
+        fr.positions = np.remainder(base, st.box.lengths)
+        res = B.compute(fr, nl, t, var)
+        ctx.set_option(_native.OPT_REPACK_MARGIN, 0)
+        try:
+            exact = B.compute(fr, nl0, t, var)
+        finally:
+            ctx.set_option(_native.OPT_REPACK_MARGIN, margin)
+        ref = oracle_mod.compute(fr.positions, fr.species, fr.box.lengths, fr.box.periodic,
+                                 nl.offsets, nl.neighbors, t)
+        assert abs(res.potential_energy - ref["energy"]) <= tol * abs(ref["energy"]), k
+        assert rel_f(res.forces, ref["forces"]) <= tol, k
+        # fp64: the same terms in the same order (dead lanes add exact zeros);
+        # mixed: the chunk shapes differ, so the fp32 partial sums round apart
+        same = 1e-12 if precision == "double" else MIXED_TOL
+        assert abs(res.potential_energy - exact.potential_energy) <= same * abs(ref["energy"])
+        assert res.stats["zeta_visits"] == exact.stats["zeta_visits"]
+    ctx.set_option(_native.OPT_REPACK_MARGIN, 1)
