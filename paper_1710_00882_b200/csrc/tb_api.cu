@@ -662,10 +662,22 @@ extern "C" int tb_build_neighbors(tb_context *ctx, tb_nlist *nl, int64_t n,
   return tb_build_neighbors_owned(ctx, nl, n, n, positions, box, periodic, r_cut, skin);
 }
 
+static int build_owned(tb_context *ctx, tb_nlist *nl, int64_t n, int64_t n_owned,
+                       const double *positions, const double *box, const int32_t *periodic,
+                       double r_cut, double skin, int cx_lo, int cx_hi);
+
 extern "C" int tb_build_neighbors_owned(tb_context *ctx, tb_nlist *nl, int64_t n,
                                         int64_t n_owned, const double *positions,
                                         const double *box, const int32_t *periodic,
                                         double r_cut, double skin) {
+  return build_owned(ctx, nl, n, n_owned, positions, box, periodic, r_cut, skin, 0, INT_MAX);
+}
+
+// cx_lo..cx_hi: x columns holding every owned atom (slab decomposition); the
+// cell scan skips the others
+static int build_owned(tb_context *ctx, tb_nlist *nl, int64_t n, int64_t n_owned,
+                       const double *positions, const double *box, const int32_t *periodic,
+                       double r_cut, double skin, int cx_lo, int cx_hi) {
   if (n_owned < 0 || n_owned > n) return fail(ctx, TB_ERR_ARG, "n_owned outside [0, n]");
   if (!ctx || !nl || !box || !periodic || (n && !positions))
     return fail(ctx, TB_ERR_ARG, "null argument");
@@ -758,6 +770,11 @@ extern "C" int tb_build_neighbors_owned(tb_context *ctx, tb_nlist *nl, int64_t n
     return fail(ctx, TB_ERR_CONFIG, "cell grid of %lld cells is too large", (long long)ncell);
 
   const int N = (int)n;
+  // cells [c0, c1) are scanned (the slab's own x columns, or all)
+  const int64_t nyz = ncell / g.nc[0];
+  const int64_t c0 = (int64_t)std::min(std::max(cx_lo, 0), g.nc[0]) * nyz;
+  const int64_t c1 = std::max<int64_t>(std::min<int64_t>((int64_t)std::min(cx_hi, g.nc[0] - 1) + 1,
+                                                         g.nc[0]) * nyz, c0);
   CK(nl->atom_cell.ensure(sizeof(int) * std::max(N, 1)));
   CK(nl->cell_count.ensure(sizeof(int) * (ncell + 1)));
   CK(nl->cell_start.ensure(sizeof(int) * (ncell + 1)));
@@ -795,10 +812,11 @@ extern "C" int tb_build_neighbors_owned(tb_context *ctx, tb_nlist *nl, int64_t n
     CK(cudaGetLastError());
     // single pass: rows of <= TMPW entries land in the scratch rows, counts,
     // max row and the row-length histogram (for the warp chunks) come along
-    k_nl_cells<<<nblk(ncell, 8), 256, 0, ctx->stream>>>(
-        (int)ncell, (int)n_owned, nl->cpos.as<double4>(), g, bc * bc, nl->cell_start.as<int>(),
-        nl->row_count.as<int>(), nl->scratch.as<int>(), nl->maxrow.as<int>(), nl->hist.as<int>(),
-        nl->maxrow.as<int>() + 1);
+    if (c1 > c0)
+      k_nl_cells<<<nblk(c1 - c0, 8), 256, 0, ctx->stream>>>(
+          (int)c1, (int)n_owned, nl->cpos.as<double4>(), g, bc * bc, nl->cell_start.as<int>(),
+          nl->row_count.as<int>(), nl->scratch.as<int>(), nl->maxrow.as<int>(),
+          nl->hist.as<int>(), nl->maxrow.as<int>() + 1, (int)c0);
     CK(cudaGetLastError());
   }
   rc = exclusive_scan(ctx, nl->row_count.as<int>(), nl->offsets.as<int>(), N + 1);
@@ -808,11 +826,19 @@ extern "C" int tb_build_neighbors_owned(tb_context *ctx, tb_nlist *nl, int64_t n
                      ctx->stream));
   CK(cudaMemcpyAsync(&hm[1], nl->maxrow.p, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
   CK(cudaMemcpyAsync(&hm[2], nl->hist.p, sizeof(int) * 34, cudaMemcpyDeviceToHost, ctx->stream));
+  const bool partial = c0 > 0 || c1 < ncell;
+  if (partial) {  // atoms of the unscanned cells (ghosts) have empty rows too
+    CK(cudaMemcpyAsync(&hm[36], nl->cell_start.as<int>() + c0, sizeof(int), cudaMemcpyDeviceToHost,
+                       ctx->stream));
+    CK(cudaMemcpyAsync(&hm[37], nl->cell_start.as<int>() + c1, sizeof(int), cudaMemcpyDeviceToHost,
+                       ctx->stream));
+  }
   CK(cudaStreamSynchronize(ctx->stream));
   nl->entries = hm[0];
   nl->max_row = hm[1];
   int hist[34];
   memcpy(hist, hm + 2, sizeof(hist));
+  if (partial) hist[0] += N - (hm[37] - hm[36]);
   // entry-sized buffers carry a margin so that the device-resident rebuild
   // (tb_md_run) can regrow the list in place
   if (nl->margin < 0) nl->margin = ctx->list_margin;

@@ -420,14 +420,17 @@ __global__ void __launch_bounds__(256) k_nl_cells(int ncell, int n_owned,
                                                   int *__restrict__ row_count,
                                                   int *__restrict__ tmp, int *__restrict__ max_row,
                                                   int *__restrict__ hist,
-                                                  const int *__restrict__ unwrapped) {
+                                                  const int *__restrict__ unwrapped,
+                                                  int cell0 = 0) {
   __shared__ int s_hist[34];
   if (threadIdx.x < 34) s_hist[threadIdx.x] = 0;
   __syncthreads();
   const bool stencil_image = g.stencil_image && !*unwrapped;
   const int lane = threadIdx.x & 31;
   const unsigned lt = (1u << lane) - 1u;
-  const int cell = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  // cells [cell0, ncell): a slab-decomposed rank scans only its own x columns
+  // (its owned atoms live there; the stencil reaches the ghost columns)
+  const int cell = cell0 + blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   int maxc = 0;
   if (cell < ncell) {
     const int c0 = cell_start[cell], nA = cell_start[cell + 1] - c0;
