@@ -103,7 +103,8 @@ int tb_synchronize(tb_context *ctx);
 /* Parameter table, flattened exactly like ParamTable.views()
  * (potential.py:127-155): pair_mat[S*S*8] = [R,D,A,lam1,B,lam2,beta,eta] of
  * entry (i,j,j); trip_mat[S^3*8] = [R,D,gamma,c,d,h,lam3,m] of entry (i,j,k).
- * Host pointers.  1 <= nspecies <= 4.  r_cut_out (may be NULL) receives
+ * Host pointers.  1 <= nspecies <= 64 (1-4: compile-time kernels; 5-64: the
+ * tile kernel with a runtime species count).  r_cut_out (may be NULL) receives
  * max(R+D) (potential.py:106). */
 int tb_set_params(tb_context *ctx, int nspecies, const double *pair_mat,
                   const double *trip_mat, double *r_cut_out);

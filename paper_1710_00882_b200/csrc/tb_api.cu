@@ -70,6 +70,7 @@ struct tb_context {
   // scratch
   DevBuf pos, species, forces, per_atom, result, stats, partials, errf, drift, bounds,
       scan_tmp, facc, stats_acc, ke_part, snap;
+  DevBuf dyn_pair64, dyn_trip64, dyn_pair32, dyn_trip32;  // S > SMAX: tables of the S = 0 kernel
   cudaStream_t cap[2] = {nullptr, nullptr};  // tb_md_run graph capture
   int64_t facc_n = -1;
   ErrFlags *h_err = nullptr;      // pinned
@@ -249,14 +250,14 @@ constexpr int SCAN_G = 8;  // lanes per atom in the CSR compaction
 // parameter tables (potential.py:127-155 column order)
 // ---------------------------------------------------------------------------
 
-template <class T, int S>
-static Tables<T, S> make_tables(const tb_context *ctx) {
-  Tables<T, S> tab;
-  memset(&tab, 0, sizeof(tab));
+// per-entry constants of the flattened tables (any species count)
+template <class T>
+static void fill_entries(const tb_context *ctx, int S, PairP<T> *pair, TripP<T> *trip) {
   const double kNegQuarterPi = -0.25 * 3.141592653589793;
   for (int q = 0; q < S * S * S; ++q) {
     const double *r = &ctx->trip_mat[8 * q];
-    TripP<T> &t = tab.trip[q];
+    TripP<T> &t = trip[q];
+    memset(&t, 0, sizeof(t));
     T R = (T)r[0], D = (T)r[1];
     t.Rm = R - D;
     t.Rp = R + D;
@@ -273,6 +274,33 @@ static Tables<T, S> make_tables(const tb_context *ctx) {
     t.lam3x3 = (T)(3.0 * r[6]);
     t.m = (int)r[7];
   }
+  for (int q = 0; q < S * S; ++q) {
+    const double *r = &ctx->pair_mat[8 * q];
+    PairP<T> &p = pair[q];
+    memset(&p, 0, sizeof(p));
+    T R = (T)r[0], D = (T)r[1];
+    p.Rm = R - D;
+    p.Rp = R + D;
+    p.R = R;
+    p.halfInvD = (T)(0.5 / r[1]);
+    p.nqpInvD = (T)kNegQuarterPi / D;
+    p.A = (T)r[2];
+    p.lam1 = (T)r[3];
+    p.B = (T)r[4];
+    p.lam2 = (T)r[5];
+    p.beta = (T)r[6];
+    p.eta = (T)r[7];
+    p.neg_half_inv_eta = (T)(-0.5 / r[7]);
+    p.neg_half_beta = (T)(-0.5 * r[6]);
+  }
+}
+
+template <class T, int S>
+static Tables<T, S> make_tables(const tb_context *ctx) {
+  Tables<T, S> tab;
+  memset(&tab, 0, sizeof(tab));
+  if (S == 0) return tab;  // runtime species count: tables in ctx->dyn (global memory)
+  fill_entries<T>(ctx, S, tab.pair, tab.trip);
   tab.gsym = 1;
   for (int i = 0; i < S; ++i)
     for (int j = 0; j < S; ++j)
@@ -291,24 +319,6 @@ static Tables<T, S> make_tables(const tb_context *ctx) {
         tab.ang_i = 0;
     }
   tab.fc_same = S == 1 && ctx->pair_mat[0] == ctx->trip_mat[0] && ctx->pair_mat[1] == ctx->trip_mat[1];
-  for (int q = 0; q < S * S; ++q) {
-    const double *r = &ctx->pair_mat[8 * q];
-    PairP<T> &p = tab.pair[q];
-    T R = (T)r[0], D = (T)r[1];
-    p.Rm = R - D;
-    p.Rp = R + D;
-    p.R = R;
-    p.halfInvD = (T)(0.5 / r[1]);
-    p.nqpInvD = (T)kNegQuarterPi / D;
-    p.A = (T)r[2];
-    p.lam1 = (T)r[3];
-    p.B = (T)r[4];
-    p.lam2 = (T)r[5];
-    p.beta = (T)r[6];
-    p.eta = (T)r[7];
-    p.neg_half_inv_eta = (T)(-0.5 / r[7]);
-    p.neg_half_beta = (T)(-0.5 * r[6]);
-  }
   return tab;
 }
 
@@ -343,7 +353,8 @@ extern "C" void tb_destroy(tb_context *ctx) {
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   DevBuf *bufs[] = {&ctx->pos, &ctx->species, &ctx->forces, &ctx->per_atom, &ctx->result,
                     &ctx->stats, &ctx->partials, &ctx->facc, &ctx->stats_acc, &ctx->ke_part, &ctx->errf,
-                    &ctx->drift, &ctx->bounds, &ctx->scan_tmp, &ctx->snap};
+                    &ctx->drift, &ctx->bounds, &ctx->scan_tmp, &ctx->snap,
+                    &ctx->dyn_pair64, &ctx->dyn_trip64, &ctx->dyn_pair32, &ctx->dyn_trip32};
   for (DevBuf *b : bufs) b->release();
   for (auto *v : {&ctx->ev_used, &ctx->ev_free})
     for (auto &ev : *v) {
@@ -409,8 +420,8 @@ extern "C" int tb_synchronize(tb_context *ctx) {
 extern "C" int tb_set_params(tb_context *ctx, int nspecies, const double *pair_mat,
                              const double *trip_mat, double *r_cut_out) {
   if (!ctx || !pair_mat || !trip_mat) return fail(ctx, TB_ERR_ARG, "null argument");
-  if (nspecies < 1 || nspecies > SMAX)
-    return fail(ctx, TB_ERR_CONFIG, "the B200 kernels support 1..%d species, got %d", SMAX,
+  if (nspecies < 1 || nspecies > SDYN_MAX)
+    return fail(ctx, TB_ERR_CONFIG, "the B200 kernels support 1..%d species, got %d", SDYN_MAX,
                 nspecies);
   const int S = nspecies;
   // validate everything before touching the context (a refused table leaves
@@ -443,6 +454,24 @@ extern "C" int tb_set_params(tb_context *ctx, int nspecies, const double *pair_m
   ctx->lam3 = lam3;
   ctx->r_cut = rc;
   ctx->param_version += 1;
+  if (S > SMAX) {
+    // runtime-S tile kernel: the derived tables in device memory, per precision
+    CK(cudaSetDevice(ctx->device));
+    std::vector<PairP<double>> p64(S * S);
+    std::vector<TripP<double>> t64((size_t)S * S * S);
+    std::vector<PairP<float>> p32(S * S);
+    std::vector<TripP<float>> t32((size_t)S * S * S);
+    fill_entries<double>(ctx, S, p64.data(), t64.data());
+    fill_entries<float>(ctx, S, p32.data(), t32.data());
+    CK(ctx->dyn_pair64.ensure(sizeof(PairP<double>) * p64.size()));
+    CK(ctx->dyn_trip64.ensure(sizeof(TripP<double>) * t64.size()));
+    CK(ctx->dyn_pair32.ensure(sizeof(PairP<float>) * p32.size()));
+    CK(ctx->dyn_trip32.ensure(sizeof(TripP<float>) * t32.size()));
+    CK(cudaMemcpy(ctx->dyn_pair64.p, p64.data(), sizeof(PairP<double>) * p64.size(), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(ctx->dyn_trip64.p, t64.data(), sizeof(TripP<double>) * t64.size(), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(ctx->dyn_pair32.p, p32.data(), sizeof(PairP<float>) * p32.size(), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(ctx->dyn_trip32.p, t32.data(), sizeof(TripP<float>) * t32.size(), cudaMemcpyHostToDevice));
+  }
   if (r_cut_out) *r_cut_out = rc;
   return TB_OK;
 }
@@ -1071,7 +1100,10 @@ extern "C" int tb_needs_rebuild(tb_context *ctx, const tb_nlist *nl, const doubl
 
 template <class T, int S, bool LAM3, int MODE>
 static int launch_tersoff_t(tb_context *ctx, const tb_nlist *nl, KArgs &a, int C) {
-  size_t smem = SmemLayout<T, S>::bytes(C);
+  size_t smem = SmemLayout<T, S>::bytes(C, S > 0 ? S : ctx->S);
+  a.nspecies = ctx->S;
+  a.dyn_pair = sizeof(T) == 8 ? ctx->dyn_pair64.p : ctx->dyn_pair32.p;
+  a.dyn_trip = sizeof(T) == 8 ? ctx->dyn_trip64.p : ctx->dyn_trip32.p;
   if (smem > 220 * 1024)
     return fail(ctx, TB_ERR_CONFIG, "neighbour rows of %lld entries exceed the kernel's staging",
                 (long long)nl->max_row);
@@ -1185,6 +1217,7 @@ static int launch_prec(tb_context *ctx, const tb_nlist *nl, KArgs &a, int C, int
     case 3: return launch_s<T, 3>(ctx, nl, a, C, mode);
     case 4: return launch_s<T, 4>(ctx, nl, a, C, mode);
   }
+  if (ctx->S <= SDYN_MAX) return launch_s<T, 0>(ctx, nl, a, C, mode);  // runtime species count
   return fail(ctx, TB_ERR_CONFIG, "unsupported species count %d", ctx->S);
 }
 

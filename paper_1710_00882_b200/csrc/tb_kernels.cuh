@@ -716,17 +716,20 @@ struct KArgs {
   double *__restrict__ partials;  // per block: [E, W xx yy zz xy xz yz, pad]
   unsigned long long *__restrict__ stats;  // TB_NSTATS counters
   ErrFlags *__restrict__ err;
+  int nspecies;                   // runtime species count (tile kernel S = 0)
+  const void *dyn_pair, *dyn_trip;  // S = 0: PairP<T>[S^2], TripP<T>[S^3] in global memory
 };
 
 template <class T, int S>
 struct SmemLayout {
   // byte offsets inside dynamic shared memory for a block with C slots
-  static __host__ __device__ size_t bytes(int C) {
+  // (Sr: the species count, = S unless S = 0)
+  static __host__ __device__ size_t bytes(int C, int Sr = S) {
     size_t b = 0;
     b += sizeof(Tables<T, S>);              // tables (S > 1 path reads them here)
     b = (b + 15) & ~size_t(15);
     b += sizeof(double) * 3 * C;            // s_f
-    b += sizeof(T) * (4 + 2 * S + 3) * C;   // ex ey ez r, fc[S], dfc[S], dz, v, dvdr
+    b += sizeof(T) * (4 + 2 * Sr + 3) * C;  // ex ey ez r, fc[S], dfc[S], dz, v, dvdr
     b += sizeof(int) * 2 * C;               // j, entry
     b += sizeof(short) * C;                 // local atom
     b += sizeof(unsigned char) * C;         // species of j
@@ -741,6 +744,10 @@ template <class T, int S, bool LAM3, int MODE>
 __global__ void __launch_bounds__(NT, 3)
     k_tersoff(const KArgs a, const __grid_constant__ Tables<T, S> gtab, int C) {
   extern __shared__ __align__(16) unsigned char smem[];
+  // S = 0: any species count, tables read from global memory (L1-cached)
+  const int SS = S > 0 ? S : a.nspecies;
+  const PairP<T> *__restrict__ dpair = static_cast<const PairP<T> *>(a.dyn_pair);
+  const TripP<T> *__restrict__ dtrip = static_cast<const TripP<T> *>(a.dyn_trip);
   // ---- carve shared memory (see SmemLayout) ----
   unsigned char *p = smem;
   Tables<T, S> *s_tab = reinterpret_cast<Tables<T, S> *>(p);
@@ -752,8 +759,8 @@ __global__ void __launch_bounds__(NT, 3)
   T *s_ey = reinterpret_cast<T *>(p); p += sizeof(T) * C;
   T *s_ez = reinterpret_cast<T *>(p); p += sizeof(T) * C;
   T *s_r = reinterpret_cast<T *>(p); p += sizeof(T) * C;
-  T *s_fc = reinterpret_cast<T *>(p); p += sizeof(T) * S * C;   // [S][C]
-  T *s_dfc = reinterpret_cast<T *>(p); p += sizeof(T) * S * C;  // [S][C]
+  T *s_fc = reinterpret_cast<T *>(p); p += sizeof(T) * SS * C;   // [S][C]
+  T *s_dfc = reinterpret_cast<T *>(p); p += sizeof(T) * SS * C;  // [S][C]
   T *s_dz = reinterpret_cast<T *>(p); p += sizeof(T) * C;
   T *s_v = reinterpret_cast<T *>(p); p += sizeof(T) * C;
   T *s_dvdr = reinterpret_cast<T *>(p); p += sizeof(T) * C;
@@ -775,6 +782,8 @@ __global__ void __launch_bounds__(NT, 3)
   const int na = min(a.atoms_per_block, a.n - atom0);
 
   const Tables<T, S> &tab = (S > 1) ? *s_tab : gtab;
+  auto PAIR = [&](int k) -> const PairP<T> & { return S > 0 ? tab.pair[k] : dpair[k]; };
+  auto TRIP = [&](int k) -> const TripP<T> & { return S > 0 ? tab.trip[k] : dtrip[k]; };
   if (S > 1) {
     // species-indexed tables are read with divergent indices: stage in smem
     const int *src = reinterpret_cast<const int *>(&gtab);
@@ -793,7 +802,7 @@ __global__ void __launch_bounds__(NT, 3)
     s_xi[3 * tid + 2] = x[2];
     if (!(isfinite(x[0]) && isfinite(x[1]) && isfinite(x[2]))) atomicMin(&a.err->nonfinite_atom, i);
     int si = a.species[i];
-    if (si < 0 || si >= S) {
+    if (si < 0 || si >= SS) {
       atomicMin(&a.err->bad_species_atom, i);
       si = 0;
     }
@@ -858,13 +867,13 @@ __global__ void __launch_bounds__(NT, 3)
       s_ent[slot] = e0 + e;
       s_atom[slot] = (short)la;
       int sj = a.species[j];
-      sj = (sj < 0 || sj >= S) ? 0 : sj;
+      sj = (sj < 0 || sj >= SS) ? 0 : sj;
       s_sp[slot] = (unsigned char)sj;
       const int si = s_si[la];
 #pragma unroll
-      for (int q = 0; q < S; ++q) {  // f_C(r) of this slot acting as k in (i, q, slot)
+      for (int q = 0; q < SS; ++q) {  // f_C(r) of this slot acting as k in (i, q, slot)
         T fc, dfc;
-        cutoff((T)r, tab.trip[(si * S + q) * S + sj], fc, dfc);
+        cutoff((T)r, TRIP((si * SS + q) * SS + sj), fc, dfc);
         s_fc[q * C + slot] = fc;
         s_dfc[q * C + slot] = dfc;
       }
@@ -902,7 +911,7 @@ __global__ void __launch_bounds__(NT, 3)
     const int sa = s_sp[s];
     const int b0 = s_soff[la], b1 = s_soff[la + 1];
     const T ra = s_r[s];
-    const PairP<T> &pp = tab.pair[si * S + sa];
+    const PairP<T> &pp = PAIR(si * SS + sa);
     T v = T(0), dvdr = T(0), dz = T(0);
     if (ra < pp.Rp) {
       live_pairs++;
@@ -916,7 +925,7 @@ __global__ void __launch_bounds__(NT, 3)
         live_trips++;
         taper_trips += fcb != T(1);
         const int sb = s_sp[b];
-        const TripP<T> &tp = tab.trip[(si * S + sa) * S + sb];
+        const TripP<T> &tp = TRIP((si * SS + sa) * SS + sb);
         T cost = eax * s_ex[b] + eay * s_ey[b] + eaz * s_ez[b];
         cost = fmin(T(1), fmax(T(-1), cost));
         T g, dg;
@@ -980,7 +989,7 @@ __global__ void __launch_bounds__(NT, 3)
       cost = fmin(T(1), fmax(T(-1), cost));
       T alpha, beta;
       if (S == 1 && !LAM3) {
-        const TripP<T> &tp = tab.trip[0];
+        const TripP<T> &tp = TRIP(0);
         T g, dg;
         angular(cost, tp, g, dg);
         const T dfca = s_dfc[s];
@@ -990,7 +999,7 @@ __global__ void __launch_bounds__(NT, 3)
         alpha = T(0);
         beta = T(0);
         if (t1) {
-          const TripP<T> &tp = tab.trip[(si * S + sa) * S + sb];
+          const TripP<T> &tp = TRIP((si * SS + sa) * SS + sb);
           T g, dg, ex = T(1), darg = T(0);
           angular(cost, tp, g, dg);
           if (LAM3) lam3_term(ra - s_r[b], tp, ex, darg);
@@ -999,7 +1008,7 @@ __global__ void __launch_bounds__(NT, 3)
           beta += dza * (fcb * dg * ex);
         }
         if (t2) {
-          const TripP<T> &tp = tab.trip[(si * S + sb) * S + sa];
+          const TripP<T> &tp = TRIP((si * SS + sb) * SS + sa);
           T g, dg, ex = T(1), darg = T(0);
           angular(cost, tp, g, dg);
           if (LAM3) lam3_term(s_r[b] - ra, tp, ex, darg);

@@ -19,7 +19,8 @@
 
 namespace tb {
 
-constexpr int SMAX = 4;
+constexpr int SMAX = 4;       // compile-time species counts (1..4)
+constexpr int SDYN_MAX = 64;  // any table up to this many species: the S = 0 tile kernel
 constexpr double ZETA_TINY = 1e-30;
 
 // Per-entry constants derived on the host from the flattened tables (see
@@ -42,8 +43,10 @@ struct PairP {
 
 template <class T, int S>
 struct Tables {
-  PairP<T> pair[S * S];
-  TripP<T> trip[S * S * S];
+  // S = 0 (runtime species count): one dummy entry, the tables are in global
+  // memory (KArgs::dyn_pair / dyn_trip)
+  PairP<T> pair[S > 0 ? S * S : 1];
+  TripP<T> trip[S > 0 ? S * S * S : 1];
   // 1 when g(cos) of entry (i,j,k) equals that of (i,k,j) for every triple
   // (gamma, c, d, h, lam3, m depend on i only, as in the Tersoff-1989 tables):
   // the (i,b,a) term then reuses the (i,a,b) angular values

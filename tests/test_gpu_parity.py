@@ -409,3 +409,57 @@ def test_margin_repack_tracks_moving_atoms(oracle_mod, precision, margin):
         assert abs(res.potential_energy - exact.potential_energy) <= same * abs(ref["energy"])
         assert res.stats["zeta_visits"] == exact.stats["zeta_visits"]
     ctx.set_option(_native.OPT_REPACK_MARGIN, 1)
+
+
+def _many_species_table(S):
+    """A synthetic S-species table (not a published set): carbon-like values
+    varied by the species of each slot, m = 1 with lam3 != 0 on some triples."""
+    from paper_1710_00882_b200.potential import ParamTable, TersoffParams
+    ent = {}
+    for i in range(S):
+        for j in range(S):
+            for k in range(S):
+                m = 1 if (i + k) % 3 == 0 else 3
+                ent[(i, j, k)] = TersoffParams(
+                    m=m, gamma=1.0 + 0.05 * k, lam3=0.6 if m == 1 else 0.0,
+                    c=38049.0 * (1.0 - 0.08 * i), d=4.3484 + 0.3 * j, h=-0.57058 + 0.04 * k,
+                    eta=0.72751 + 0.05 * i, beta=1.5724e-7 * (1.0 + 0.5 * (i + j)),
+                    lam2=2.2119 - 0.05 * j, B=346.74 * (1.0 + 0.05 * i),
+                    R=1.95 + 0.06 * (i + k), D=0.15 + 0.01 * j,
+                    lam1=3.4879 - 0.05 * i, A=1393.6 * (1.0 + 0.03 * j))
+    return ParamTable(tuple(f"X{q}" for q in range(S)), ent)
+
+
+@pytest.mark.parametrize("S", [5, 7])
+@pytest.mark.parametrize("precision", ["double", "single"])
+def test_more_than_four_species(oracle_mod, S, precision):
+    # the reference's ParamTable takes any species count (potential.py:94-110):
+    # S > 4 runs the tile kernel with a runtime species count (tables in HBM)
+    table = _many_species_table(S)
+    rng = np.random.default_rng(40 + S)
+    # periodic random packing (min separation 1.3 A) with all species present
+    n, L = 300, 14.0
+    pos = rng.uniform(0, L, (1, 3))
+    while len(pos) < n:
+        c = rng.uniform(0, L, 3)
+        d = pos - c
+        d -= L * np.round(d / L)
+        if (d * d).sum(1).min() > 1.3 ** 2:
+            pos = np.vstack([pos, c])
+    species = rng.integers(0, S, n)
+    fr = Frame(pos, [L, L, L], (True, True, True), species)
+    nl, res = gpu_eval(fr, table, precision=precision)
+    off, nb = oracle_mod.build_neighbor_list(fr.positions, fr.box.lengths, fr.box.periodic,
+                                             table.r_cut, 0.3)
+    assert np.array_equal(nl.offsets, off) and np.array_equal(nl.neighbors, nb)
+    ref = oracle_mod.compute(fr.positions, fr.species, fr.box.lengths, fr.box.periodic, off, nb,
+                             table)
+    tol = FP64_TOL if precision == "double" else MIXED_TOL
+    assert abs(res.potential_energy - ref["energy"]) <= tol * abs(ref["energy"])
+    assert rel_f(res.forces, ref["forces"]) <= tol
+    assert np.abs(res.virial - ref["virial"]).max() <= 1e3 * tol * np.abs(ref["virial"]).max()
+    assert res.stats["zeta_visits"] == int(ref["zeta_visits"])
+    with pytest.raises(B.ConfigurationError, match="species"):
+        bad = fr.species.copy()
+        bad[0] = S
+        B.compute(Frame(pos, [L, L, L], (True, True, True), bad), nl, table)
