@@ -1101,9 +1101,10 @@ extern "C" int tb_needs_rebuild(tb_context *ctx, const tb_nlist *nl, const doubl
 template <class T, int S, bool LAM3, int MODE>
 static int launch_tersoff_t(tb_context *ctx, const tb_nlist *nl, KArgs &a, int C) {
   size_t smem = SmemLayout<T, S>::bytes(C, S > 0 ? S : ctx->S);
-  a.nspecies = ctx->S;
-  a.dyn_pair = sizeof(T) == 8 ? ctx->dyn_pair64.p : ctx->dyn_pair32.p;
-  a.dyn_trip = sizeof(T) == 8 ? ctx->dyn_trip64.p : ctx->dyn_trip32.p;
+  DynTab dyn;
+  dyn.nspecies = ctx->S;
+  dyn.pair = sizeof(T) == 8 ? ctx->dyn_pair64.p : ctx->dyn_pair32.p;
+  dyn.trip = sizeof(T) == 8 ? ctx->dyn_trip64.p : ctx->dyn_trip32.p;
   if (smem > 220 * 1024)
     return fail(ctx, TB_ERR_CONFIG, "neighbour rows of %lld entries exceed the kernel's staging",
                 (long long)nl->max_row);
@@ -1127,7 +1128,7 @@ static int launch_tersoff_t(tb_context *ctx, const tb_nlist *nl, KArgs &a, int C
     }
     CK(cudaEventRecord(ev.first, ctx->stream));
   }
-  kern<<<nb, NT, smem, ctx->stream>>>(a, tab, C);
+  kern<<<nb, NT, smem, ctx->stream>>>(a, tab, C, dyn);
   CK(cudaGetLastError());
   if (ctx->profile) {
     CK(cudaEventRecord(ev.second, ctx->stream));

@@ -716,8 +716,12 @@ struct KArgs {
   double *__restrict__ partials;  // per block: [E, W xx yy zz xy xz yz, pad]
   unsigned long long *__restrict__ stats;  // TB_NSTATS counters
   ErrFlags *__restrict__ err;
-  int nspecies;                   // runtime species count (tile kernel S = 0)
-  const void *dyn_pair, *dyn_trip;  // S = 0: PairP<T>[S^2], TripP<T>[S^3] in global memory
+};
+
+// tile kernel with a runtime species count (S = 0): tables in global memory
+struct DynTab {
+  int nspecies;
+  const void *pair, *trip;  // PairP<T>[S^2], TripP<T>[S^3]
 };
 
 template <class T, int S>
@@ -742,12 +746,12 @@ struct SmemLayout {
 
 template <class T, int S, bool LAM3, int MODE>
 __global__ void __launch_bounds__(NT, 3)
-    k_tersoff(const KArgs a, const __grid_constant__ Tables<T, S> gtab, int C) {
+    k_tersoff(const KArgs a, const __grid_constant__ Tables<T, S> gtab, int C, const DynTab dyn) {
   extern __shared__ __align__(16) unsigned char smem[];
   // S = 0: any species count, tables read from global memory (L1-cached)
-  const int SS = S > 0 ? S : a.nspecies;
-  const PairP<T> *__restrict__ dpair = static_cast<const PairP<T> *>(a.dyn_pair);
-  const TripP<T> *__restrict__ dtrip = static_cast<const TripP<T> *>(a.dyn_trip);
+  const int SS = S > 0 ? S : dyn.nspecies;
+  const PairP<T> *__restrict__ dpair = static_cast<const PairP<T> *>(dyn.pair);
+  const TripP<T> *__restrict__ dtrip = static_cast<const TripP<T> *>(dyn.trip);
   // ---- carve shared memory (see SmemLayout) ----
   unsigned char *p = smem;
   Tables<T, S> *s_tab = reinterpret_cast<Tables<T, S> *>(p);

@@ -165,22 +165,23 @@ __device__ __forceinline__ void pair_part_fc(T r, T zeta, const PairP<T> &p, T f
     // u = t^eta, b = (1+u)^(-1/2eta), and with t^(eta-1) = u/t, t = beta zeta:
     //   db/dzeta = -beta/2 t^(eta-1) (1+u)^(-1/2eta-1) = -(1/2) u b / (zeta (1+u))
     // one reciprocal serves db and the log1p correction (1/w = zeta / (zeta w)).
-    // Range (any table, branch-free): x = eta log t above XBIG makes 1/u
-    // smaller than the rounding unit, so log1p(u) = x and u/(1+u) = 1 exactly
-    // in T -- no u, no overflow however large eta; below -708 u is a
-    // subnormal at most (clamped: b = 1, db ~ 1e-308/zeta).  Every exp / log
-    // argument then stays on the fast domain: -l1p/2eta >= -log(t)/2 >= -355.
+    // Range (any table, branch-free): beyond x = eta log t = XBIG, 1/u is below
+    // the rounding unit, so log1p(u) = XBIG + (x - XBIG) to rounding and
+    // u/(1+u) = 1: u is formed from x clamped to XBIG (no overflow however
+    // large eta) and the excess added to log1p; below -708 u is at most a
+    // subnormal (clamped: b = 1, db ~ 1e-308/zeta).  Every exp / log argument
+    // stays on the fast domain: -l1p/2eta >= -log(t)/2 >= -355.
     constexpr T XBIG = sizeof(T) == 8 ? T(36) : T(17);
     const T lt = t_log(t);
     const T x = p.eta * lt;
-    const bool big = x > XBIG;
-    const T u = t_exp(fmax(big ? T(0) : x, T(-708)));
+    const T xc = fmin(x, XBIG);
+    const T u = t_exp(fmax(xc, T(-708)));
     const T w = T(1) + u;
-    const T rzw = t_rcp(big ? zeta : zeta * w);
+    const T rzw = t_rcp(zeta * w);
     // log1p(u) = log(w) + (u - (w - 1)) / w, w = fl(1 + u)
-    const T l1p = big ? x : t_log(w) + (u - (w - T(1))) * (zeta * rzw);
+    const T l1p = t_log(w) + (u - (w - T(1))) * (zeta * rzw) + (x - xc);
     b = t_exp(p.neg_half_inv_eta * l1p);
-    db = T(-0.5) * (big ? b : u * b) * rzw;
+    db = T(-0.5) * (u * b) * rzw;
   }
   T inner = fr + b * fa;
   v = fc * inner;

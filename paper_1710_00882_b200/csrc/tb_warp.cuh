@@ -318,7 +318,8 @@ __device__ __forceinline__ void chunk_body(const KArgs &a, const WArgs &w, const
   T zeta = T(0);
   // two species with i-only angular constants: in registers for the row
   const bool ang_i = S > 1 && tab.ang_i;
-  const AngP<T> ai = ang_of(tab.trip[si * S * S]);
+  AngP<T> ai;
+  if (S > 1) ai = ang_of(tab.trip[si * S * S]);
   // only live partners of the row contribute (a dead b has f_C = dzeta = 0);
   // lanes iterate their own row's live mask (the table is in shared memory,
   // so no warp-uniform trip count is needed)
