@@ -1328,7 +1328,7 @@ static int live_repack(tb_context *ctx, tb_nlist *nl, const double *d_pos, doubl
 static int enqueue_compute(tb_context *ctx, const tb_nlist *nl, const double *d_pos,
                            const int *d_species, double r_cut, int precision, int scatter,
                            double *d_forces, double *d_per_atom, double *d_result,
-                           unsigned long long *d_stats) {
+                           unsigned long long *d_stats, bool direct_ok = true) {
   if (ctx->S == 0) return fail(ctx, TB_ERR_CONFIG, "parameters not set");
   if (!nl->built) return fail(ctx, TB_ERR_ARG, "neighbour list not built");
   if (r_cut > nl->r_cut)
@@ -1406,7 +1406,18 @@ static int enqueue_compute(tb_context *ctx, const tb_nlist *nl, const double *d_
   a.species = d_species;
   a.off = nl->offsets.as<int>();
   a.nbr = nl->nbr.as<int>();
-  a.forces = ctx->facc.as<double>();
+  // Atomic scatter into a device force array: the kernels accumulate straight
+  // into the caller's array after one memset (24 B/atom written), instead of
+  // into the context accumulator that the finalize copies out and re-zeroes
+  // (24 B read + 48 B written per atom; config 5: ~200 -> ~60 us).  Starting
+  // from +0.0, a sum of forces cannot come out as -0.0, so the reference's
+  // +0.0 flush holds without the copy.  Host-mapped outputs (tb_compute with
+  // pinned buffers) and the fused MD graph keep the accumulator.
+  // (below ~256k atoms the extra memset node costs more than the copy it
+  // saves: config 2 step 24.9 -> 26.7 us; config 5 2.86 -> 2.60 ms)
+  const bool direct = direct_ok && scatter == TB_SCATTER_ATOMIC && !ctx->md_fuse && n >= (1 << 18);
+  if (direct) CK(cudaMemsetAsync(d_forces, 0, sizeof(double) * 3 * (size_t)n, ctx->stream));
+  a.forces = direct ? d_forces : ctx->facc.as<double>();
   a.fbuf = nl->fbuf.as<double>();
   a.per_atom = d_per_atom;
   a.partials = ctx->partials.as<double>();
@@ -1444,7 +1455,7 @@ static int enqueue_compute(tb_context *ctx, const tb_nlist *nl, const double *d_
       // counts, so k_pack_stats still counts over the full rows
       w.count_packed = filtered ? 0 : 1;
     }
-    w.facc = ctx->facc.as<double>();
+    w.facc = a.forces;
     const bool want_stats = d_stats != nullptr;
     rc = precision == TB_PREC_DOUBLE ? launch_warp_prec<double>(ctx, nl, a, w, scatter, want_stats)
                                      : launch_warp_prec<float>(ctx, nl, a, w, scatter, want_stats);
@@ -1465,8 +1476,10 @@ static int enqueue_compute(tb_context *ctx, const tb_nlist *nl, const double *d_
   }
   // finalize grid: block 0 reduces E/W; the rest move the forces (atomic: 16-byte
   // vectors, ~4 per thread; gather: one atom row per thread)
-  int fb = 1 + std::min(scatter == TB_SCATTER_GATHER ? nblk(n, 256) : nblk(3 * (int64_t)n, 256 * 2 * 4),
-                        4 * 148);
+  int fb = direct ? 1
+                  : 1 + std::min(scatter == TB_SCATTER_GATHER ? nblk(n, 256)
+                                                              : nblk(3 * (int64_t)n, 256 * 2 * 4),
+                                 4 * 148);
   // (a programmatic-dependent finalize launch, a cooperative grid-barrier
   //  finalize and a last-block reduction were all measured slower)
 #ifdef TB_DBG_NO_FINALIZE
@@ -1479,9 +1492,9 @@ static int enqueue_compute(tb_context *ctx, const tb_nlist *nl, const double *d_
                                                 d_forces, nparts, a.partials, d_result, a.stats,
                                                 d_stats, err_src, ctx->fin_err_dst);
   else
-    k_finalize<0><<<fb, 256, 0, ctx->stream>>>(n, a.forces, nullptr, nullptr, nullptr, d_forces,
-                                                nparts, a.partials, d_result, a.stats, d_stats,
-                                                err_src, ctx->fin_err_dst);
+    k_finalize<0><<<fb, 256, 0, ctx->stream>>>(n, direct ? nullptr : a.forces, nullptr, nullptr,
+                                                nullptr, d_forces, nparts, a.partials, d_result,
+                                                a.stats, d_stats, err_src, ctx->fin_err_dst);
   CK(cudaGetLastError());
   return TB_OK;
 }
@@ -1608,7 +1621,7 @@ evaluate:
   if (!pa_async) ctx->ev_kernel_done = nullptr;
   rc = enqueue_compute(ctx, nl, d_pos, d_sp, r_cut, precision, scatter, d_f, d_e,
                        reinterpret_cast<double *>(hd + 64),
-                       reinterpret_cast<unsigned long long *>(hd + 128));
+                       reinterpret_cast<unsigned long long *>(hd + 128), f_dev);
   ctx->fin_err_dst = nullptr;
   ctx->ev_kernel_done = keep_ev;
   if (rc) return rc;

@@ -640,6 +640,7 @@ __device__ __forceinline__ void finalize_body(int n, double *__restrict__ facc,
   }
   const int nb = gridDim.x > 1 ? gridDim.x - 1 : 1;
   const int b0 = gridDim.x > 1 ? blockIdx.x - 1 : 0;
+  if (MODE == 0 && !facc) return;  // forces accumulated in place (enqueue_compute)
   if (MODE == 0) {
     const int64_t m3 = 3 * (int64_t)n;
     if ((reinterpret_cast<uintptr_t>(forces) & 15) == 0) {
