@@ -1438,8 +1438,14 @@ static int enqueue_compute(tb_context *ctx, const tb_nlist *nl, const double *d_
     // filtered rows (SiC: 12 mostly dead Si-Si entries per Si row; c3 step
     // 501 -> 395 us).  Long single-species rows (disordered Si, c4) gain
     // 575 -> 371 us in the kernel but pay it back in the repack pass.
+    // Auto also takes long single-species rows (skin rows of >= 6 entries on
+    // average, e.g. disordered Si at 6.9): with the margin gate (§3.5) the
+    // repack pass runs only after atoms moved, so repeated evaluations keep
+    // the short rows for free.
+    const bool long_rows = nl->n > 0 && nl->entries >= 6 * nl->n;
     const bool live = !ctx->dplan && scatter == TB_SCATTER_ATOMIC && (!filtered || nl->fnbr_ok) &&
-                      (ctx->live_pack == 1 || (ctx->live_pack == 2 && filtered));
+                      (ctx->live_pack == 1 ||
+                       (ctx->live_pack == 2 && (filtered || (long_rows && ctx->repack_margin > 0))));
     if (ctx->dplan) {  // tb_md_run capture: chunk counts live in the device plan
       w.dinfo = ctx->dplan;
       w.nchunks = (int)nl->ccap;  // grid sizing only
