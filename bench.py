@@ -592,6 +592,14 @@ def gpu_arm(args):
                                                  0, 1000)
         extra["md"]["config2_mixed"] = md_measure(B, _native, ctx, st2, builtin_params(tn2), dev,
                                                   1, 1000)
+        if args.md3_steps > 0:
+            # BASELINE config 3 protocol: 512,000-atom SiC, 1500 K, dt 1 fs, 500 steps
+            st3, tn3 = structures.config(3)
+            for pname, pcode in (("fp64", 0), ("mixed", 1)):
+                extra["md"][f"config3_{pname}"] = md_measure(B, _native, ctx, st3,
+                                                             builtin_params(tn3), dev, pcode,
+                                                             args.md3_steps, warm=10)
+            del st3
         if cfg["config"] == 5 and args.md5_steps > 0:
             extra["md"]["config5_fp64"] = md_measure(B, _native, ctx, state, table, dev, 0,
                                                      args.md5_steps, warm=10)
@@ -813,6 +821,7 @@ def main():
     ap.add_argument("--cpu-budget", type=float, default=12.0)
     ap.add_argument("--ref-budget", type=float, default=60.0)
     ap.add_argument("--md5-steps", type=int, default=200)
+    ap.add_argument("--md3-steps", type=int, default=500)
     ap.add_argument("--dd-md-steps", type=int, default=50)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-extras", dest="extras", action="store_false")

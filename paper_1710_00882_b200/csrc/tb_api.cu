@@ -88,6 +88,7 @@ struct tb_context {
 #define TB_REPACK_MARGIN_DEFAULT 0.001  // c3 step (A): 0 -> 333 us, 1e-3 -> 261, 5e-3 -> 268, 0.01 -> 276, 0.05 -> 331
 #endif
   double repack_margin = TB_REPACK_MARGIN_DEFAULT;  // TB_OPT_REPACK_MARGIN (A)
+  bool md_live = getenv("TB_NO_MD_REPACK") == nullptr;  // live repack inside tb_md_run (S > 1)
   bool warp_per_chunk = getenv("TB_WARP_PER_CHUNK") != nullptr;
   bool no_filter = getenv("TB_NO_FILTER") != nullptr;  // disable the species-pair compute filter
   bool err_unchecked = false;     // kernels may have raised error flags nobody read yet
@@ -139,7 +140,7 @@ struct tb_nlist {
   DevBuf ref_log;  // tb_md_run loose list: positions of the reference's last rebuild
   // margin repack (TB_OPT_REPACK_MARGIN): positions of the last repack, the
   // gate's drift word and flag; valid until the list or its filter changes
-  DevBuf lref, lgate;
+  DevBuf lref, lgate, lforce;  // lforce: device flag, set by the in-graph rebuild
   bool lvalid = false, lfilt = false;
   double lmargin = -1.0;
   bool fnbr_ok = false;  // fnbr matches centry (written by every filter pass since)
@@ -150,13 +151,14 @@ struct tb_nlist {
 
 // captured device-resident NVE loop (tb_md_run), reused while its key holds
 struct MdKey {
-  const void *ptr[40];
+  const void *ptr[48];
   int64_t n, ecap, ccap, ncell;
   double dt, accel, skin, r_cut;
   double L[3], width[3], origin[3];  // the graph bakes the box and cell grid in by value
   int per[3], nc[3], stencil_image;
   int rebuild_every, precision, scatter, record_every, param_version, filtered, S, tile;
-  double loose;
+  double loose, margin;
+  int64_t lcap;
 };
 
 struct MdGraph {
@@ -552,7 +554,7 @@ extern "C" void tb_nlist_destroy(tb_nlist *nl) {
                     &nl->iota, &nl->lanes, &nl->hist, &nl->cpos, &nl->crow, &nl->coff,
                     &nl->centry, &nl->fnbr, &nl->fbuf, &nl->plan, &nl->scratch, &nl->lplan,
                     &nl->llen, &nl->lrow, &nl->lrowj, &nl->lsorted, &nl->llanes, &nl->ref_log,
-                    &nl->fspecies, &nl->lref, &nl->lgate};
+                    &nl->fspecies, &nl->lref, &nl->lgate, &nl->lforce};
   for (DevBuf *b : bufs) b->release();
   md_graph_release(nl);
   delete nl;
@@ -1249,8 +1251,8 @@ static int reset_errors(tb_context *ctx) {
 // (k_live_rows, then the tb_md_run plan kernels).  Rows of the skin list that
 // are mostly dead (SiC: 12 Si-Si second neighbours at 3.08 A just outside the
 // 3.0 A cutoff) then no longer occupy idle lanes.
-static int live_repack(tb_context *ctx, tb_nlist *nl, const double *d_pos, double r_cut,
-                       bool filtered, const Box &box, ErrFlags *err) {
+// buffers of the live repack (sized before a graph capture by md_prepare)
+static int live_reserve(tb_context *ctx, tb_nlist *nl, bool filtered) {
   const int N = (int)nl->n;
   const int64_t ent = filtered ? nl->ecap : std::max<int64_t>(nl->ecap, nl->entries);
   // chunk bound: a bucket of length L holds floor(32/L) rows of L lanes, and
@@ -1266,6 +1268,18 @@ static int live_repack(tb_context *ctx, tb_nlist *nl, const double *d_pos, doubl
     nl->lcap = cap;
     nl->lvalid = false;
   }
+  if (ctx->repack_margin > 0) {
+    CK(nl->lref.ensure(sizeof(double) * 3 * std::max(N, 1)));
+    CK(nl->lgate.ensure(16));
+  }
+  return TB_OK;
+}
+
+static int live_repack(tb_context *ctx, tb_nlist *nl, const double *d_pos, double r_cut,
+                       bool filtered, const Box &box, ErrFlags *err) {
+  const int N = (int)nl->n;
+  int rr = live_reserve(ctx, nl, filtered);
+  if (rr) return rr;
   DevPlan *plan = nl->lplan.as<DevPlan>();
   const int *start = filtered ? nl->coff.as<int>() : nl->offsets.as<int>();
 #ifndef TB_LIVE_G
@@ -1282,16 +1296,18 @@ static int live_repack(tb_context *ctx, tb_nlist *nl, const double *d_pos, doubl
   const int *go = nullptr;
   double *lref = nullptr;
   if (margin > 0) {
-    CK(nl->lref.ensure(sizeof(double) * 3 * std::max(N, 1)));
-    CK(nl->lgate.ensure(16));
     unsigned long long *dbits = nl->lgate.as<unsigned long long>();
     int *gop = reinterpret_cast<int *>(dbits + 1);
-    const bool force = !nl->lvalid || nl->lmargin != margin || nl->lfilt != filtered;
+    // inside tb_md_run's graph the list may be rebuilt on the device: the
+    // rebuild raises lforce and the gate repacks unconditionally then
+    const bool in_graph = ctx->dplan != nullptr;
+    const bool force = !in_graph && (!nl->lvalid || nl->lmargin != margin || nl->lfilt != filtered);
     CK(cudaMemsetAsync(dbits, 0, sizeof(unsigned long long), ctx->stream));
     if (!force && N)
       k_max_drift<<<std::min(nblk(N, 256), 4 * 148), 256, 0, ctx->stream>>>(
           N, d_pos, nl->lref.as<double>(), box, dbits);
-    k_repack_gate<<<1, 128, 0, ctx->stream>>>(dbits, 0.25 * margin * margin, force ? 1 : 0, gop,
+    k_repack_gate<<<1, 128, 0, ctx->stream>>>(dbits, 0.25 * margin * margin, force ? 1 : 0,
+                                               in_graph ? nl->lforce.as<int>() : nullptr, gop,
                                                plan);
     CK(cudaGetLastError());
     go = gop;
@@ -1443,10 +1459,16 @@ static int enqueue_compute(tb_context *ctx, const tb_nlist *nl, const double *d_
     // repack pass runs only after atoms moved, so repeated evaluations keep
     // the short rows for free.
     const bool long_rows = nl->n > 0 && nl->entries >= 6 * nl->n;
-    const bool live = !ctx->dplan && scatter == TB_SCATTER_ATOMIC && (!filtered || nl->fnbr_ok) &&
+    // Inside tb_md_run's graph (dplan set): species-filtered rows only, with
+    // the margin gate and its device-side force flag (md_prepare sized the
+    // buffers; the in-graph rebuild raises lforce).
+    const bool live_ok = ctx->dplan ? (filtered && ctx->md_live && ctx->repack_margin > 0 &&
+                                       nl->lforce.p != nullptr)
+                                    : true;
+    const bool live = live_ok && scatter == TB_SCATTER_ATOMIC && (!filtered || nl->fnbr_ok) &&
                       (ctx->live_pack == 1 ||
                        (ctx->live_pack == 2 && (filtered || (long_rows && ctx->repack_margin > 0))));
-    if (ctx->dplan) {  // tb_md_run capture: chunk counts live in the device plan
+    if (ctx->dplan && !live) {  // tb_md_run capture: chunk counts live in the device plan
       w.dinfo = ctx->dplan;
       w.nchunks = (int)nl->ccap;  // grid sizing only
     } else if (live) {
@@ -1861,6 +1883,7 @@ static int enqueue_rebuild_device(tb_context *ctx, tb_nlist *nl, const double *d
   if (scatter == TB_SCATTER_GATHER)
     k_nl_reverse<<<nblk(N, 256), 256, 0, st>>>(N, nl->offsets.as<int>(), nl->nbr.as<int>(),
                                                  nl->rev.as<int>());
+  if (nl->lforce.p) k_set_flag<<<1, 1, 0, st>>>(nl->lforce.as<int>());  // live repack: redo
   CK(cudaGetLastError());
   return TB_OK;
 }
@@ -1888,8 +1911,10 @@ static MdKey md_key(const tb_context *ctx, const tb_nlist *nl, const MdArgs &m) 
                      nl->row_count.p, nl->nl_row.p, nl->sorted_atoms.p, nl->sort_keys.p,
                      nl->iota.p, nl->lanes.p, nl->cpos.p, nl->crow.p, nl->coff.p, nl->centry.p,
                      nl->fbuf.p, ctx->facc.p, ctx->partials.p, ctx->ke_part.p, ctx->errf.p,
-                     ctx->scan_tmp.p, nl->scratch.p, m.ref_log};
-  static_assert(sizeof(p) / sizeof(p[0]) <= 40, "MdKey::ptr too small");
+                     ctx->scan_tmp.p, nl->scratch.p, m.ref_log, nl->lplan.p, nl->llen.p,
+                     nl->lrow.p, nl->lrowj.p, nl->lsorted.p, nl->llanes.p, nl->lref.p,
+                     nl->lgate.p, nl->lforce.p, nl->fnbr.p, nl->fspecies.p};
+  static_assert(sizeof(p) / sizeof(p[0]) <= 48, "MdKey::ptr too small");
   memcpy(k.ptr, p, sizeof(p));
   k.n = m.n;
   k.ecap = nl->ecap;
@@ -1908,6 +1933,8 @@ static MdKey md_key(const tb_context *ctx, const tb_nlist *nl, const MdArgs &m) 
   k.skin = m.skin;
   k.r_cut = m.r_cut;
   k.loose = m.loose;
+  k.margin = ctx->repack_margin;
+  k.lcap = nl->lcap;
   k.rebuild_every = m.rebuild_every;
   k.precision = m.precision;
   k.scatter = m.scatter;
@@ -2041,6 +2068,15 @@ static int md_prepare(tb_context *ctx, tb_nlist *nl, const int *d_species, int s
     if (rc) return rc;
   }
   CK(nl->plan.ensure(sizeof(DevPlan)));
+  if (filter_wanted && scatter == TB_SCATTER_ATOMIC && ctx->md_live && ctx->repack_margin > 0 &&
+      ctx->live_pack != 0) {
+    int rc = live_reserve(ctx, nl, true);
+    if (rc) return rc;
+    CK(nl->lforce.ensure(sizeof(int)));
+    const int one = 1;
+    CK(cudaMemcpyAsync(nl->lforce.p, &one, sizeof(int), cudaMemcpyHostToDevice, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+  }
   CK(nl->centry.ensure(sizeof(int) * nl->ecap));
   CK(nl->crow.ensure(sizeof(int) * (N + 1)));
   CK(nl->coff.ensure(sizeof(int) * (N + 1)));
@@ -2108,7 +2144,7 @@ extern "C" int tb_md_run(tb_context *ctx, tb_nlist *nl, int64_t n, double *d_pos
   // kept (ref_log) -- and the exact list at the last of them is rebuilt when
   // the run ends.  Pair terms are the same either way: every evaluation
   // re-tests r < r_cut on a list that holds all such pairs.
-  const bool loose = ctx->md_loose > 0 && ctx->S == 1 && scatter == TB_SCATTER_ATOMIC;
+  const bool loose = ctx->md_loose > 0 && scatter == TB_SCATTER_ATOMIC;
   const double skin_list = loose ? skin + ctx->md_loose : skin;
   // snapshot: x, v, F, E of the entry state and the entry list's reference
   // positions (every failing exit rebuilds that exact list: the in-graph

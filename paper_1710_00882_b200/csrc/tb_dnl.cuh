@@ -330,16 +330,26 @@ __global__ void __launch_bounds__(256) k_bucket_fill(int n, const int *__restric
 // when some atom moved more than margin/2 since the last repack; a repack
 // starts from a zeroed plan (what the ungated path's memset does)
 __global__ void k_repack_gate(const unsigned long long *__restrict__ drift_bits, double thr2,
-                              int force, int *__restrict__ go, DevPlan *__restrict__ plan) {
+                              int force, int *__restrict__ force_dev, int *__restrict__ go,
+                              DevPlan *__restrict__ plan) {
+  // force_dev: set by the device list rebuild inside tb_md_run's graph (the
+  // host cannot know when that happens)
   __shared__ int need;
-  if (threadIdx.x == 0) need = force || __longlong_as_double((long long)*drift_bits) > thr2;
+  if (threadIdx.x == 0)
+    need = force || (force_dev && *force_dev) ||
+           __longlong_as_double((long long)*drift_bits) > thr2;
   __syncthreads();
-  if (threadIdx.x == 0) *go = need;
+  if (threadIdx.x == 0) {
+    *go = need;
+    if (force_dev) *force_dev = 0;
+  }
   if (need) {
     int *p = reinterpret_cast<int *>(plan);
     for (int k = threadIdx.x; k < (int)(sizeof(DevPlan) / sizeof(int)); k += blockDim.x) p[k] = 0;
   }
 }
+
+__global__ void k_set_flag(int *__restrict__ flag) { *flag = 1; }
 
 // histogram of row lengths into the device plan (block-private bins)
 __global__ void k_len_hist_plan(int n, const int *__restrict__ len, DevPlan *__restrict__ plan,
