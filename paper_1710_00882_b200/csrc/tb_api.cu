@@ -89,6 +89,7 @@ struct tb_context {
 #endif
   double repack_margin = TB_REPACK_MARGIN_DEFAULT;  // TB_OPT_REPACK_MARGIN (A)
   bool md_live = getenv("TB_NO_MD_REPACK") == nullptr;  // live repack inside tb_md_run (S > 1)
+  bool nl_atoms = getenv("TB_NL_CELLS") == nullptr;  // atom-centric list scan (all-periodic grids)
   bool warp_per_chunk = getenv("TB_WARP_PER_CHUNK") != nullptr;
   bool no_filter = getenv("TB_NO_FILTER") != nullptr;  // disable the species-pair compute filter
   bool err_unchecked = false;     // kernels may have raised error flags nobody read yet
@@ -843,7 +844,12 @@ static int build_owned(tb_context *ctx, tb_nlist *nl, int64_t n, int64_t n_owned
     CK(cudaGetLastError());
     // single pass: rows of <= TMPW entries land in the scratch rows, counts,
     // max row and the row-length histogram (for the warp chunks) come along
-    if (c1 > c0)
+    if (c1 > c0 && g.stencil_image == 2 && ctx->nl_atoms)
+      k_nl_atoms<<<nblk(N, 256), 256, 0, ctx->stream>>>(
+          (int)c0, (int)c1, (int)n_owned, nl->cpos.as<double4>(), g, bc * bc,
+          nl->cell_start.as<int>(), nl->row_count.as<int>(), nl->scratch.as<int>(),
+          nl->maxrow.as<int>(), nl->hist.as<int>(), nl->maxrow.as<int>() + 1);
+    else if (c1 > c0)
       k_nl_cells<<<nblk(c1 - c0, 8), 256, 0, ctx->stream>>>(
           (int)c1, (int)n_owned, nl->cpos.as<double4>(), g, bc * bc, nl->cell_start.as<int>(),
           nl->row_count.as<int>(), nl->scratch.as<int>(), nl->maxrow.as<int>(),
@@ -1825,10 +1831,16 @@ static int enqueue_rebuild_device(tb_context *ctx, tb_nlist *nl, const double *d
       N, d_pos, nl->atom_cell.as<int>(), nl->cell_start.as<int>(), nl->cell_count.as<int>(),
       nl->cell_atoms.as<int>(), nl->cpos.as<double4>(), nl->ref_pos.as<double>());
   const double bc2 = nl->bc * nl->bc;
-  k_nl_cells<<<nblk(nl->ncell, 8), 256, 0, st>>>(
-      (int)nl->ncell, N, nl->cpos.as<double4>(), g, bc2, nl->cell_start.as<int>(),
-      nl->row_count.as<int>(), nl->scratch.as<int>(), &plan->max_row, plan->hist,
-      &plan->unwrapped);
+  if (g.stencil_image == 2 && ctx->nl_atoms)
+    k_nl_atoms<<<nblk(N, 256), 256, 0, st>>>(0, (int)nl->ncell, N, nl->cpos.as<double4>(), g, bc2,
+                                              nl->cell_start.as<int>(), nl->row_count.as<int>(),
+                                              nl->scratch.as<int>(), &plan->max_row, plan->hist,
+                                              &plan->unwrapped);
+  else
+    k_nl_cells<<<nblk(nl->ncell, 8), 256, 0, st>>>(
+        (int)nl->ncell, N, nl->cpos.as<double4>(), g, bc2, nl->cell_start.as<int>(),
+        nl->row_count.as<int>(), nl->scratch.as<int>(), &plan->max_row, plan->hist,
+        &plan->unwrapped);
   CK(cudaGetLastError());
   rc = exclusive_scan(ctx, nl->row_count.as<int>(), nl->offsets.as<int>(), N + 1);
   if (rc) return rc;
