@@ -247,7 +247,7 @@ static Box make_box(const double *L, const int *per) {
 
 static inline int nblk(int64_t n, int t) { return (int)((n + t - 1) / t); }
 
-constexpr int SCAN_G = 8;  // lanes per atom in the CSR compaction
+constexpr int SCAN_G = 4;  // lanes per atom in the CSR compaction (rows of ~4-8 entries)
 
 // ---------------------------------------------------------------------------
 // parameter tables (potential.py:127-155 column order)
@@ -614,9 +614,9 @@ static int build_chunks(tb_context *ctx, tb_nlist *nl, const int *row_len, const
   nl->ccap = chunks + (int64_t)(nl->margin * (double)chunks) + (nl->margin > 0 ? 64 : 0);
   if (chunks > 0) {
     CK(nl->lanes.ensure(sizeof(int4) * 32 * (size_t)nl->ccap));
-    k_fill_lanes<<<chunks, 32, 0, ctx->stream>>>(plan, nl->sorted_atoms.as<int>(),
+    k_fill_lanes<<<nblk(chunks, 8), 256, 0, ctx->stream>>>(plan, nl->sorted_atoms.as<int>(),
                                                   coff ? coff : nl->offsets.as<int>(), centry,
-                                                  nl->nbr.as<int>(), nl->lanes.as<int4>());
+                                                  nl->nbr.as<int>(), nl->lanes.as<int4>(), chunks);
     CK(cudaGetLastError());
   }
   nl->nchunks = chunks;
@@ -883,18 +883,17 @@ static int build_owned(tb_context *ctx, tb_nlist *nl, int64_t n, int64_t n_owned
   nl->grid = g;
   nl->ncell = ncell;
   CK(nl->nbr.ensure(sizeof(int) * nl->ecap));
-  CK(nl->nl_row.ensure(sizeof(int) * nl->ecap));
   if (N && nl->max_row <= TMPW) {
     k_nl_compact<SCAN_G><<<nblk((int64_t)N * SCAN_G, 256), 256, 0, ctx->stream>>>(
         N, nl->scratch.as<int>(), nl->row_count.as<int>(), nl->offsets.as<int>(),
-        nl->nbr.as<int>(), nl->nl_row.as<int>(), nullptr);
+        nl->nbr.as<int>(), nullptr, nullptr);
     CK(cudaGetLastError());
   } else if (N) {
     // rows longer than the scratch rows: second full scan straight into CSR
     k_nl_scan<true><<<nblk(N, 128), 128, 0, ctx->stream>>>(
         N, (int)n_owned, nl->cpos.as<double4>(), g, bc * bc, nl->atom_cell.as<int>(), nl->cell_start.as<int>(),
         nl->cell_atoms.as<int>(), nullptr, nl->offsets.as<int>(), nl->nbr.as<int>(), nullptr,
-        nl->nl_row.as<int>());
+        nullptr);
     CK(cudaGetLastError());
   }
   if (N) {
@@ -1850,7 +1849,7 @@ static int enqueue_rebuild_device(tb_context *ctx, tb_nlist *nl, const double *d
   k_guard_offsets<<<nblk(N + 1, 256), 256, 0, st>>>(N, plan, nl->offsets.as<int>());
   k_nl_compact<SCAN_G><<<nblk((int64_t)N * SCAN_G, 256), 256, 0, st>>>(
       N, nl->scratch.as<int>(), nl->row_count.as<int>(), nl->offsets.as<int>(), nl->nbr.as<int>(),
-      nl->nl_row.as<int>(), &plan->list_overflow);
+      nullptr, &plan->list_overflow);
   CK(cudaGetLastError());
   const int *row_len = nl->row_count.as<int>(), *loff = nl->offsets.as<int>();
   const int *cent = nullptr;

@@ -361,7 +361,8 @@ __global__ void __launch_bounds__(128) k_nl_scan(int n, int n_owned, const doubl
         }
       }
     if (FILL) {
-      for (int u = 0; u < cnt; ++u) nl_row[base + u] = i;
+      if (nl_row)
+        for (int u = 0; u < cnt; ++u) nl_row[base + u] = i;
       // rows ascending by j (neighbor.py:210-212); rows are short
       int *rowp = nbr + base;
       for (int u = 1; u < cnt; ++u) {
@@ -673,7 +674,7 @@ __global__ void __launch_bounds__(256) k_nl_compact(int n, const int *__restrict
     int rank = 0;
     for (int q = 0; q < cnt; ++q) rank += src[q] < v;
     nbr[base + rank] = v;
-    nl_row[base + rank] = i;
+    if (nl_row) nl_row[base + rank] = i;
   }
 }
 

@@ -865,11 +865,17 @@ __global__ void k_len_hist(int n, const int *__restrict__ len, int *__restrict__
   if (threadIdx.x < 34 && h[threadIdx.x]) atomicAdd(hist + threadIdx.x, h[threadIdx.x]);
 }
 
-// one warp per chunk: lane -> {entry, i, j, L} (entry -1: idle lane)
-__global__ void k_fill_lanes(const ChunkPlan plan, const int *__restrict__ sorted_atoms,
-                             const int *__restrict__ offsets, const int *__restrict__ centry,
-                             const int *__restrict__ nbr, int4 *__restrict__ lanes) {
-  const int c = blockIdx.x, lane = threadIdx.x;
+// one warp per chunk (8 chunks per 256-thread block: 1-warp blocks made the
+// block scheduler the limit, config 5 1.09 ms): lane -> {entry, i, j, L}
+// (entry -1: idle lane)
+__global__ void __launch_bounds__(256) k_fill_lanes(const ChunkPlan plan,
+                                                    const int *__restrict__ sorted_atoms,
+                                                    const int *__restrict__ offsets,
+                                                    const int *__restrict__ centry,
+                                                    const int *__restrict__ nbr,
+                                                    int4 *__restrict__ lanes, int nchunks) {
+  const int c = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (c >= nchunks) return;
   int L = 1;
   while (L < 32 && plan.chunk_base[L + 1] <= c) ++L;
   const int rpc = 32 / L;
