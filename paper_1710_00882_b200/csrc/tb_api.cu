@@ -1996,9 +1996,8 @@ static int md_capture(tb_context *ctx, tb_nlist *nl, const MdArgs &m, MdGraph *G
   int rc = TB_OK;
   do {
     const double hl = 0.5 * (m.skin + m.loose);
-    k_md_kick_drift<<<nblk(n, 256), 256, 0, s0>>>(n, m.pos, m.vel, m.forces, m.mass,
-                                                   nl->ref_pos.as<double>(), half, m.dt, box,
-                                                   plan, m.loose > 0 ? m.ref_log : nullptr);
+    // (step 1's kick + drift is launched by tb_md_run ahead of the graph; each
+    // step's second kick carries the next step's first kick + drift)
     k_md_decide<<<1, 1, 0, s0>>>(plan, hs * hs, m.rebuild_every, h_reb, m.loose > 0 ? 1 : 0,
                                  hl * hl);
     if (cudaGetLastError() != cudaSuccess) {
@@ -2046,13 +2045,16 @@ static int md_capture(tb_context *ctx, tb_nlist *nl, const MdArgs &m, MdGraph *G
     if (rc) break;
     const int nparts = fuse ? ctx->last_blocks : 0;
     if (fuse)
-      k_md_kick_ke<true><<<kb, 256, 0, s0>>>(n, m.vel, m.forces, m.mass, half,
-                                             ctx->ke_part.as<double>(), ctx->facc.as<double>(),
-                                             plan, m.pos, m.loose > 0 ? m.ref_log : nullptr);
+      k_md_kick2_drift<true><<<kb, 256, 0, s0>>>(n, m.pos, m.vel, m.forces, m.mass, half, m.dt,
+                                                 box, ctx->ke_part.as<double>(),
+                                                 ctx->facc.as<double>(), plan,
+                                                 nl->ref_pos.as<double>(),
+                                                 m.loose > 0 ? m.ref_log : nullptr);
     else
-      k_md_kick_ke<false><<<kb, 256, 0, s0>>>(n, m.vel, m.forces, m.mass, half,
-                                              ctx->ke_part.as<double>(), nullptr, plan, m.pos,
-                                              m.loose > 0 ? m.ref_log : nullptr);
+      k_md_kick2_drift<false><<<kb, 256, 0, s0>>>(n, m.pos, m.vel, m.forces, m.mass, half, m.dt,
+                                                  box, ctx->ke_part.as<double>(), nullptr, plan,
+                                                  nl->ref_pos.as<double>(),
+                                                  m.loose > 0 ? m.ref_log : nullptr);
     k_md_tail<<<1, 256, 0, s0>>>(kb, ctx->ke_part.as<double>(), 0.5 / m.accel, m.result, plan,
                                  m.series, m.record_every, h_loop, nparts,
                                  ctx->partials.as<double>());
@@ -2222,6 +2224,13 @@ extern "C" int tb_md_run(tb_context *ctx, tb_nlist *nl, int64_t n, double *d_pos
     hp.max_row = (int)nl->max_row;
     hp.target = (int)steps;
     CK(cudaMemcpyAsync(nl->plan.p, &hp, sizeof(hp), cudaMemcpyHostToDevice, ctx->stream));
+    {  // step 1's half-kick + drift (later steps' are fused into the graph's kick pass)
+      const Box box = make_box(nl->L, nl->per);
+      k_md_kick_drift<<<nblk(n, 256), 256, 0, ctx->stream>>>(
+          (int)n, d_positions, d_velocities, d_forces, d_mass, nl->ref_pos.as<double>(),
+          0.5 * dt * accel, dt, box, nl->plan.as<DevPlan>(), loose ? m.ref_log : nullptr);
+      CK(cudaGetLastError());
+    }
     CK(cudaGraphLaunch(nl->md->exec, ctx->stream));
     CK(cudaMemcpyAsync(&hp, nl->plan.p, sizeof(hp), cudaMemcpyDeviceToHost, ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));

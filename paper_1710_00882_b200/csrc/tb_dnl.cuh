@@ -419,6 +419,96 @@ __global__ void __launch_bounds__(256) k_md_kick_ke(int n, double *__restrict__ 
 // the WHILE handle continues while steps remain and nothing overflowed
 // nparts > 0 (fused step): also E and the virial from the Tersoff kernel's
 // block partials (8 doubles per block), the finalize kernel's reduction
+// Second half-kick of step s fused with the first half-kick + drift of step
+// s + 1 (one pass over v, F, m, x instead of two; the same operations in the
+// same order, so the trajectory is bit-identical to the separate kernels):
+//   v1 = v + half F(s)/m          E_kin(s) partials from v1
+//   [s < target]  v2 = v1 + half F(s)/m, x += dt v2, wrap, drift^2 maxima
+// FUSED (atomic scatter): F comes out of the Tersoff accumulator (copied to
+// f with the +0.0 flush and re-zeroed).  Loose-list runs keep x(s) in ref_log
+// when step s is one of the reference's rebuilds.  Fixed grid: the KE partials
+// are deterministic.
+template <bool FUSED>
+__global__ void __launch_bounds__(256) k_md_kick2_drift(int n, double *__restrict__ pos,
+                                                        double *__restrict__ vel,
+                                                        double *__restrict__ f,
+                                                        const double *__restrict__ mass,
+                                                        double half, double dt, Box box,
+                                                        double *__restrict__ part,
+                                                        double *__restrict__ facc,
+                                                        DevPlan *__restrict__ plan,
+                                                        const double *__restrict__ ref,
+                                                        double *__restrict__ ref_log) {
+  __shared__ double s[8];
+  double acc = 0.0;
+  unsigned long long best = 0, best_log = 0;
+  const bool keep = ref_log && plan->log_now;
+  const bool next = plan->step < plan->target && plan->overflow == 0;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const double m = mass[i];
+    double x[3], v[3];
+#pragma unroll
+    for (int ax = 0; ax < 3; ++ax) {
+      const int64_t k = 3 * (int64_t)i + ax;
+      x[ax] = pos[k];
+      double fk;
+      if (FUSED) {
+        fk = __ldcg(facc + k) + 0.0;
+        f[k] = fk;
+        facc[k] = 0.0;
+      } else {
+        fk = f[k];
+      }
+      const double dv = __ddiv_rn(__dmul_rn(half, fk), m);
+      v[ax] = __dadd_rn(vel[k], dv);
+      if (next) {
+        const double v2 = __dadd_rn(v[ax], dv);
+        vel[k] = v2;
+        double xx = __dadd_rn(x[ax], __dmul_rn(dt, v2));
+        if (box.per[ax]) xx = np_remainder(xx, box.L[ax]);
+        pos[k] = xx;
+      } else {
+        vel[k] = v[ax];
+      }
+    }
+    acc += m * ((v[0] * v[0] + v[1] * v[1]) + v[2] * v[2]);
+    if (keep) {
+#pragma unroll
+      for (int ax = 0; ax < 3; ++ax) ref_log[3 * (int64_t)i + ax] = x[ax];
+    }
+    if (next) {
+      double xn[3], r[3], d[3];
+      load3(pos, i, xn);
+      load3(ref, i, r);
+      const unsigned long long b = __double_as_longlong(disp_r2(r, xn, box, d));
+      best = b > best ? b : best;
+      if (ref_log) {
+        load3(ref_log, i, r);
+        const unsigned long long bl = __double_as_longlong(disp_r2(r, xn, box, d));
+        best_log = bl > best_log ? bl : best_log;
+      }
+    }
+  }
+  acc = warp_sum(acc);
+  for (int o = 16; o > 0; o >>= 1) {
+    unsigned long long w = __shfl_down_sync(0xffffffffu, best, o);
+    best = w > best ? w : best;
+    w = __shfl_down_sync(0xffffffffu, best_log, o);
+    best_log = w > best_log ? w : best_log;
+  }
+  if ((threadIdx.x & 31) == 0) {
+    s[threadIdx.x >> 5] = acc;
+    if (best) atomicMax(&plan->drift_bits, best);
+    if (best_log) atomicMax(&plan->drift_log_bits, best_log);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += s[w];
+    part[blockIdx.x] = t;
+  }
+}
+
 __global__ void k_md_tail(int nb, const double *__restrict__ part, double scale,
                           double *__restrict__ result, DevPlan *__restrict__ plan,
                           double *__restrict__ series, int every,
