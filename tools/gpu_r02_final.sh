@@ -1,7 +1,7 @@
 # Round-2 verification + measurement on one B200 (run from the repo root):
 # GPU tests, smoke, the bench (default = config 5) and its reference arm, the
 # two-rank functional run, per-config table, ncu launch list + --set full.
-O=gpurun_out/r02_final; mkdir -p $O
+O=${OUT:-gpurun_out/r02_final}; mkdir -p $O
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv > $O/smi.txt
 timeout 1500 python -m pytest tests -m gpu -q -p no:cacheprovider > $O/pytest_gpu.txt 2>&1; echo "pytest rc=$?"
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.txt 2>&1; echo "smoke rc=$?"
