@@ -75,6 +75,9 @@ struct WarpCfg {
   static constexpr int minb = sizeof(T) == 8 ? TB_WARP_MINB64 : TB_WARP_MINB_F;
 };
 constexpr int QCAP = 4;   // k-iterations whose angular values are cached
+#ifndef TB_MIXED_NO_SCACHE
+#define TB_MIXED_NO_SCACHE 1
+#endif
 #ifndef TB_MIXED_LC8
 #define TB_MIXED_LC8 0  // measured: c4 mixed -2%, c3 mixed +19%, c5 mixed +14% (code size / registers)
 #endif
@@ -315,6 +318,10 @@ __device__ __forceinline__ void chunk_body(const KArgs &a, const WArgs &w, const
   // recomputed in phase 2 from the partner's unit vector it loads anyway
   constexpr bool RC2 = !RC && LC > 0 && S == 1 && TB_FP64_RC2;
   T rcos[RC ? QCAP : 1], rg[RC || RC2 ? QCAP : 1], rdg[RC || RC2 ? QCAP : 1];
+  // dynamic-length rows of the mixed kernel: no shared-memory angular cache --
+  // phase 2 recomputes g, dg (~10 FP32 ops) instead of 3 STS + 3 LDS per
+  // partner, the L1/shared pipe being that kernel's bottleneck
+  constexpr bool SC = !(sizeof(T) == 4 && LC == 0 && TB_MIXED_NO_SCACHE);
   T zeta = T(0);
   // two species with i-only angular constants: in registers for the row
   const bool ang_i = S > 1 && tab.ang_i;
@@ -350,7 +357,7 @@ __device__ __forceinline__ void chunk_body(const KArgs &a, const WArgs &w, const
       angular(cost, ai, g, dg);
     else
       angular(cost, tp, g, dg);
-    if (q < QCAP) {
+    if (SC && q < QCAP) {
       if (RC) {
         rcos[q] = cost;
         rg[q] = g;
@@ -435,7 +442,7 @@ __device__ __forceinline__ void chunk_body(const KArgs &a, const WArgs &w, const
     const typename Vec4<T>::t be = tb.e(src);
     const T rb = be.w;
     T cost, g, dg;
-    if (q < QCAP) {
+    if (SC && q < QCAP) {
       if (RC) {
         cost = rcos[q];
         g = rg[q];
