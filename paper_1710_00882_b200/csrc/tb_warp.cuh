@@ -78,6 +78,9 @@ constexpr int QCAP = 4;   // k-iterations whose angular values are cached
 #ifndef TB_MIXED_NO_SCACHE
 #define TB_MIXED_NO_SCACHE 1
 #endif
+#ifndef TB_FP64_NO_SCACHE
+#define TB_FP64_NO_SCACHE 0
+#endif
 #ifndef TB_MIXED_LC8
 #define TB_MIXED_LC8 0  // measured: c4 mixed -2%, c3 mixed +19%, c5 mixed +14% (code size / registers)
 #endif
@@ -321,7 +324,7 @@ __device__ __forceinline__ void chunk_body(const KArgs &a, const WArgs &w, const
   // dynamic-length rows of the mixed kernel: no shared-memory angular cache --
   // phase 2 recomputes g, dg (~10 FP32 ops) instead of 3 STS + 3 LDS per
   // partner, the L1/shared pipe being that kernel's bottleneck
-  constexpr bool SC = !(sizeof(T) == 4 && LC == 0 && TB_MIXED_NO_SCACHE);
+  constexpr bool SC = !(LC == 0 && (sizeof(T) == 4 ? TB_MIXED_NO_SCACHE : TB_FP64_NO_SCACHE));
   T zeta = T(0);
   // two species with i-only angular constants: in registers for the row
   const bool ang_i = S > 1 && tab.ang_i;
