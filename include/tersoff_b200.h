@@ -95,6 +95,16 @@ int tb_set_stream(tb_context *ctx, void *stream);
  * exactly at every evaluation.  (Wider margins keep the repack across MD steps
  * but add dead lanes: config 3 step 261 / 276 / 331 us at 1 / 10 / 50 mA.) */
 #define TB_OPT_REPACK_MARGIN 5
+/* TB_OPT_STREAM_RANGE = r (default 131072, 0 = off): tb_compute called with
+ * PINNED host positions / forces / per-atom energies on a system of at least
+ * 8 r atoms (one species, atomic scatter) streams the call: the atoms are cut
+ * into up to 32 index ranges of at least r atoms, a warp chunk runs as soon as
+ * the ranges it references are on the device, and a range's forces go back
+ * once the last chunk touching it has run -- host-to-device copy, kernel and
+ * device-to-host copy overlap (PCIe is full duplex).  Same chunks, same
+ * arithmetic as the unstreamed call; pays off when the atom order is
+ * spatially coherent (lattice order), falls back to sequential otherwise. */
+#define TB_OPT_STREAM_RANGE 6
 int tb_set_option(tb_context *ctx, int option, int value);
 
 /* Synchronise the context's stream. */

@@ -27,6 +27,7 @@ OPT_LIST_MARGIN = 2  # percent of spare list entries / warp chunks (tb_md_run)
 OPT_LIVE_PACK = 3  # 0 off / 1 on / 2 auto: rows cut to r < r_cut and re-chunked per evaluation
 OPT_MD_LOOSE_SKIN = 4  # tb_md_run list skin extra in 1/100 A (default 30; 0 = exact list)
 OPT_REPACK_MARGIN = 5  # live repack margin in 1/1000 A (default 1; 0 = repack every evaluation)
+OPT_STREAM_RANGE = 6  # tb_compute with pinned host buffers: atoms per streamed range (default 131072; 0 = off)
 
 # symbol -> (restype, argtypes); the exported surface of the C ABI
 _P = ctypes.c_void_p

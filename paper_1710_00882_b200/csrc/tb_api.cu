@@ -24,6 +24,7 @@
 #include "tb_warp.cuh"
 #include "tb_dnl.cuh"
 #include "tb_dd.cuh"
+#include "tb_stream.cuh"
 
 #ifndef TB_VERSION_TAG
 #define TB_VERSION_TAG "dev"
@@ -101,6 +102,14 @@ struct tb_context {
   cudaStream_t side = nullptr;
   const int *dplan = nullptr;  // tb_md_run capture: device {nchunks, n_empty}
   bool md_fuse = false;  // tb_md_run capture (atomic): finalize folded into the kick kernels
+  // streamed tb_compute (tb_stream.cuh): pinned host buffers, ranges of atoms
+  // copied in / evaluated / copied out concurrently
+  int stream_range = 131072;  // TB_OPT_STREAM_RANGE: atoms per range at least; 0 = off
+  cudaStream_t s_h2d = nullptr, s_d2h = nullptr;
+  std::vector<cudaEvent_t> ev_h2d, ev_stage;
+  cudaEvent_t ev_fork = nullptr;
+  struct StreamCtl *sctl = nullptr;  // set by tb_compute around enqueue_compute
+  int part_off = 0;     // first block-partial slot of the next warp launch
   int last_blocks = 0;  // grid of the last Tersoff launch (partials to reduce)  // tb_set_option(TB_OPT_TILE_KERNEL): general tile kernel only
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_used, ev_free;
 };
@@ -146,8 +155,22 @@ struct tb_nlist {
   double lmargin = -1.0;
   bool fnbr_ok = false;  // fnbr matches centry (written by every filter pass since)
   int64_t lcap = 0;  // chunk capacity of llanes
+  // streamed tb_compute: chunks sorted by stage (tb_stream.cuh)
+  int64_t lanes_version = 0;  // bumped whenever `lanes` is rewritten
+  int64_t sp_version = -1;
+  int sp_K = 0, sp_R = 0;
+  std::vector<int> sp_cstart, sp_fin;  // [K+1] first chunk of a stage; [K] last stage touching a range
+  DevBuf sp_lanes, sp_tmp;
   bool imported = false;  // rows from tb_nlist_import (no cell grid: no device rebuild)
   struct MdGraph *md = nullptr;
+};
+
+// streamed tb_compute: host endpoints of one call (tb_stream.cuh)
+struct StreamCtl {
+  const double *h_pos;   // pinned host positions (n,3)
+  double *h_forces;      // pinned host forces (n,3)
+  double *h_per_atom;    // pinned host per-atom energies (n) or nullptr
+  double *d_pos;         // device staging of the positions
 };
 
 // captured device-resident NVE loop (tb_md_run), reused while its key holds
@@ -365,6 +388,11 @@ extern "C" void tb_destroy(tb_context *ctx) {
       cudaEventDestroy(ev.second);
     }
   if (ctx->side) cudaStreamDestroy(ctx->side);
+  if (ctx->s_h2d) cudaStreamDestroy(ctx->s_h2d);
+  if (ctx->s_d2h) cudaStreamDestroy(ctx->s_d2h);
+  for (auto *v : {&ctx->ev_h2d, &ctx->ev_stage})
+    for (cudaEvent_t ev : *v) cudaEventDestroy(ev);
+  if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
   if (ctx->ev_kernel_done) cudaEventDestroy(ctx->ev_kernel_done);
   if (ctx->h_err) cudaFreeHost(ctx->h_err);
   if (ctx->h_small) cudaFreeHost(ctx->h_small);
@@ -409,6 +437,11 @@ extern "C" int tb_set_option(tb_context *ctx, int option, int value) {
   if (option == TB_OPT_LIST_MARGIN) {
     if (value < 0 || value > 1000) return fail(ctx, TB_ERR_ARG, "list margin %d%% out of range", value);
     ctx->list_margin = value / 100.0;
+    return TB_OK;
+  }
+  if (option == TB_OPT_STREAM_RANGE) {
+    if (value < 0) return fail(ctx, TB_ERR_ARG, "stream range %d out of range", value);
+    ctx->stream_range = value;
     return TB_OK;
   }
   return fail(ctx, TB_ERR_ARG, "unknown option %d", option);
@@ -555,7 +588,8 @@ extern "C" void tb_nlist_destroy(tb_nlist *nl) {
                     &nl->iota, &nl->lanes, &nl->hist, &nl->cpos, &nl->crow, &nl->coff,
                     &nl->centry, &nl->fnbr, &nl->fbuf, &nl->plan, &nl->scratch, &nl->lplan,
                     &nl->llen, &nl->lrow, &nl->lrowj, &nl->lsorted, &nl->llanes, &nl->ref_log,
-                    &nl->fspecies, &nl->lref, &nl->lgate, &nl->lforce};
+                    &nl->fspecies, &nl->lref, &nl->lgate, &nl->lforce, &nl->sp_lanes,
+                    &nl->sp_tmp};
   for (DevBuf *b : bufs) b->release();
   md_graph_release(nl);
   delete nl;
@@ -620,6 +654,45 @@ static int build_chunks(tb_context *ctx, tb_nlist *nl, const int *row_len, const
     CK(cudaGetLastError());
   }
   nl->nchunks = chunks;
+  nl->lanes_version++;
+  return TB_OK;
+}
+
+// Stage plan of the streamed tb_compute (tb_stream.cuh): K ranges of R atoms,
+// chunks sorted stably by stage into sp_lanes; cached per list version.
+static int stream_plan(tb_context *ctx, tb_nlist *nl, int K, int R) {
+  if (nl->sp_version == nl->lanes_version && nl->sp_K == K && nl->sp_R == R) return TB_OK;
+  const int nc = nl->nchunks;
+  // [stage nc | order nc | hist 34 | touch 32]
+  CK(nl->sp_tmp.ensure(sizeof(int) * (2 * (size_t)nc + 34 + STREAM_KMAX)));
+  int *stage = nl->sp_tmp.as<int>(), *order = stage + nc, *hist = order + nc;
+  unsigned *touch = reinterpret_cast<unsigned *>(hist + 34);
+  CK(nl->sp_lanes.ensure(sizeof(int4) * 32 * (size_t)nc));
+  CK(ctx->scan_tmp.ensure(sizeof(int) * lsort_scratch(nc)));
+  CK(cudaMemsetAsync(hist, 0, sizeof(int) * (34 + STREAM_KMAX), ctx->stream));
+  k_chunk_stage<<<nblk(nc, 8), 256, 0, ctx->stream>>>(nl->lanes.as<int4>(), nc, R, stage, touch);
+  k_len_hist<<<std::min(nblk(nc, 256), 592), 256, 0, ctx->stream>>>(nc, stage, hist);
+  CK(sort_by_length(stage, nc, order, ctx->scan_tmp.as<int>(), ctx->stream));
+  k_permute_chunks<<<nblk(nc, 8), 256, 0, ctx->stream>>>(nl->lanes.as<int4>(), order,
+                                                         nl->sp_lanes.as<int4>(), nc);
+  CK(cudaGetLastError());
+  int h[34 + STREAM_KMAX];
+  CK(cudaMemcpyAsync(h, hist, sizeof(h), cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  nl->sp_cstart.assign(K + 1, 0);
+  for (int q = 0; q < K; ++q) nl->sp_cstart[q + 1] = nl->sp_cstart[q] + h[q];
+  if (nl->sp_cstart[K] != nc) return fail(ctx, TB_ERR_CUDA, "internal error: stage plan");
+  // a range's forces / per-atom energies are final after the last stage that
+  // touches it; atoms with empty rows are written by the last launch
+  nl->sp_fin.assign(K, nl->n_empty > 0 ? K - 1 : 0);
+  for (int q = 0; q < K; ++q) {
+    const unsigned m = (unsigned)h[34 + q];
+    for (int r = 0; r < K; ++r)
+      if (m >> r & 1u) nl->sp_fin[r] = std::max(nl->sp_fin[r], q);
+  }
+  nl->sp_version = nl->lanes_version;
+  nl->sp_K = K;
+  nl->sp_R = R;
   return TB_OK;
 }
 
@@ -910,6 +983,7 @@ static int build_owned(tb_context *ctx, tb_nlist *nl, int64_t n, int64_t n_owned
     if (rc2) return rc2;
   } else {
     nl->nchunks = 0;
+    nl->lanes_version++;
     nl->n_empty = 0;
   }
   nl->built = true;
@@ -1009,6 +1083,7 @@ extern "C" int tb_nlist_import(tb_context *ctx, tb_nlist *nl, int64_t n, const i
     if (rc) return rc;
   } else {
     nl->nchunks = 0;
+    nl->lanes_version++;
     nl->n_empty = 0;
   }
   CK(cudaStreamSynchronize(ctx->stream));  // host staging vectors go out of scope
@@ -1161,8 +1236,9 @@ static int launch_warp_t(tb_context *ctx, const tb_nlist *nl, KArgs &a, WArgs &w
   int need = nblk(w.nchunks, WarpCfg<T>::wpb);
   // persistent grid: one resident wave, warps stride over the chunks
   int nb = std::max(1, ctx->warp_per_chunk ? need : std::min(need, sms * per_sm));
-  CK(ctx->partials.ensure(sizeof(double) * 8 * nb));
-  a.partials = ctx->partials.as<double>();
+  if (ctx->part_off == 0) CK(ctx->partials.ensure(sizeof(double) * 8 * nb));
+  // (streamed stages: pre-sized by the caller, one slot range per launch)
+  a.partials = ctx->partials.as<double>() + 8 * (int64_t)ctx->part_off;
   Tables<T, S> tab = make_tables<T, S>(ctx);
   std::pair<cudaEvent_t, cudaEvent_t> ev{nullptr, nullptr};
   if (ctx->profile) {
@@ -1436,7 +1512,8 @@ static int enqueue_compute(tb_context *ctx, const tb_nlist *nl, const double *d_
   // pinned buffers) and the fused MD graph keep the accumulator.
   // (below ~256k atoms the extra memset node costs more than the copy it
   // saves: config 2 step 24.9 -> 26.7 us; config 5 2.86 -> 2.60 ms)
-  const bool direct = direct_ok && scatter == TB_SCATTER_ATOMIC && !ctx->md_fuse && n >= (1 << 18);
+  const bool direct = direct_ok && scatter == TB_SCATTER_ATOMIC && !ctx->md_fuse &&
+                      (n >= (1 << 18) || ctx->sctl);
   if (direct) CK(cudaMemsetAsync(d_forces, 0, sizeof(double) * 3 * (size_t)n, ctx->stream));
   a.forces = direct ? d_forces : ctx->facc.as<double>();
   a.fbuf = nl->fbuf.as<double>();
@@ -1490,8 +1567,55 @@ static int enqueue_compute(tb_context *ctx, const tb_nlist *nl, const double *d_
     }
     w.facc = a.forces;
     const bool want_stats = d_stats != nullptr;
-    rc = precision == TB_PREC_DOUBLE ? launch_warp_prec<double>(ctx, nl, a, w, scatter, want_stats)
-                                     : launch_warp_prec<float>(ctx, nl, a, w, scatter, want_stats);
+    if (ctx->sctl) {
+      // streamed: one launch per stage, behind the stage's last range of
+      // positions; finished ranges of forces / per-atom energies go back on
+      // the D2H stream while later stages run (tb_stream.cuh)
+      if (live || !direct) return fail(ctx, TB_ERR_CUDA, "internal error: streamed evaluation");
+      const StreamCtl &sc = *ctx->sctl;
+      const int K = nl->sp_K;
+      const int64_t R = nl->sp_R;
+      int total = 0;
+      rc = TB_OK;
+      for (int s = 0; s < K && !rc; ++s) {
+        CK(cudaStreamWaitEvent(ctx->stream, ctx->ev_h2d[s], 0));
+        const int c0 = nl->sp_cstart[s], c1 = nl->sp_cstart[s + 1];
+        const bool last = s == K - 1;
+        if (c1 > c0 || (last && nl->n_empty > 0) || (last && total == 0)) {
+          w.lanes = nl->sp_lanes.as<int4>() + 32 * (int64_t)c0;
+          w.nchunks = c1 - c0;
+          w.n_empty = last ? nl->n_empty : 0;
+          ctx->part_off = total;
+          rc = precision == TB_PREC_DOUBLE
+                   ? launch_warp_prec<double>(ctx, nl, a, w, scatter, want_stats)
+                   : launch_warp_prec<float>(ctx, nl, a, w, scatter, want_stats);
+          ctx->part_off = 0;
+          if (rc) break;
+          total += ctx->last_blocks;
+        }
+        CK(cudaEventRecord(ctx->ev_stage[s], ctx->stream));
+        bool waited = false;
+        for (int r = 0; r < K; ++r) {
+          if (nl->sp_fin[r] != s) continue;
+          int r1 = r;  // merge the run of ranges finishing with this stage
+          while (r1 + 1 < K && nl->sp_fin[r1 + 1] == s) ++r1;
+          const int64_t a0 = r * R, a1 = std::min<int64_t>(n, (r1 + 1) * R);
+          if (!waited) CK(cudaStreamWaitEvent(ctx->s_d2h, ctx->ev_stage[s], 0));
+          waited = true;
+          CK(cudaMemcpyAsync(sc.h_forces + 3 * a0, d_forces + 3 * a0,
+                             sizeof(double) * 3 * (a1 - a0), cudaMemcpyDeviceToHost, ctx->s_d2h));
+          if (sc.h_per_atom)
+            CK(cudaMemcpyAsync(sc.h_per_atom + a0, d_per_atom + a0, sizeof(double) * (a1 - a0),
+                               cudaMemcpyDeviceToHost, ctx->s_d2h));
+          r = r1;
+        }
+      }
+      ctx->last_blocks = total;
+      a.partials = ctx->partials.as<double>();  // the finalize reduces every stage's slots
+    } else {
+      rc = precision == TB_PREC_DOUBLE ? launch_warp_prec<double>(ctx, nl, a, w, scatter, want_stats)
+                                       : launch_warp_prec<float>(ctx, nl, a, w, scatter, want_stats);
+    }
     nparts = ctx->last_blocks;
     if (!rc && filtered && want_stats && !w.count_packed) {
       k_pack_stats<<<nblk(n, 256), 256, 0, ctx->stream>>>(n, d_pos, a.box, a.rc2, a.off, a.nbr,
@@ -1591,11 +1715,80 @@ extern "C" int tb_compute(tb_context *ctx, const tb_nlist *nl, const double *pos
   int rc = TB_OK;
   if (ctx->err_unchecked || !ctx->errf.p) rc = reset_errors(ctx);
   if (rc) return rc;
-  const double *d_pos = stage_in(ctx, positions, 3 * (size_t)n, ctx->pos, rc);
-  if (rc) return rc;
+  // Streamed path (tb_stream.cuh): pinned host positions in, pinned host
+  // forces / per-atom energies out, one species, atomic scatter, warp chunks
+  // without the live repack, at least 8 ranges of stream_range atoms.
+  bool streamed = false;
+  int sK = 0, sR = 0;
+  StreamCtl sctl{nullptr, nullptr, nullptr, nullptr};
+  {
+    const int64_t rmin = ctx->stream_range;
+    const bool long_rows = n > 0 && nl->entries >= 6 * n;
+    const bool live = ctx->live_pack == 1 ||
+                      (ctx->live_pack == 2 && long_rows && ctx->repack_margin > 0);
+    if (rmin > 0 && n >= 8 * rmin && scatter == TB_SCATTER_ATOMIC && ctx->S == 1 && nl->built &&
+        nl->nchunks > 0 && !ctx->force_tile && !live && r_cut <= nl->r_cut &&
+        (precision == TB_PREC_DOUBLE || precision == TB_PREC_MIXED) &&
+        !is_device_ptr(positions) && host_alias(positions) && !is_device_ptr(forces) &&
+        host_alias(forces) && (!per_atom || (!is_device_ptr(per_atom) && host_alias(per_atom)))) {
+      sR = (int)std::max<int64_t>(rmin, (n + STREAM_KMAX - 1) / STREAM_KMAX);
+      sK = (int)((n + sR - 1) / sR);
+      streamed = sK >= 2;
+    }
+  }
+  const double *d_pos = nullptr;
+  if (streamed) {
+    rc = stream_plan(ctx, const_cast<tb_nlist *>(nl), sK, sR);
+    if (rc) return rc;
+    if (!ctx->s_h2d) {
+      CK(cudaStreamCreateWithFlags(&ctx->s_h2d, cudaStreamNonBlocking));
+      CK(cudaStreamCreateWithFlags(&ctx->s_d2h, cudaStreamNonBlocking));
+      CK(cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming));
+    }
+    while ((int)ctx->ev_h2d.size() < sK) {
+      cudaEvent_t e1, e2;
+      CK(cudaEventCreateWithFlags(&e1, cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&e2, cudaEventDisableTiming));
+      ctx->ev_h2d.push_back(e1);
+      ctx->ev_stage.push_back(e2);
+    }
+    CK(ctx->pos.ensure(sizeof(double) * 3 * (size_t)n));
+    CK(ctx->forces.ensure(sizeof(double) * 3 * (size_t)n));
+    if (per_atom) CK(ctx->per_atom.ensure(sizeof(double) * (size_t)n));
+    int sms = 0;
+    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device));
+    CK(ctx->partials.ensure(sizeof(double) * 8 * (size_t)sK * sms * 16));
+    // the staging buffers may still be read by earlier work on the stream
+    CK(cudaEventRecord(ctx->ev_fork, ctx->stream));
+    CK(cudaStreamWaitEvent(ctx->s_h2d, ctx->ev_fork, 0));
+    CK(cudaStreamWaitEvent(ctx->s_d2h, ctx->ev_fork, 0));
+    for (int r = 0; r < sK; ++r) {
+      const int64_t a0 = (int64_t)r * sR, a1 = std::min<int64_t>(n, a0 + sR);
+      CK(cudaMemcpyAsync(ctx->pos.as<double>() + 3 * a0, positions + 3 * a0,
+                         sizeof(double) * 3 * (a1 - a0), cudaMemcpyHostToDevice, ctx->s_h2d));
+      CK(cudaEventRecord(ctx->ev_h2d[r], ctx->s_h2d));
+    }
+    d_pos = ctx->pos.as<double>();
+    sctl.h_pos = positions;
+    sctl.h_forces = forces;
+    sctl.h_per_atom = per_atom;
+    sctl.d_pos = ctx->pos.as<double>();
+  } else {
+    d_pos = stage_in(ctx, positions, 3 * (size_t)n, ctx->pos, rc);
+    if (rc) return rc;
+  }
+  // a failing call drains the side streams before it returns
+  auto drain = [&](int code) {
+    if (streamed) {
+      cudaStreamSynchronize(ctx->s_h2d);
+      cudaStreamSynchronize(ctx->stream);
+      cudaStreamSynchronize(ctx->s_d2h);
+    }
+    return code;
+  };
   const bool sp_host = !is_device_ptr(species);
   const int *d_sp = stage_in(ctx, species, (size_t)n, ctx->species, rc);
-  if (rc) return rc;
+  if (rc) return drain(rc);
   if (sp_host && ctx->S > 1) {
     // host species go through one staging buffer: a content change (checked
     // per list) invalidates the species-pair compute filter built for the old
@@ -1625,7 +1818,7 @@ extern "C" int tb_compute(tb_context *ctx, const tb_nlist *nl, const double *pos
   // written by the finalize kernel through their device alias (no copy-back);
   // pageable host buffers go through staging and a copy
   const bool f_dev = is_device_ptr(forces);
-  double *f_alias = f_dev ? nullptr : static_cast<double *>(host_alias(forces));
+  double *f_alias = f_dev || streamed ? nullptr : static_cast<double *>(host_alias(forces));
   double *d_f = f_dev ? forces : f_alias;
   if (!d_f) {
     CK(ctx->forces.ensure(sizeof(double) * 3 * std::max<int64_t>(n, 1)));
@@ -1641,8 +1834,8 @@ extern "C" int tb_compute(tb_context *ctx, const tb_nlist *nl, const double *pos
   // written by the finalize kernel
   char *h = reinterpret_cast<char *>(ctx->h_small);
   char *hd = static_cast<char *>(host_alias(h));
-  if (!hd) return fail(ctx, TB_ERR_CUDA, "pinned result block is not device-mapped");
-  const bool pa_async = per_atom && !e_dev && host_alias(per_atom);
+  if (!hd) return drain(fail(ctx, TB_ERR_CUDA, "pinned result block is not device-mapped"));
+  const bool pa_async = !streamed && per_atom && !e_dev && host_alias(per_atom);
   if (pa_async && !ctx->side) {
     CK(cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking));
     CK(cudaEventCreateWithFlags(&ctx->ev_kernel_done, cudaEventDisableTiming));
@@ -1652,13 +1845,20 @@ evaluate:
   ctx->fin_err_dst = reinterpret_cast<unsigned long long *>(hd);
   cudaEvent_t keep_ev = ctx->ev_kernel_done;
   if (!pa_async) ctx->ev_kernel_done = nullptr;
+  ctx->sctl = streamed ? &sctl : nullptr;
   rc = enqueue_compute(ctx, nl, d_pos, d_sp, r_cut, precision, scatter, d_f, d_e,
                        reinterpret_cast<double *>(hd + 64),
-                       reinterpret_cast<unsigned long long *>(hd + 128), f_dev);
+                       reinterpret_cast<unsigned long long *>(hd + 128), f_dev || streamed);
+  ctx->sctl = nullptr;
+  ctx->part_off = 0;
   ctx->fin_err_dst = nullptr;
   ctx->ev_kernel_done = keep_ev;
-  if (rc) return rc;
-  if (pa_async) {
+  if (rc) return drain(rc);
+  if (streamed) {
+    // every range was queued on the D2H stream behind its last stage
+    CK(spin_sync(ctx->stream));
+    CK(spin_sync(ctx->s_d2h));
+  } else if (pa_async) {
     // per-atom energies are final when the Tersoff kernel ends: copy them back
     // on the side stream while the finalize kernel runs
     CK(cudaStreamWaitEvent(ctx->side, ctx->ev_kernel_done, 0));
@@ -1666,7 +1866,7 @@ evaluate:
   } else if (per_atom && !e_dev) {
     CK(cudaMemcpyAsync(per_atom, d_e, sizeof(double) * n, cudaMemcpyDeviceToHost, ctx->stream));
   }
-  if (!f_dev && !f_alias)
+  if (!streamed && !f_dev && !f_alias)
     CK(cudaMemcpyAsync(forces, d_f, sizeof(double) * 3 * n, cudaMemcpyDeviceToHost, ctx->stream));
   CK(spin_sync(ctx->stream));
   if (pa_async) CK(spin_sync(ctx->side));
@@ -2238,6 +2438,7 @@ extern "C" int tb_md_run(tb_context *ctx, tb_nlist *nl, int64_t n, double *d_pos
       nl->entries = hp.entries;
       nl->max_row = hp.max_row;
       nl->nchunks = hp.nchunks;
+      nl->lanes_version++;
       nl->n_empty = hp.n_empty;
       nl->lanes_used = hp.lanes_used;
       if (hp.rebuilds > 0 && scatter != TB_SCATTER_GATHER) nl->rev_valid = false;
@@ -2295,6 +2496,7 @@ extern "C" int tb_nlist_rebuild_device(tb_context *ctx, tb_nlist *nl, const doub
   nl->entries = hp.entries;
   nl->max_row = hp.max_row;
   nl->nchunks = hp.nchunks;
+  nl->lanes_version++;
   nl->n_empty = hp.n_empty;
   nl->lanes_used = hp.lanes_used;
   nl->lvalid = false;
