@@ -296,8 +296,11 @@ def ncu_profile(config, precision):
 
 
 def kernel_time(ctx, step, flush, k):
-    """Average Tersoff-kernel duration: CUDA events bracket every launch on the
-    launch stream (tb_profile)."""
+    """Tersoff kernel time per evaluation: CUDA events bracket every Tersoff
+    launch on the launch stream (tb_profile); an evaluation is one launch, or
+    two when the list is split between the atom-per-lane kernel (rows of <= 4
+    entries) and the warp-chunk kernel (the longer rows).  Returns (ms per
+    evaluation, launches per evaluation)."""
     import ctypes
     import torch
     lib = ctx.lib
@@ -310,7 +313,7 @@ def kernel_time(ctx, step, flush, k):
     lib.tb_profile(ctx.handle, 0)
     tot, cnt = ctypes.c_double(), ctypes.c_int64()
     ctx.check(lib.tb_profile_read(ctx.handle, ctypes.byref(tot), ctypes.byref(cnt)))
-    return tot.value / max(cnt.value, 1)
+    return tot.value / max(k, 1), cnt.value / max(k, 1)
 
 
 class Evaluator:
@@ -383,17 +386,32 @@ class Evaluator:
         pcode = self.native.PRECISION[precision]
         st = self.counts(pcode)
         flops = flops_for(st, precision)
-        kms = kernel_time(self.ctx, lambda: self.step(pcode), flush, k)
-        kms_api = kernel_time(self.ctx, lambda: self.step(pcode, True), flush, k)
+        kms, nlaunch = kernel_time(self.ctx, lambda: self.step(pcode), flush, k)
+        kms_api, _ = kernel_time(self.ctx, lambda: self.step(pcode, True), flush, k)
         ach = flops / (kms * 1e-3) / 1e12
         prof = ncu_profile(config, precision)
         pipe = "fp64_pipe_pct" if precision == "double" else "fma_pipe_pct"
+        tname = "double" if pcode == 0 else "float"
+        kname = f"k_tersoff_warp<{tname},S={self.table.nspecies},atomic>"
+        if nlaunch > 1.5:
+            kname = (f"k_tersoff_row<{tname},4,atomic> (rows of <= 4 entries, one lane per atom) + "
+                     f"{kname} (longer rows); kernel_ms is their sum")
+        peak_tf = peak["tflops"] if peak else None
+        exe = prof.get("executed_flops") if prof else None
         return {
             "bound": "fp64" if precision == "double" else "fp32",
             "achieved": ach, "peak": peak["tflops"] if peak else None, "unit": "TFLOP/s",
             "frac": ach / peak["tflops"] if peak else None,
             "traffic": prof.get("dram_bytes") if prof else None,
-            "kernel": f"k_tersoff_warp<{'double' if pcode == 0 else 'float'},S={self.table.nspecies},atomic>",
+            "frac_note": "algorithmic fraction by the SURVEY 8(d) convention; it can exceed 1: "
+                         "the kernels execute fewer flops than the reference expression tree "
+                         "(2 log + 2 exp + 1 reciprocal instead of 4 pow per pair, g(cos) once "
+                         "per unordered pair in the row kernel) -- frac_executed and ncu.pipe_pct "
+                         "are the hardware view",
+            "executed_flops_per_launch": exe,
+            "frac_executed": (exe / (kms * 1e-3) / 1e12 / peak_tf) if exe and peak_tf else None,
+            "kernel": kname,
+            "kernel_launches_per_step": nlaunch,
             "kernel_ms": kms,
             "kernel_ms_api": kms_api,
             "kernel_ms_note": "kernel_ms: counter-free instantiation (the timed step); "
@@ -719,14 +737,17 @@ def gpu_arm_decomposed(args):
     value = n_total * k / t_max
     # Tersoff kernel of this rank (its owned rows of [owned | ghosts])
     prec = eng.native.PRECISION[args.precision]
-    kern_ms = kernel_time(eng.ctx, lambda: eng.compute(md.result), None, min(k, 20))
+    kern_ms, kern_launches = kernel_time(eng.ctx, lambda: eng.compute(md.result), None,
+                                         min(k, 20))
     peak = measure_peak(eng.ctx.lib, eng.ctx, prec) if rank == 0 else None
     flops = flops_for(st_h, args.precision)
     ach = flops / (kern_ms * 1e-3) / 1e12
     roof = {"bound": "fp64" if prec == 0 else "fp32", "achieved": ach,
             "peak": peak["tflops"] if peak else None, "unit": "TFLOP/s",
             "frac": ach / peak["tflops"] if peak else None, "traffic": None,
-            "kernel": "k_tersoff_warp (rank 0: its owned rows of [owned | ghosts])",
+            "kernel": ("k_tersoff_row + k_tersoff_warp" if kern_launches > 1.5 else
+                       "k_tersoff_warp") + " (rank 0: its owned rows of [owned | ghosts])",
+            "kernel_launches_per_step": kern_launches,
             "kernel_ms": kern_ms, "flops_per_launch": flops,
             "peak_source": peak["source"] if peak else None}
     counts = eng.counts()

@@ -28,6 +28,7 @@ OPT_LIVE_PACK = 3  # 0 off / 1 on / 2 auto: rows cut to r < r_cut and re-chunked
 OPT_MD_LOOSE_SKIN = 4  # tb_md_run list skin extra in 1/100 A (default 30; 0 = exact list)
 OPT_REPACK_MARGIN = 5  # live repack margin in 1/1000 A (default 1; 0 = repack every evaluation)
 OPT_STREAM_RANGE = 6  # tb_compute with pinned host buffers: atoms per streamed range (default 131072; 0 = off)
+OPT_ROW_KERNEL = 7  # atom-per-lane kernel for rows of <= 4 entries (one species, lam3 = 0); 0 = warp kernel only
 
 # symbol -> (restype, argtypes); the exported surface of the C ABI
 _P = ctypes.c_void_p

@@ -25,6 +25,7 @@
 #include "tb_dnl.cuh"
 #include "tb_dd.cuh"
 #include "tb_stream.cuh"
+#include "tb_row.cuh"
 
 #ifndef TB_VERSION_TAG
 #define TB_VERSION_TAG "dev"
@@ -110,6 +111,10 @@ struct tb_context {
   cudaEvent_t ev_fork = nullptr;
   struct StreamCtl *sctl = nullptr;  // set by tb_compute around enqueue_compute
   int part_off = 0;     // first block-partial slot of the next warp launch
+  bool row_kernel = getenv("TB_NO_ROW_KERNEL") == nullptr;  // TB_OPT_ROW_KERNEL: atom-per-lane kernel for rows <= 4
+  // ... for lists with at least this many such rows (one lane per atom needs
+  // ~150k atoms to fill the GPU: config 2, 64k atoms, 20.7 -> 36.7 us with it)
+  int64_t row_min = getenv("TB_ROW_MIN") ? atoll(getenv("TB_ROW_MIN")) : 262144;
   int last_blocks = 0;  // grid of the last Tersoff launch (partials to reduce)  // tb_set_option(TB_OPT_TILE_KERNEL): general tile kernel only
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_used, ev_free;
 };
@@ -155,6 +160,9 @@ struct tb_nlist {
   double lmargin = -1.0;
   bool fnbr_ok = false;  // fnbr matches centry (written by every filter pass since)
   int64_t lcap = 0;  // chunk capacity of llanes
+  // rows of 1..ROW_LM entries (tb_row.cuh): sorted_atoms[r4_first, r4_first + r4_count),
+  // their warp chunks are lanes[0, r4_chunks)
+  int r4_first = 0, r4_count = 0, r4_chunks = 0;
   // streamed tb_compute: chunks sorted by stage (tb_stream.cuh)
   int64_t lanes_version = 0;  // bumped whenever `lanes` is rewritten
   int64_t sp_version = -1;
@@ -439,6 +447,12 @@ extern "C" int tb_set_option(tb_context *ctx, int option, int value) {
     ctx->list_margin = value / 100.0;
     return TB_OK;
   }
+  if (option == TB_OPT_ROW_KERNEL) {
+    if (value < 0) return fail(ctx, TB_ERR_ARG, "row-kernel threshold %d out of range", value);
+    ctx->row_kernel = value != 0;
+    if (value > 0) ctx->row_min = value == 1 ? 262144 : value;
+    return TB_OK;
+  }
   if (option == TB_OPT_STREAM_RANGE) {
     if (value < 0) return fail(ctx, TB_ERR_ARG, "stream range %d out of range", value);
     ctx->stream_range = value;
@@ -621,6 +635,19 @@ static int build_rev(tb_context *ctx, tb_nlist *nl) {
   return TB_OK;
 }
 
+constexpr int ROW_LM = 4;  // rows the atom-per-lane kernel takes (tb_row.cuh)
+
+// where the rows of 1..ROW_LM entries and their chunks sit (hist = row-length histogram)
+static void set_row_info(tb_nlist *nl, const int *hist) {
+  nl->r4_first = hist[0];
+  nl->r4_count = 0;
+  nl->r4_chunks = 0;
+  for (int L = 1; L <= ROW_LM; ++L) {
+    nl->r4_count += hist[L];
+    nl->r4_chunks += (hist[L] + 32 / L - 1) / (32 / L);
+  }
+}
+
 // Warp chunks: rows sorted by length (stable radix sort -> deterministic),
 // floor(32/L) rows of length L per warp.  row_len[i] = lanes of atom i; lane
 // k of row i maps to entry coff[i] + k of centry (or offsets[i] + k when
@@ -642,6 +669,7 @@ static int build_chunks(tb_context *ctx, tb_nlist *nl, const int *row_len, const
     chunks += (hist[L] + 32 / L - 1) / (32 / L);
   }
   plan.chunk_base[33] = chunks;
+  set_row_info(nl, hist);
   nl->n_empty = hist[0];
   nl->lanes_used = 0;
   for (int L = 1; L <= 32; ++L) nl->lanes_used += (int64_t)L * hist[L];
@@ -983,6 +1011,7 @@ static int build_owned(tb_context *ctx, tb_nlist *nl, int64_t n, int64_t n_owned
     if (rc2) return rc2;
   } else {
     nl->nchunks = 0;
+    nl->r4_count = 0;
     nl->lanes_version++;
     nl->n_empty = 0;
   }
@@ -1083,6 +1112,7 @@ extern "C" int tb_nlist_import(tb_context *ctx, tb_nlist *nl, int64_t n, const i
     if (rc) return rc;
   } else {
     nl->nchunks = 0;
+    nl->r4_count = 0;
     nl->lanes_version++;
     nl->n_empty = 0;
   }
@@ -1259,6 +1289,57 @@ static int launch_warp_t(tb_context *ctx, const tb_nlist *nl, KArgs &a, WArgs &w
     ctx->ev_used.push_back(ev);
   }
   return TB_OK;
+}
+
+// atom-per-lane kernel for the rows of 1..ROW_LM entries (tb_row.cuh)
+template <class T, int MODE, bool ST>
+static int launch_row_t(tb_context *ctx, KArgs &a, const RArgs &r, int cap) {
+  auto kern = k_tersoff_row<T, ROW_LM, MODE, ST>;
+  static int per_sm = 0;
+  if (!per_sm) {
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, RowCfg<T>::nt, 0));
+    per_sm = std::max(per_sm, 1);
+  }
+  int sms = 0;
+  CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device));
+  const int nb = std::max(1, std::min(nblk(cap, RowCfg<T>::nt), sms * per_sm));
+  if (ctx->part_off == 0) CK(ctx->partials.ensure(sizeof(double) * 8 * nb));
+  a.partials = ctx->partials.as<double>() + 8 * (int64_t)ctx->part_off;
+  Tables<T, 1> tab = make_tables<T, 1>(ctx);
+  std::pair<cudaEvent_t, cudaEvent_t> ev{nullptr, nullptr};
+  if (ctx->profile) {
+    if (ctx->ev_free.empty()) {
+      CK(cudaEventCreate(&ev.first));
+      CK(cudaEventCreate(&ev.second));
+    } else {
+      ev = ctx->ev_free.back();
+      ctx->ev_free.pop_back();
+    }
+    CK(cudaEventRecord(ev.first, ctx->stream));
+  }
+  constexpr int bs = (int)(offsetof(DevPlan, bucket_start) / sizeof(int));
+  kern<<<nb, RowCfg<T>::nt, 0, ctx->stream>>>(a, r, tab, bs + 1, bs + ROW_LM + 1);
+  ctx->last_blocks = nb;
+  CK(cudaGetLastError());
+  if (ctx->profile) {
+    CK(cudaEventRecord(ev.second, ctx->stream));
+    ctx->ev_used.push_back(ev);
+  }
+  return TB_OK;
+}
+
+static int launch_row(tb_context *ctx, KArgs &a, const RArgs &r, int cap, int precision, int mode,
+                      bool stats) {
+  if (precision == TB_PREC_DOUBLE) {
+    if (mode) return stats ? launch_row_t<double, 1, true>(ctx, a, r, cap)
+                           : launch_row_t<double, 1, false>(ctx, a, r, cap);
+    return stats ? launch_row_t<double, 0, true>(ctx, a, r, cap)
+                 : launch_row_t<double, 0, false>(ctx, a, r, cap);
+  }
+  if (mode) return stats ? launch_row_t<float, 1, true>(ctx, a, r, cap)
+                         : launch_row_t<float, 1, false>(ctx, a, r, cap);
+  return stats ? launch_row_t<float, 0, true>(ctx, a, r, cap)
+               : launch_row_t<float, 0, false>(ctx, a, r, cap);
 }
 
 template <class T, int S, int MODE>
@@ -1530,6 +1611,7 @@ static int enqueue_compute(tb_context *ctx, const tb_nlist *nl, const double *d_
     w.nchunks = nl->nchunks;
     w.n_empty = nl->n_empty;
     w.dinfo = nullptr;
+    w.dskip = 0;
     w.count_packed = filtered ? 0 : 1;
     // live repack: atomic scatter only (the gather finalize reads every entry's
     // slot, which must then be rewritten each evaluation); auto = species-
@@ -1612,6 +1694,41 @@ static int enqueue_compute(tb_context *ctx, const tb_nlist *nl, const double *d_
       }
       ctx->last_blocks = total;
       a.partials = ctx->partials.as<double>();  // the finalize reduces every stage's slots
+    } else if (ctx->row_kernel && ctx->S == 1 && !ctx->lam3 && !live &&
+               nl->r4_count >= ctx->row_min && make_tables<double, 1>(ctx).fc_same) {
+      // rows of <= ROW_LM entries: one lane per atom (tb_row.cuh); the warp
+      // chunks of the longer rows follow, with their own partial slots
+      int sms = 0;
+      CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device));
+      CK(ctx->partials.ensure(sizeof(double) * 8 * (size_t)2 * sms * 16));
+      RArgs r;
+      r.atoms = nl->sorted_atoms.as<int>();
+      r.first = nl->r4_first;
+      r.count = nl->r4_count;
+      r.dplan = ctx->dplan;  // tb_md_run capture: the bounds live in the device plan
+      r.n_empty = nl->n_empty;
+      r.count_packed = w.count_packed;
+      rc = launch_row(ctx, a, r, ctx->dplan ? n : nl->r4_count, precision, scatter, want_stats);
+      int total = ctx->last_blocks;
+      if (!rc && (ctx->dplan || nl->nchunks > nl->r4_chunks)) {
+        if (ctx->dplan) {
+          // the longer rows' chunks start at chunk_base[ROW_LM + 1] of the plan
+          w.dskip = (int)(offsetof(DevPlan, chunk_base) / sizeof(int)) + ROW_LM + 1;
+          w.nchunks = (int)std::max<int64_t>(nl->ccap / 8, 1024);  // grid sizing only
+        } else {
+          w.lanes += 32 * (int64_t)nl->r4_chunks;
+          w.nchunks -= nl->r4_chunks;
+        }
+        w.n_empty = 0;
+        ctx->part_off = total;
+        rc = precision == TB_PREC_DOUBLE
+                 ? launch_warp_prec<double>(ctx, nl, a, w, scatter, want_stats)
+                 : launch_warp_prec<float>(ctx, nl, a, w, scatter, want_stats);
+        ctx->part_off = 0;
+        total += ctx->last_blocks;
+      }
+      ctx->last_blocks = total;
+      a.partials = ctx->partials.as<double>();
     } else {
       rc = precision == TB_PREC_DOUBLE ? launch_warp_prec<double>(ctx, nl, a, w, scatter, want_stats)
                                        : launch_warp_prec<float>(ctx, nl, a, w, scatter, want_stats);
@@ -2439,6 +2556,7 @@ extern "C" int tb_md_run(tb_context *ctx, tb_nlist *nl, int64_t n, double *d_pos
       nl->max_row = hp.max_row;
       nl->nchunks = hp.nchunks;
       nl->lanes_version++;
+      set_row_info(nl, hp.hist);
       nl->n_empty = hp.n_empty;
       nl->lanes_used = hp.lanes_used;
       if (hp.rebuilds > 0 && scatter != TB_SCATTER_GATHER) nl->rev_valid = false;
@@ -2497,6 +2615,7 @@ extern "C" int tb_nlist_rebuild_device(tb_context *ctx, tb_nlist *nl, const doub
   nl->max_row = hp.max_row;
   nl->nchunks = hp.nchunks;
   nl->lanes_version++;
+  set_row_info(nl, hp.hist);
   nl->n_empty = hp.n_empty;
   nl->lanes_used = hp.lanes_used;
   nl->lvalid = false;

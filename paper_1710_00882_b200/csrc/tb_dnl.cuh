@@ -311,10 +311,10 @@ __global__ void __launch_bounds__(256) k_bucket_fill(int n, const int *__restric
   __syncthreads();
   if (L < 0 || L > 32 || plan->overflow) return;  // (the chunk bound makes overflow impossible)
   const int s = s_base[L] + slot;
-  if (L == 0) {
-    empty_atoms[s] = i;  // the kernel's empty-row list (per-atom energy 0)
-    return;
-  }
+  // atoms by row length: [empty rows | L = 1 | L = 2 | ...] -- the kernels'
+  // empty-row list (per-atom energy 0) and the row kernel's atom list
+  empty_atoms[plan->bucket_start[L] + s] = i;
+  if (L == 0) return;
   const int rpc = 32 / L, r = s % rpc;
   int4 *dst = lanes + 32 * (int64_t)(plan->chunk_base[L] + s / rpc);
   const int b = start[i];

@@ -148,45 +148,58 @@ __device__ __forceinline__ void lam3_term(T dr, const TripP<T> &p, T &ex, T &dar
 // Pair part of one ordered (i,j) bond at fixed zeta (potential.py:280-290):
 // returns V, dV/dr and delta_zeta = f_C f_A db/dzeta.
 // pair_part_fc: the same with f_C(r), dF_C/dr already known (r < R + D)
+// Main path of the pair part, zeta >= ZETA_TINY, branch-free (the row kernel
+// interleaves several of these; pair_part_fc adds the isolated-bond branch).
+//   u = t^eta, b = (1+u)^(-1/2eta), and with t^(eta-1) = u/t, t = beta zeta:
+//   db/dzeta = -beta/2 t^(eta-1) (1+u)^(-1/2eta-1) = -(1/2) u b / (zeta (1+u))
+// one reciprocal serves db and the log1p correction (1/w = zeta / (zeta w)).
+// Range (any table): beyond x = eta log t = XBIG, 1/u is below the rounding
+// unit, so log1p(u) = XBIG + (x - XBIG) to rounding and u/(1+u) = 1: u is
+// formed from x clamped to XBIG (no overflow however large eta) and the excess
+// added to log1p; below -708 u is at most a subnormal (clamped: b = 1,
+// db ~ 1e-308/zeta).  Every exp / log argument stays on the fast domain:
+// -l1p/2eta >= -log(t)/2 >= -355.
 template <class T>
-__device__ __forceinline__ void pair_part_fc(T r, T zeta, const PairP<T> &p, T fc, T dfc, T &v,
-                                             T &dvdr, T &dzeta) {
+__device__ __forceinline__ void pair_part_main(T r, T zeta, const PairP<T> &p, T fc, T dfc, T &v,
+                                               T &dvdr, T &dzeta) {
   T fr = p.A * t_exp(-p.lam1 * r);
   T fa = -p.B * t_exp(-p.lam2 * r);
   T t = p.beta * zeta;
-  T b, db;
-  if (zeta < T(ZETA_TINY)) {
-    // isolated bond (potential.py:202-215): db = 0; b from the library
-    // functions, which also cover subnormal beta*zeta (exact b = 1 at zeta = 0)
-    T u = zeta > T(0) ? pow(t, p.eta) : T(0);
-    b = pow(T(1) + u, p.neg_half_inv_eta);
-    db = T(0);
-  } else {
-    // u = t^eta, b = (1+u)^(-1/2eta), and with t^(eta-1) = u/t, t = beta zeta:
-    //   db/dzeta = -beta/2 t^(eta-1) (1+u)^(-1/2eta-1) = -(1/2) u b / (zeta (1+u))
-    // one reciprocal serves db and the log1p correction (1/w = zeta / (zeta w)).
-    // Range (any table, branch-free): beyond x = eta log t = XBIG, 1/u is below
-    // the rounding unit, so log1p(u) = XBIG + (x - XBIG) to rounding and
-    // u/(1+u) = 1: u is formed from x clamped to XBIG (no overflow however
-    // large eta) and the excess added to log1p; below -708 u is at most a
-    // subnormal (clamped: b = 1, db ~ 1e-308/zeta).  Every exp / log argument
-    // stays on the fast domain: -l1p/2eta >= -log(t)/2 >= -355.
-    constexpr T XBIG = sizeof(T) == 8 ? T(36) : T(17);
-    const T lt = t_log(t);
-    const T x = p.eta * lt;
-    const T xc = fmin(x, XBIG);
-    const T u = t_exp(fmax(xc, T(-708)));
-    const T w = T(1) + u;
-    const T rzw = t_rcp(zeta * w);
-    // log1p(u) = log(w) + (u - (w - 1)) / w, w = fl(1 + u)
-    const T l1p = t_log(w) + (u - (w - T(1))) * (zeta * rzw) + (x - xc);
-    b = t_exp(p.neg_half_inv_eta * l1p);
-    db = T(-0.5) * (u * b) * rzw;
-  }
+  constexpr T XBIG = sizeof(T) == 8 ? T(36) : T(17);
+  const T lt = t_log(t);
+  const T x = p.eta * lt;
+  const T xc = fmin(x, XBIG);
+  const T u = t_exp(fmax(xc, T(-708)));
+  const T w = T(1) + u;
+  const T rzw = t_rcp(zeta * w);
+  // log1p(u) = log(w) + (u - (w - 1)) / w, w = fl(1 + u)
+  const T l1p = t_log(w) + (u - (w - T(1))) * (zeta * rzw) + (x - xc);
+  const T b = t_exp(p.neg_half_inv_eta * l1p);
+  const T db = T(-0.5) * (u * b) * rzw;
   T inner = fr + b * fa;
   v = fc * inner;
   dvdr = dfc * inner + fc * (-p.lam1 * fr + b * (-p.lam2 * fa));
   dzeta = fc * fa * db;
+}
+
+template <class T>
+__device__ __forceinline__ void pair_part_fc(T r, T zeta, const PairP<T> &p, T fc, T dfc, T &v,
+                                             T &dvdr, T &dzeta) {
+  if (zeta < T(ZETA_TINY)) {
+    // isolated bond (potential.py:202-215): db = 0; b from the library
+    // functions, which also cover subnormal beta*zeta (exact b = 1 at zeta = 0)
+    T fr = p.A * t_exp(-p.lam1 * r);
+    T fa = -p.B * t_exp(-p.lam2 * r);
+    T t = p.beta * zeta;
+    T u = zeta > T(0) ? pow(t, p.eta) : T(0);
+    T b = pow(T(1) + u, p.neg_half_inv_eta);
+    T inner = fr + b * fa;
+    v = fc * inner;
+    dvdr = dfc * inner + fc * (-p.lam1 * fr + b * (-p.lam2 * fa));
+    dzeta = fc * fa * T(0);
+  } else {
+    pair_part_main(r, zeta, p, fc, dfc, v, dvdr, dzeta);
+  }
 }
 
 template <class T>

@@ -104,6 +104,8 @@ struct WArgs {
   const int *__restrict__ empty_atoms; // atoms with empty rows (per_atom = 0)
   int nchunks, n_empty;
   const int *__restrict__ dinfo;       // non-null: {nchunks, n_empty} in device memory (tb_md_run)
+  int dskip;                           // > 0 (with dinfo): dinfo[dskip] = first chunk to run, the
+                                       // shorter rows and the empty rows went to the row kernel
   int count_packed;                    // rows are the full skin rows: count zeta_visits here
   double *__restrict__ facc;           // ATOMIC: zeroed force accumulator (n,3)
 };
@@ -730,9 +732,14 @@ __global__ void __launch_bounds__(WarpCfg<T>::nt, WarpCfg<T>::minb)
   }
   const Tables<T, S> &tab = (S > 1) ? s_tab : gtab;
   int nchunks = w.nchunks, n_empty = w.n_empty;
+  int cfirst = 0;
   if (w.dinfo) {
     nchunks = __ldg(w.dinfo);
     n_empty = __ldg(w.dinfo + 1);
+    if (w.dskip) {
+      cfirst = __ldg(w.dinfo + w.dskip);
+      n_empty = 0;
+    }
   }
   for (int k = blockIdx.x * NT + threadIdx.x; k < n_empty; k += gridDim.x * NT) {
     const int m = w.empty_atoms[k];
@@ -760,7 +767,7 @@ __global__ void __launch_bounds__(WarpCfg<T>::nt, WarpCfg<T>::minb)
   // from a global atomic counter was measured slower: no better balance at
   // the pipeline's look-ahead, and c5 fp64 atomic mode went 2.96 -> 5.76 ms.)
   const int stride = gridDim.x * NW;
-  int c = wid * gridDim.x + blockIdx.x;
+  int c = cfirst + wid * gridDim.x + blockIdx.x;
   const int4 idle = make_int4(-1, 0, 0, 1);
   int4 cur = c < nchunks ? __ldg(w.lanes + 32 * (int64_t)c + lane) : idle;
   int4 nxt = c + stride < nchunks ? __ldg(w.lanes + 32 * (int64_t)(c + stride) + lane) : idle;

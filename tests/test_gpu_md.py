@@ -215,3 +215,29 @@ def test_loose_list_matches_exact_list(precision):
     tol = 1e-9 if precision == "double" else 1e-6
     assert np.max(np.abs(loose["total"] - exact["total"])) <= tol * scale
     assert np.abs(loose["positions"] - exact["positions"]).max() <= (1e-7 if precision == "double" else 1e-4)
+
+
+@pytest.mark.parametrize("precision", ["double", "single"])
+@pytest.mark.parametrize("loop", ["graph", "step"])
+def test_row_kernel_md_matches_warp_kernel(loop, precision):
+    """The atom-per-lane kernel (rows of <= 4 entries) inside the NVE loops --
+    in the graph its bounds come from the device plan of the in-graph rebuild --
+    against the same run on the warp-chunk kernel."""
+    from paper_1710_00882_b200 import _native
+    ctx = _native.default_context(0)
+    st, tname = structures.config(2, small=True)
+    t = builtin_params(tname)
+    cfg = RunConfig(dt=1.0, steps=200, skin=0.3, rebuild_every=10)
+    ctx.set_option(_native.OPT_ROW_KERNEL, 0)
+    try:
+        a = run_nve_device(st.copy(), t, cfg, precision=precision, loop=loop)
+        ctx.set_option(_native.OPT_ROW_KERNEL, 2)
+        b = run_nve_device(st.copy(), t, cfg, precision=precision, loop=loop)
+    finally:
+        ctx.set_option(_native.OPT_ROW_KERNEL, 1)
+    assert a["loop"] == loop and b["loop"] == loop
+    assert a["rebuilds"] == b["rebuilds"] and a["rebuilds"] >= 20
+    scale = abs(a["total"][0])
+    tol = 1e-9 if precision == "double" else 2e-5
+    assert np.max(np.abs(a["total"] - b["total"])) <= tol * scale
+    assert np.abs(a["positions"] - b["positions"]).max() <= (1e-7 if precision == "double" else 1e-3)

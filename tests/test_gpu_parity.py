@@ -20,17 +20,22 @@ FP64_TOL = 1e-10
 MIXED_TOL = 1e-5
 MIXED_E_TOL = 1e-5
 SCATTERS = ["atomic", "gather"]
-PATHS = ["warp", "tile"]
+PATHS = ["warp", "tile", "row"]
 
 
 @pytest.fixture(params=PATHS)
 def kernel_path(request):
-    """Run the test on the warp-chunk kernel and on the general tile kernel."""
+    """Run the test on the warp-chunk kernel, on the general tile kernel and on
+    the atom-per-lane row kernel (rows of <= 4 entries of one-species tables;
+    the remaining rows -- and every row of a multi-species table -- stay on the
+    warp-chunk kernel)."""
     from paper_1710_00882_b200 import _native
     ctx = _native.default_context(0)
     ctx.set_option(_native.OPT_TILE_KERNEL, request.param == "tile")
+    ctx.set_option(_native.OPT_ROW_KERNEL, 2 if request.param == "row" else 0)
     yield request.param
     ctx.set_option(_native.OPT_TILE_KERNEL, 0)
+    ctx.set_option(_native.OPT_ROW_KERNEL, 1)
 
 
 def rel_f(a, b):

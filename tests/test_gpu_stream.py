@@ -26,8 +26,11 @@ def stream_range():
 
     def set_range(r):
         ctx.set_option(_native.OPT_STREAM_RANGE, r)
+    # the streamed stages run the warp-chunk kernel: compare like with like
+    ctx.set_option(_native.OPT_ROW_KERNEL, 0)
     yield set_range
     ctx.set_option(_native.OPT_STREAM_RANGE, 131072)
+    ctx.set_option(_native.OPT_ROW_KERNEL, 1)
 
 
 class HostState:

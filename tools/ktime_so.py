@@ -51,8 +51,9 @@ for path in sys.argv[1:]:
             lib.tb_profile(ctx, 0)
             tot, cnt = ctypes.c_double(), ctypes.c_int64()
             lib.tb_profile_read(ctx, ctypes.byref(tot), ctypes.byref(cnt))
-            res[f"c{c}_p{prec}_us"] = round(1e3 * tot.value / cnt.value, 2)
-            res[f"c{c}_E"] = float(r[0])
+            res[f"c{c}_p{prec}_us"] = round(1e3 * tot.value / reps, 2)  # per evaluation (all Tersoff launches)
+            res[f"c{c}_p{prec}_launches"] = cnt.value / reps
+            res[f"c{c}_p{prec}_E"] = float(r[0])
         del pos, sp, f, flush
     out[os.path.basename(path)] = res
     print(json.dumps({os.path.basename(path): res}), flush=True)
