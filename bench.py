@@ -531,7 +531,8 @@ def e2e_arm(args, B, state, table, nl, dev):
             "path": "paper_1710_00882_b200.compute(state, nl, params, variant, out=pinned), "
                     "pinned host positions in (species resident on the device: constant over a "
                     "run), pinned host forces/per-atom energy out, energy/virial/stats to host, "
-                    "wall clock per call (synchronous)"}
+                    "wall clock per call (synchronous); tb_compute streams the call in atom "
+                    "ranges: H2D copy, kernel stages and D2H copy overlap (TB_OPT_STREAM_RANGE)"}
 
 
 # ---------------------------------------------------------------------------

@@ -38,8 +38,13 @@ namespace tb {
 #ifndef TB_ROW_VIR_RE
 #define TB_ROW_VIR_RE 1  // virial from r_p e_p (x) f_p: the displacement registers die after the unit vectors
 #endif
+#ifndef TB_ROW_SACC
+#define TB_ROW_SACC 0  // fp64: energy / virial accumulators in per-thread shared slots instead of
+                       // registers (spills 128 -> 96 B; measured c5 2.13 -> 2.20 ms: off)
+#endif
 #ifndef TB_ROW_RECOS
 #define TB_ROW_RECOS 0   // recompute cos in the force phase instead of keeping it over the pair parts
+                         // (measured neutral: c5 2.130 vs 2.133 ms)
 #endif
 #ifndef TB_ROW_MAXREG
 #define TB_ROW_MAXREG 0  // > 0: __maxnreg__ instead of the min-blocks bound (fp64)
@@ -96,7 +101,13 @@ __launch_bounds__(RowCfg<T>::nt, RowCfg<T>::minb)
       atomicMin(&a.err->nonfinite_atom, m);
   }
 
+  constexpr bool SACC = TB_ROW_SACC && sizeof(T) == 8;
+  __shared__ double s_acc[SACC ? 7 : 1][SACC ? NTH : 1];
   double acc[7] = {0, 0, 0, 0, 0, 0, 0};  // E, W xx yy zz xy xz yz
+  if (SACC) {
+#pragma unroll
+    for (int q = 0; q < 7; ++q) s_acc[q][threadIdx.x] = 0.0;
+  }
   unsigned long long c_vis = 0, c_pk = 0, c_lp = 0, c_lt = 0, c_tp = 0, c_tt = 0;
   const PairP<T> &pp = tab.pair[0];
   const TripP<T> &tp = tab.trip[0];
@@ -105,7 +116,9 @@ __launch_bounds__(RowCfg<T>::nt, RowCfg<T>::minb)
   // indices of the next atom are fetched while this one computes.  (A second
   // stage with prefetch.global.L1/L2 of the next atom's positions was measured
   // slower: the extra index registers spill, c5 fp64 2.19 -> 2.41 ms without
-  // and 2.57 ms with the prefetches.)
+  // and 2.57 ms with the prefetches.  Prefetching only each lane's own
+  // position a few iterations ahead, without the second index stage: 2.13 ->
+  // 2.22 ms.)
   int i = -1, o = 0, L = 0, jn[LM];
   if (gid < count) {
     i = __ldg(ra.atoms + first + gid);
@@ -302,6 +315,10 @@ __launch_bounds__(RowCfg<T>::nt, RowCfg<T>::minb)
         beta[u] = dg[u] * (dz[p] * fc[q] + dz[q] * fc[p]);
       }
     double fix = 0.0, fiy = 0.0, fiz = 0.0;
+    if (SACC) {
+#pragma unroll
+      for (int q = 1; q < 7; ++q) acc[q] = 0.0;
+    }
 #pragma unroll
     for (int p = 0; p < LM; ++p) {
       T Sal = T(0), Sc = T(0), Sbx = T(0), Sby = T(0), Sbz = T(0);
@@ -354,7 +371,13 @@ __launch_bounds__(RowCfg<T>::nt, RowCfg<T>::minb)
       atomicAdd(fi + 1, fiy);
       atomicAdd(fi + 2, fiz);
     }
-    acc[0] += e_i;
+    if (SACC) {
+      s_acc[0][threadIdx.x] += e_i;
+#pragma unroll
+      for (int q = 1; q < 7; ++q) s_acc[q][threadIdx.x] += acc[q];
+    } else {
+      acc[0] += e_i;
+    }
     if (a.per_atom) a.per_atom[ci] = e_i + 0.0;
   }
 
@@ -369,7 +392,7 @@ __launch_bounds__(RowCfg<T>::nt, RowCfg<T>::minb)
   }
 #pragma unroll
   for (int q = 0; q < 7; ++q) {
-    double v = warp_sum(acc[q]);
+    double v = warp_sum(SACC ? s_acc[q][threadIdx.x] : acc[q]);
     if (lane == 0) s_red[wid][q] = v;
   }
   __syncthreads();

@@ -63,11 +63,12 @@ for cfg in cfgs:
         torch.cuda.synchronize(); ctx.lib.tb_profile(ctx.handle, 0)
         tot = ctypes.c_double(); l = ctypes.c_int64()
         ctx.lib.tb_profile_read(ctx.handle, ctypes.byref(tot), ctypes.byref(l))
-        kms = tot.value / l.value
+        kms = tot.value / K  # per evaluation: the row kernel + the warp kernel when the list is split
         fl = bench.algorithmic_flops(cnt) if prec == 0 else bench.algorithmic_flops32(cnt)
         pk = peak64 if prec == 0 else peak32
         rec["fp64" if prec == 0 else "mixed"] = {
             "atom_steps_per_s": n / (step_ms * 1e-3), "step_ms": step_ms, "kernel_ms": kms,
+            "kernel_launches_per_step": l.value / K,
             "achieved_tflops": fl / (kms * 1e-3) / 1e12, "frac": fl / (kms * 1e-3) / 1e12 / pk,
             "live_pairs": int(cnt[2]), "live_triplets": int(cnt[3])}
         del g
