@@ -53,7 +53,8 @@ for f in sorted(glob.glob(f"{indir}/ncu_tk_c*_p*_raw.csv")):
     for r in srows:
         if r and r[0] in ("Function Name", "Kernel Name"):
             kname = r[1]
-            ops = best.setdefault(kname, {})
+            # (a multi-kernel report prints every kernel's block twice: keep the first)
+            ops = {} if kname in best else best.setdefault(kname, {})
         if r and r[0] in ("Line No", "Address", "#"):
             hdr = r
             continue
