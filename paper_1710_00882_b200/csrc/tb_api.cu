@@ -129,7 +129,8 @@ struct tb_nlist {
   bool built = false;
   DevBuf offsets, nbr, rev, ref_pos, atom_cell, cell_count, cell_start, cell_atoms, row_count,
       maxrow, nl_row, sorted_atoms, sort_keys, iota, lanes, hist, cpos, crow, coff, centry,
-      fnbr, scratch;  // TMPW-wide per-atom rows of the single-pass scan
+      fnbr, scratch,  // TMPW-wide per-atom rows of the single-pass scan
+      crel;           // fp32 cell-relative candidate records (k_cell_rel)
   bool filtered = false;                 // chunks built from the species-pair filter
   DevBuf fbuf;                           // gather mode: per-entry force pieces
   bool fbuf_zero = false;                // entries without lanes hold zeros
@@ -603,7 +604,7 @@ extern "C" void tb_nlist_destroy(tb_nlist *nl) {
                     &nl->centry, &nl->fnbr, &nl->fbuf, &nl->plan, &nl->scratch, &nl->lplan,
                     &nl->llen, &nl->lrow, &nl->lrowj, &nl->lsorted, &nl->llanes, &nl->ref_log,
                     &nl->fspecies, &nl->lref, &nl->lgate, &nl->lforce, &nl->sp_lanes,
-                    &nl->sp_tmp};
+                    &nl->sp_tmp, &nl->crel};
   for (DevBuf *b : bufs) b->release();
   md_graph_release(nl);
   delete nl;
@@ -945,11 +946,17 @@ static int build_owned(tb_context *ctx, tb_nlist *nl, int64_t n, int64_t n_owned
     CK(cudaGetLastError());
     // single pass: rows of <= TMPW entries land in the scratch rows, counts,
     // max row and the row-length histogram (for the warp chunks) come along
-    if (c1 > c0 && g.stencil_image == 2 && ctx->nl_atoms)
+    if (c1 > c0 && g.stencil_image == 2 && ctx->nl_atoms) {
+      CK(nl->crel.ensure(sizeof(float4) * N));
+      k_cell_rel<<<nblk(N, 256), 256, 0, ctx->stream>>>(N, nl->cpos.as<double4>(),
+                                                         nl->atom_cell.as<int>(), g,
+                                                         nl->crel.as<float4>());
       k_nl_atoms<<<nblk(N, 256), 256, 0, ctx->stream>>>(
           (int)c0, (int)c1, (int)n_owned, nl->cpos.as<double4>(), g, bc * bc,
           nl->cell_start.as<int>(), nl->row_count.as<int>(), nl->scratch.as<int>(),
-          nl->maxrow.as<int>(), nl->hist.as<int>(), nl->maxrow.as<int>() + 1);
+          nl->maxrow.as<int>(), nl->hist.as<int>(), nl->maxrow.as<int>() + 1,
+          nl->crel.as<float4>());
+    }
     else if (c1 > c0)
       k_nl_cells<<<nblk(c1 - c0, 8), 256, 0, ctx->stream>>>(
           (int)c1, (int)n_owned, nl->cpos.as<double4>(), g, bc * bc, nl->cell_start.as<int>(),
@@ -2147,11 +2154,17 @@ static int enqueue_rebuild_device(tb_context *ctx, tb_nlist *nl, const double *d
       N, d_pos, nl->atom_cell.as<int>(), nl->cell_start.as<int>(), nl->cell_count.as<int>(),
       nl->cell_atoms.as<int>(), nl->cpos.as<double4>(), nl->ref_pos.as<double>());
   const double bc2 = nl->bc * nl->bc;
-  if (g.stencil_image == 2 && ctx->nl_atoms)
+  if (g.stencil_image == 2 && ctx->nl_atoms) {
+    // (crel is sized by the host build that precedes every device rebuild)
+    const float4 *crel = nl->crel.cap >= sizeof(float4) * (size_t)N ? nl->crel.as<float4>() : nullptr;
+    if (crel)
+      k_cell_rel<<<nblk(N, 256), 256, 0, st>>>(N, nl->cpos.as<double4>(), nl->atom_cell.as<int>(), g,
+                                                nl->crel.as<float4>());
     k_nl_atoms<<<nblk(N, 256), 256, 0, st>>>(0, (int)nl->ncell, N, nl->cpos.as<double4>(), g, bc2,
                                               nl->cell_start.as<int>(), nl->row_count.as<int>(),
                                               nl->scratch.as<int>(), &plan->max_row, plan->hist,
-                                              &plan->unwrapped);
+                                              &plan->unwrapped, crel);
+  }
   else
     k_nl_cells<<<nblk(nl->ncell, 8), 256, 0, st>>>(
         (int)nl->ncell, N, nl->cpos.as<double4>(), g, bc2, nl->cell_start.as<int>(),

@@ -567,6 +567,40 @@ __global__ void __launch_bounds__(256) k_nl_cells(int ncell, int n_owned,
   if (threadIdx.x < 34 && s_hist[threadIdx.x]) atomicAdd(hist + threadIdx.x, s_hist[threadIdx.x]);
 }
 
+// fp32 coordinates relative to the atom's own cell origin, in cell order, with
+// the atom index in .w: the 16-byte candidate record of k_nl_atoms' fp32
+// pre-test (all-periodic grids)
+__global__ void k_cell_rel(int n, const double4 *__restrict__ cpos,
+                           const int *__restrict__ atom_cell, Grid g, float4 *__restrict__ crel) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n) return;
+  const double4 p = cpos[t];
+  const int i = (int)__double_as_longlong(p.w);
+  int id = __ldg(atom_cell + i);
+  int c[3];
+  c[2] = id % g.nc[2];
+  id /= g.nc[2];
+  c[1] = id % g.nc[1];
+  c[0] = id / g.nc[1];
+  const double x[3] = {p.x, p.y, p.z};
+  float r[3];
+#pragma unroll
+  for (int ax = 0; ax < 3; ++ax) {
+    double v = __dsub_rn(x[ax], g.origin[ax]);
+    if (g.box.per[ax]) v = np_remainder(v, g.box.L[ax]);
+    r[ax] = (float)(v - (double)c[ax] * g.width[ax]);
+  }
+  crel[t] = make_float4(r[0], r[1], r[2], __int_as_float(i));
+}
+
+#ifndef TB_NL_F32
+#define TB_NL_F32 1
+#endif
+// r^2 band around bc^2 inside which the fp32 pre-test defers to the exact fp64
+// test: the fp32 error of r^2 near bc^2 is ~1e-5 A^2 (cell-relative coordinates
+// below 2 bc, a handful of roundings)
+constexpr float NL_F32_BAND = 2e-3f;
+
 // Atom-centric single-pass scan for all-periodic grids (stencil_image == 2),
 // the large-system path: one thread per atom in cell order (cpos), the 27
 // stencil cells walked directly, candidates tested with the same operations
@@ -581,7 +615,8 @@ __global__ void __launch_bounds__(256) k_nl_atoms(int cell0, int cell1, int n_ow
                                                   int *__restrict__ row_count,
                                                   int *__restrict__ tmp, int *__restrict__ max_row,
                                                   int *__restrict__ hist,
-                                                  const int *__restrict__ unwrapped) {
+                                                  const int *__restrict__ unwrapped,
+                                                  const float4 *__restrict__ crel = nullptr) {
   __shared__ int s_hist[34];
   if (threadIdx.x < 34) s_hist[threadIdx.x] = 0;
   __syncthreads();
@@ -602,6 +637,14 @@ __global__ void __launch_bounds__(256) k_nl_atoms(int cell0, int cell1, int n_ow
         cell_coords(p, g, cc);
       }
       int *row = tmp + (int64_t)i * TMPW;
+      // fp32 pre-test (TB_NL_F32): a candidate's 16-byte record decides it
+      // unless its fp32 r^2 is within NL_F32_BAND of bc^2 -- then the exact
+      // fp64 test below runs as before.  Membership only: the list stores
+      // indices, the kernels recompute every distance in fp64.
+      const bool f32 = TB_NL_F32 && crel != nullptr && stencil_image;
+      float4 qi = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (f32) qi = crel[t];
+      const float lo2 = (float)bc2 - NL_F32_BAND, hi2 = (float)bc2 + NL_F32_BAND;
 #pragma unroll 1
       for (int a = -1; a <= 1; ++a) {
         int x = cc[0] + a;
@@ -620,6 +663,30 @@ __global__ void __launch_bounds__(256) k_nl_atoms(int cell0, int cell1, int n_ow
             z += z < 0 ? g.nc[2] : (z >= g.nc[2] ? -g.nc[2] : 0);
             const int id = colbase + z;
             const int s0 = __ldg(cell_start + id), s1 = __ldg(cell_start + id + 1);
+            if (f32) {
+              const float sx = (float)a * (float)g.width[0] - qi.x;
+              const float sy = (float)b * (float)g.width[1] - qi.y;
+              const float sz = (float)r * (float)g.width[2] - qi.z;
+              for (int s = s0; s < s1; ++s) {
+                const float4 qj = __ldg(crel + s);
+                const float dx = qj.x + sx, dy = qj.y + sy, dz = qj.z + sz;
+                const float r2f = dx * dx + dy * dy + dz * dz;
+                bool hit = r2f < lo2;
+                if (!hit && r2f < hi2) {  // borderline: the exact test
+                  const double4 pj = cpos[s];
+                  const double e0 = __dsub_rn(__dsub_rn(pj.x, pi.x), lx);
+                  const double e1 = __dsub_rn(__dsub_rn(pj.y, pi.y), ly);
+                  const double e2 = __dsub_rn(__dsub_rn(pj.z, pi.z), lz);
+                  hit = __dadd_rn(__dadd_rn(__dmul_rn(e0, e0), __dmul_rn(e1, e1)),
+                                  __dmul_rn(e2, e2)) < bc2;
+                }
+                if (hit && s != t) {
+                  if (cnt < TMPW) row[cnt] = __float_as_int(qj.w);
+                  ++cnt;
+                }
+              }
+              continue;
+            }
             for (int s = s0; s < s1; ++s) {
               if (s == t) continue;
               const double4 pj = cpos[s];

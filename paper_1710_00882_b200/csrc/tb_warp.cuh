@@ -81,6 +81,12 @@ constexpr int QCAP = 4;   // k-iterations whose angular values are cached
 #ifndef TB_FP64_NO_SCACHE
 #define TB_FP64_NO_SCACHE 0
 #endif
+#ifndef TB_PAIR_DYN
+// dynamic-length rows of the mixed one-species kernel: two partners per trip of
+// the k-loops (the second predicated), so that the shared-memory loads and the
+// rcp of one partner overlap the other's arithmetic (same sums, same order)
+#define TB_PAIR_DYN 1
+#endif
 #ifndef TB_MIXED_LC8
 #define TB_MIXED_LC8 0  // measured: c4 mixed -2%, c3 mixed +19%, c5 mixed +14% (code size / registers)
 #endif
@@ -339,10 +345,36 @@ __device__ __forceinline__ void chunk_body(const KArgs &a, const WArgs &w, const
   // unroll; a dead partner has f_C = dzeta = 0 and contributes exactly 0)
   const unsigned rowmask = (L >= 32 ? 0xffffffffu : ((1u << L) - 1u)) << first;
   const unsigned partners = live ? (lmask & rowmask & ~(1u << lane)) : 0u;
+  constexpr bool PAIR = TB_PAIR_DYN && LC == 0 && S == 1 && !LAM3 && sizeof(T) == 4 && !SC;
   unsigned m = partners;
   int q = 0;
+  if (PAIR) {
+    const TripP<T> &tp0 = tab.trip[0];
+    while (m != 0) {
+      const int s0 = __ffs(m) - 1;
+      m &= m - 1;
+      const bool h1 = m != 0;
+      const int s1 = h1 ? __ffs(m) - 1 : s0;
+      m &= m - 1;
+      const typename Vec4<T>::t b0 = tb.e(s0), b1 = tb.e(s1);
+      const T f0 = tb.fc[s0].x, f1 = h1 ? tb.fc[s1].x : T(0);
+      T c0 = ex * b0.x + ey * b0.y + ez * b0.z;
+      T c1 = ex * b1.x + ey * b1.y + ez * b1.z;
+      TB_CLAMP_COS(c0);
+      TB_CLAMP_COS(c1);
+      T g0, dg0, g1, dg1;
+      angular(c0, tp0, g0, dg0);
+      angular(c1, tp0, g1, dg1);
+      if (ST && pair_live) {
+        A.c_lt += (f0 != T(0)) + (f1 != T(0));
+        A.c_tt += (f0 != T(0) && f0 != T(1)) + (f1 != T(0) && f1 != T(1));
+      }
+      zeta += f0 * g0;  // a dead partner (f = 0) adds exactly 0
+      zeta += f1 * g1;
+    }
+  }
 #pragma unroll
-  for (int it = 1; LC > 0 ? (live && it < LC) : m != 0; ++it, ++q) {
+  for (int it = 1; PAIR ? false : (LC > 0 ? (live && it < LC) : m != 0); ++it, ++q) {
     int src;
     if (LC > 0) {
       src = POW2 ? first + ((pos + it) & (LC - 1))
@@ -422,8 +454,42 @@ __device__ __forceinline__ void chunk_body(const KArgs &a, const WArgs &w, const
   T Sal = T(0), Sc = T(0), Sbx = T(0), Sby = T(0), Sbz = T(0);
   m = partners;
   q = 0;
+  if (PAIR) {
+    const TripP<T> &tp0 = tab.trip[0];
+    const T f_a = fck[0], df_a = dfck[0];
+    while (m != 0) {
+      const int s0 = __ffs(m) - 1;
+      m &= m - 1;
+      const bool h1 = m != 0;
+      const int s1 = h1 ? __ffs(m) - 1 : s0;
+      m &= m - 1;
+      const typename Vec4<T>::t b0 = tb.e(s0), b1 = tb.e(s1);
+      const T2 q0 = tb.fc[s0], q1 = tb.fc[s1];  // {f_C, delta_zeta} of the partner
+      const T fb0 = q0.x, dzb0 = q0.y;
+      const T fb1 = h1 ? q1.x : T(0), dzb1 = h1 ? q1.y : T(0);
+      T c0 = ex * b0.x + ey * b0.y + ez * b0.z;
+      T c1 = ex * b1.x + ey * b1.y + ez * b1.z;
+      TB_CLAMP_COS(c0);
+      TB_CLAMP_COS(c1);
+      T g0, dg0, g1, dg1;
+      angular(c0, tp0, g0, dg0);
+      angular(c1, tp0, g1, dg1);
+      const T al0 = dzb0 * (df_a * g0), be0 = dg0 * (dz * fb0 + dzb0 * f_a);
+      const T al1 = dzb1 * (df_a * g1), be1 = dg1 * (dz * fb1 + dzb1 * f_a);
+      Sal += al0;
+      Sc += be0 * c0;
+      Sbx += be0 * b0.x;
+      Sby += be0 * b0.y;
+      Sbz += be0 * b0.z;
+      Sal += al1;
+      Sc += be1 * c1;
+      Sbx += be1 * b1.x;
+      Sby += be1 * b1.y;
+      Sbz += be1 * b1.z;
+    }
+  }
 #pragma unroll
-  for (int it = 1; LC > 0 ? (live && it < LC) : m != 0; ++it, ++q) {
+  for (int it = 1; PAIR ? false : (LC > 0 ? (live && it < LC) : m != 0); ++it, ++q) {
     int src;
     if (LC > 0) {
       src = POW2 ? first + ((pos + it) & (LC - 1))
