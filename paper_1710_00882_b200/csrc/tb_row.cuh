@@ -42,6 +42,9 @@ namespace tb {
 #define TB_ROW_SACC 0  // fp64: energy / virial accumulators in per-thread shared slots instead of
                        // registers (spills 128 -> 96 B; measured c5 2.13 -> 2.20 ms: off)
 #endif
+#ifndef TB_ROW_SSTATE
+#define TB_ROW_SSTATE 0  // fp64: unit vectors, 1/r, cos, g' parked in shared memory over the pair parts
+#endif
 #ifndef TB_ROW_RECOS
 #define TB_ROW_RECOS 0   // recompute cos in the force phase instead of keeping it over the pair parts
                          // (measured neutral: c5 2.130 vs 2.133 ms)
@@ -103,12 +106,16 @@ __launch_bounds__(RowCfg<T>::nt, RowCfg<T>::minb)
 
   constexpr bool SACC = TB_ROW_SACC && sizeof(T) == 8;
   __shared__ double s_acc[SACC ? 7 : 1][SACC ? NTH : 1];
+  constexpr bool SST = TB_ROW_SSTATE && sizeof(T) == 8;
+  constexpr int NST = 4 * LM + 2 * NP;
+  __shared__ T s_st[SST ? NST : 1][SST ? NTH : 1];
   double acc[7] = {0, 0, 0, 0, 0, 0, 0};  // E, W xx yy zz xy xz yz
   if (SACC) {
 #pragma unroll
     for (int q = 0; q < 7; ++q) s_acc[q][threadIdx.x] = 0.0;
   }
-  unsigned long long c_vis = 0, c_pk = 0, c_lp = 0, c_lt = 0, c_tp = 0, c_tt = 0;
+  // per-thread counters: at most 16 per atom and n / blockDim atoms per thread, so 32 bits hold them
+  unsigned c_vis = 0, c_pk = 0, c_lp = 0, c_lt = 0, c_tp = 0, c_tt = 0;
   const PairP<T> &pp = tab.pair[0];
   const TripP<T> &tp = tab.trip[0];
 
@@ -239,7 +246,7 @@ __launch_bounds__(RowCfg<T>::nt, RowCfg<T>::minb)
         if (live[q] && rr[q] > tp.Rm && rr[q] < tp.Rp) cutoff(rr[q], tp, fc[q], dfc[q]);
     }
     if (ST && ra.count_packed) {
-      c_vis += (unsigned long long)(nlive * nlive);  // zeta_visits = sum_i n_i^2 (kernels.py:537-544)
+      c_vis += (unsigned)(nlive * nlive);  // zeta_visits = sum_i n_i^2 (kernels.py:537-544)
       c_pk += nlive;
     }
     if (more) {
@@ -260,9 +267,25 @@ __launch_bounds__(RowCfg<T>::nt, RowCfg<T>::minb)
         angular(c, tp, g[u], dg[u]);
       }
 
+    if (SST) {
+      volatile T(*st)[SST ? NTH : 1] = s_st;
+#pragma unroll
+      for (int q = 0; q < LM; ++q) {
+        st[4 * q][threadIdx.x] = ex[q];
+        st[4 * q + 1][threadIdx.x] = ey[q];
+        st[4 * q + 2][threadIdx.x] = ez[q];
+        st[4 * q + 3][threadIdx.x] = inv[q];
+      }
+#pragma unroll
+      for (int u = 0; u < NP; ++u) {
+        st[4 * LM + u][threadIdx.x] = cs[u];
+        st[4 * LM + NP + u][threadIdx.x] = dg[u];
+      }
+    }
     // ---- zeta, pair parts ----
     T zeta[LM], vv[LM], dvdr[LM], dz[LM];
     bool pair_live[LM], tiny = false;
+    int n_lt = 0, n_tt = 0, n_lp = 0, n_tp = 0;  // this atom's counts (one 64-bit add each below)
 #pragma unroll
     for (int p = 0; p < LM; ++p) {
       pair_live[p] = live[p] && rr[p] < pp.Rp;
@@ -273,15 +296,21 @@ __launch_bounds__(RowCfg<T>::nt, RowCfg<T>::minb)
         const int u = p < q ? pair_index<LM>(p, q) : pair_index<LM>(q, p);
         zeta[p] += fc[q] * g[u];  // a dead partner has f_C = 0
         if (ST) {
-          c_lt += pair_live[p] && fc[q] != T(0);
-          c_tt += pair_live[p] && fc[q] != T(0) && fc[q] != T(1);
+          n_lt += pair_live[p] && fc[q] != T(0);
+          n_tt += pair_live[p] && fc[q] != T(0) && fc[q] != T(1);
         }
       }
       tiny |= pair_live[p] && zeta[p] < T(ZETA_TINY);
       if (ST) {
-        c_lp += pair_live[p];
-        c_tp += pair_live[p] && rr[p] > pp.Rm;
+        n_lp += pair_live[p];
+        n_tp += pair_live[p] && rr[p] > pp.Rm;
       }
+    }
+    if (ST) {
+      c_lt += n_lt;
+      c_tt += n_tt;
+      c_lp += n_lp;
+      c_tp += n_tp;
     }
 #pragma unroll
     for (int p = 0; p < LM; ++p) {
@@ -305,6 +334,21 @@ __launch_bounds__(RowCfg<T>::nt, RowCfg<T>::minb)
       for (int q = 0; q < LM; ++q) jn[q] = q < L ? __ldg(a.nbr + o + q) : i;
     }
 
+    if (SST) {
+      volatile T(*st)[SST ? NTH : 1] = s_st;
+#pragma unroll
+      for (int q = 0; q < LM; ++q) {
+        ex[q] = st[4 * q][threadIdx.x];
+        ey[q] = st[4 * q + 1][threadIdx.x];
+        ez[q] = st[4 * q + 2][threadIdx.x];
+        inv[q] = st[4 * q + 3][threadIdx.x];
+      }
+#pragma unroll
+      for (int u = 0; u < NP; ++u) {
+        cs[u] = st[4 * LM + u][threadIdx.x];
+        dg[u] = st[4 * LM + NP + u][threadIdx.x];
+      }
+    }
     // ---- forces ----
     T beta[NP];
 #pragma unroll

@@ -1,5 +1,3 @@
 O=gpurun_out/r02_row; mkdir -p $O
-timeout 1200 python -m pytest tests/test_gpu_parity.py tests/test_gpu_dnl.py tests/test_gpu_decomp.py tests/test_gpu_md.py -q -x -p no:cacheprovider > $O/pytest.txt 2>&1; echo "pytest rc=$?"; tail -3 $O/pytest.txt
-timeout 1200 python -m pytest tests/test_gpu_fullsize.py -q -x -p no:cacheprovider -k "pair or neighbor or list or config" > $O/pytest_full.txt 2>&1; echo "pytest full rc=$?"; tail -3 $O/pytest_full.txt
-bash tools/md_step_launches.sh 5 12 $O/md_step_c5.csv
-grep -E "k_nl_atoms|k_nl_compact|k_fill_lanes" -A3 $O/md_step_c5.json | grep -E "tb::|us_mean"
+cp paper_1710_00882_b200/lib/libtersoff_b200.so /tmp/cur.so
+KT_CONFIGS=5 KT_OUT=$O/ktime9.json timeout 1200 python tools/ktime_so.py /tmp/cur.so tools/ab/sst_m3.so tools/ab/sst_m4.so tools/ab/sst_m4_sacc.so 2> $O/ktime.err; echo "ktime rc=$?"; tail -3 $O/ktime.err
