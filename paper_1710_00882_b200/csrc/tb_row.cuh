@@ -29,7 +29,8 @@ namespace tb {
 #define TB_ROW_NT 128
 #endif
 #ifndef TB_ROW_MINB64
-#define TB_ROW_MINB64 3
+#define TB_ROW_MINB64 4  // 16 warps/SM at 128 registers with TB_ROW_SSTATE + TB_ROW_SACC (c5 2.128 -> 2.088 ms);
+                         // without them: 3 (12 warps at 168 registers), see DESIGN 3.10
 #endif
 #ifndef TB_ROW_MINB32
 #define TB_ROW_MINB32 4
@@ -39,11 +40,12 @@ namespace tb {
 #define TB_ROW_VIR_RE 1  // virial from r_p e_p (x) f_p: the displacement registers die after the unit vectors
 #endif
 #ifndef TB_ROW_SACC
-#define TB_ROW_SACC 0  // fp64: energy / virial accumulators in per-thread shared slots instead of
-                       // registers (spills 128 -> 96 B; measured c5 2.13 -> 2.20 ms: off)
+#define TB_ROW_SACC 1  // fp64: energy / virial accumulators in per-thread shared slots instead of
+                       // registers (alone at 12 warps/SM: c5 2.13 -> 2.20 ms; with SSTATE at 16: 2.09)
 #endif
 #ifndef TB_ROW_SSTATE
-#define TB_ROW_SSTATE 0  // fp64: unit vectors, 1/r, cos, g' parked in shared memory over the pair parts
+#define TB_ROW_SSTATE 1  // fp64: unit vectors, 1/r, cos, g' parked in shared memory over the pair parts
+                         // (28 doubles per thread; frees their registers where the four pair chains peak)
 #endif
 #ifndef TB_ROW_RECOS
 #define TB_ROW_RECOS 0   // recompute cos in the force phase instead of keeping it over the pair parts
