@@ -2488,7 +2488,7 @@ extern "C" int tb_md_run(tb_context *ctx, tb_nlist *nl, int64_t n, double *d_pos
   // the run ends.  Pair terms are the same either way: every evaluation
   // re-tests r < r_cut on a list that holds all such pairs.
   const bool loose = ctx->md_loose > 0 && scatter == TB_SCATTER_ATOMIC;
-  const double skin_list = loose ? skin + ctx->md_loose : skin;
+  double skin_list = loose ? skin + ctx->md_loose : skin;
   // snapshot: x, v, F, E of the entry state and the entry list's reference
   // positions (every failing exit rebuilds that exact list: the in-graph
   // rebuilds may have left the list at a later trajectory point)
@@ -2501,13 +2501,30 @@ extern "C" int tb_md_run(tb_context *ctx, tb_nlist *nl, int64_t n, double *d_pos
     CK(nl->ref_log.ensure(sizeof(double) * 3 * (size_t)N));
     CK(cudaMemcpyAsync(nl->ref_log.p, nl->ref_pos.p, sizeof(double) * 3 * N,
                        cudaMemcpyDeviceToDevice, ctx->stream));
-    int rc = tb_build_neighbors(ctx, nl, n, d_positions, nl->L, nl->per, r_cut, skin_list);
+    // The wider list must not push rows out of the row kernel (tb_row.cuh, rows
+    // of <= 4 entries): in Si the second-neighbour shell (3.84 A) starts to
+    // enter at skin + 0.3 -- 42% of the rows of config 5 get a fifth entry and
+    // fall to the warp-chunk kernel, which costs what the saved rebuilds gain
+    // (4.83 ms/step; 4.94 with the exact list; 4.35 at 0.2).  When the exact
+    // list's rows are nearly all short, the extra skin is reduced (x 2/3, then
+    // x 1/2) until 85% of the wider list's rows are.
+    const bool row_ok = ctx->row_kernel && ctx->S == 1 && !ctx->lam3 && n >= ctx->row_min;
+    const double f_exact = n ? (double)nl->r4_count / (double)n : 0.0;
+    double lw = ctx->md_loose;
+    int rc = TB_OK;
+    for (int t = 0;; ++t) {
+      skin_list = skin + lw;
+      rc = tb_build_neighbors(ctx, nl, n, d_positions, nl->L, nl->per, r_cut, skin_list);
+      if (rc || !row_ok || f_exact < 0.98 || t == 2 || nl->nchunks <= 0) break;
+      if ((double)nl->r4_count >= 0.85 * (double)n) break;
+      lw *= t == 0 ? 2.0 / 3.0 : 0.5;
+    }
     if (rc) return rc;
     if (nl->nchunks <= 0) {  // rows beyond the warp kernel: back to the exact list, per-step path
       rc = tb_build_neighbors(ctx, nl, n, nl->ref_log.as<double>(), nl->L, nl->per, r_cut, skin);
       return rc ? rc : fail(ctx, TB_ERR_UNSUPPORTED, "device-resident loop: rows exceed 32 entries");
     }
-    m.loose = ctx->md_loose;
+    m.loose = lw;
     m.ref_log = nl->ref_log.as<double>();
   }
   // the exact list at the reference's last rebuild (loose runs, any exit)
