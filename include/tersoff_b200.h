@@ -109,7 +109,7 @@ int tb_set_stream(tb_context *ctx, void *stream);
  * evaluate rows of at most 4 skin-list entries with the atom-per-lane kernel
  * (one lane holds an atom's neighbours in registers; g(cos) once per unordered
  * pair) when the list has at least m such rows (1 = the default threshold,
- * 262144: one lane per atom needs that many atoms to fill the GPU); longer
+ * 1000000: one lane per atom needs about that many atoms to beat the warp-chunk kernel); longer
  * rows keep the warp-chunk kernel.  0 = warp-chunk kernel for every row. */
 #define TB_OPT_ROW_KERNEL 7
 int tb_set_option(tb_context *ctx, int option, int value);

@@ -112,9 +112,10 @@ struct tb_context {
   struct StreamCtl *sctl = nullptr;  // set by tb_compute around enqueue_compute
   int part_off = 0;     // first block-partial slot of the next warp launch
   bool row_kernel = getenv("TB_NO_ROW_KERNEL") == nullptr;  // TB_OPT_ROW_KERNEL: atom-per-lane kernel for rows <= 4
-  // ... for lists with at least this many such rows (one lane per atom needs
-  // ~150k atoms to fill the GPU: config 2, 64k atoms, 20.7 -> 36.7 us with it)
-  int64_t row_min = getenv("TB_ROW_MIN") ? atoll(getenv("TB_ROW_MIN")) : 262144;
+  // ... for lists with at least this many such rows (tools/row_crossover.py,
+  // fp64 row vs warp-chunk kernel: 64k atoms 34 vs 21 us, 512k 94 vs 87 us,
+  // 1M 152 vs 159 us, 2.1M 285 vs 318 us)
+  int64_t row_min = getenv("TB_ROW_MIN") ? atoll(getenv("TB_ROW_MIN")) : 1000000;
   int last_blocks = 0;  // grid of the last Tersoff launch (partials to reduce)  // tb_set_option(TB_OPT_TILE_KERNEL): general tile kernel only
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_used, ev_free;
 };
@@ -451,7 +452,7 @@ extern "C" int tb_set_option(tb_context *ctx, int option, int value) {
   if (option == TB_OPT_ROW_KERNEL) {
     if (value < 0) return fail(ctx, TB_ERR_ARG, "row-kernel threshold %d out of range", value);
     ctx->row_kernel = value != 0;
-    if (value > 0) ctx->row_min = value == 1 ? 262144 : value;
+    if (value > 0) ctx->row_min = value == 1 ? 1000000 : value;
     return TB_OK;
   }
   if (option == TB_OPT_STREAM_RANGE) {
