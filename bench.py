@@ -621,7 +621,7 @@ def gpu_arm(args):
             del st3
         if cfg["config"] == 5 and args.md5_steps > 0:
             extra["md"]["config5_fp64"] = md_measure(B, _native, ctx, state, table, dev, 0,
-                                                     args.md5_steps, warm=10)
+                                                     args.md5_steps, warm=20)
         ctx.set_stream(stream.cuda_stream)
         ctx.set_table(table)
     e2e = e2e_arm(args, B, state, table, ev.nl, dev)

@@ -2508,7 +2508,9 @@ extern "C" int tb_md_run(tb_context *ctx, tb_nlist *nl, int64_t n, double *d_pos
     // fall to the warp-chunk kernel, which costs what the saved rebuilds gain
     // (4.83 ms/step; 4.94 with the exact list; 4.35 at 0.2).  When the exact
     // list's rows are nearly all short, the extra skin is reduced (x 2/3, then
-    // x 1/2) until 85% of the wider list's rows are.
+    // x 1/2) until 90% of the wider list's rows are.  (Config 5 over a run: the
+    // short-row fraction is 0.62-0.89 at skin + 0.3, 0.92-0.99 at skin + 0.2;
+    // tools/row_fraction_vs_time.py.)
     const bool row_ok = ctx->row_kernel && ctx->S == 1 && !ctx->lam3 && n >= ctx->row_min;
     const double f_exact = n ? (double)nl->r4_count / (double)n : 0.0;
     double lw = ctx->md_loose;
@@ -2517,7 +2519,7 @@ extern "C" int tb_md_run(tb_context *ctx, tb_nlist *nl, int64_t n, double *d_pos
       skin_list = skin + lw;
       rc = tb_build_neighbors(ctx, nl, n, d_positions, nl->L, nl->per, r_cut, skin_list);
       if (rc || !row_ok || f_exact < 0.98 || t == 2 || nl->nchunks <= 0) break;
-      if ((double)nl->r4_count >= 0.85 * (double)n) break;
+      if ((double)nl->r4_count >= 0.90 * (double)n) break;
       lw *= t == 0 ? 2.0 / 3.0 : 0.5;
     }
     if (rc) return rc;

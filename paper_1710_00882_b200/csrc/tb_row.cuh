@@ -47,6 +47,9 @@ namespace tb {
 #define TB_ROW_SSTATE 1  // fp64: unit vectors, 1/r, cos, g' parked in shared memory over the pair parts
                          // (28 doubles per thread; frees their registers where the four pair chains peak)
 #endif
+#ifndef TB_ROW_SCNT
+#define TB_ROW_SCNT 1  // fp64, counters on: the six counters in per-thread shared slots
+#endif
 #ifndef TB_ROW_RECOS
 #define TB_ROW_RECOS 0   // recompute cos in the force phase instead of keeping it over the pair parts
                          // (measured neutral: c5 2.130 vs 2.133 ms)
@@ -117,6 +120,13 @@ __launch_bounds__(RowCfg<T>::nt, RowCfg<T>::minb)
     for (int q = 0; q < 7; ++q) s_acc[q][threadIdx.x] = 0.0;
   }
   // per-thread counters: at most 16 per atom and n / blockDim atoms per thread, so 32 bits hold them
+  // (fp64 keeps them in per-thread shared slots: its registers are spent, SCNT)
+  constexpr bool SCNT = ST && sizeof(T) == 8 && TB_ROW_SCNT;
+  __shared__ unsigned s_cnt[SCNT ? 6 : 1][SCNT ? NTH : 1];
+  if (SCNT) {
+#pragma unroll
+    for (int q = 0; q < 6; ++q) s_cnt[q][threadIdx.x] = 0u;
+  }
   unsigned c_vis = 0, c_pk = 0, c_lp = 0, c_lt = 0, c_tp = 0, c_tt = 0;
   const PairP<T> &pp = tab.pair[0];
   const TripP<T> &tp = tab.trip[0];
@@ -248,8 +258,14 @@ __launch_bounds__(RowCfg<T>::nt, RowCfg<T>::minb)
         if (live[q] && rr[q] > tp.Rm && rr[q] < tp.Rp) cutoff(rr[q], tp, fc[q], dfc[q]);
     }
     if (ST && ra.count_packed) {
-      c_vis += (unsigned)(nlive * nlive);  // zeta_visits = sum_i n_i^2 (kernels.py:537-544)
-      c_pk += nlive;
+      // zeta_visits = sum_i n_i^2 (kernels.py:537-544)
+      if (SCNT) {
+        s_cnt[0][threadIdx.x] += (unsigned)(nlive * nlive);
+        s_cnt[1][threadIdx.x] += (unsigned)nlive;
+      } else {
+        c_vis += (unsigned)(nlive * nlive);
+        c_pk += nlive;
+      }
     }
     if (more) {
       o = __ldg(a.off + i);
@@ -309,10 +325,17 @@ __launch_bounds__(RowCfg<T>::nt, RowCfg<T>::minb)
       }
     }
     if (ST) {
-      c_lt += n_lt;
-      c_tt += n_tt;
-      c_lp += n_lp;
-      c_tp += n_tp;
+      if (SCNT) {
+        s_cnt[2][threadIdx.x] += (unsigned)n_lp;
+        s_cnt[3][threadIdx.x] += (unsigned)n_lt;
+        s_cnt[4][threadIdx.x] += (unsigned)n_tp;
+        s_cnt[5][threadIdx.x] += (unsigned)n_tt;
+      } else {
+        c_lt += n_lt;
+        c_tt += n_tt;
+        c_lp += n_lp;
+        c_tp += n_tp;
+      }
     }
 #pragma unroll
     for (int p = 0; p < LM; ++p) {
@@ -430,6 +453,10 @@ __launch_bounds__(RowCfg<T>::nt, RowCfg<T>::minb)
   // ---- stats and block partials (reduced by the finalize kernel) ----
   if (ST) {
     unsigned long long csum[6] = {c_vis, c_pk, c_lp, c_lt, c_tp, c_tt};
+    if (SCNT) {
+#pragma unroll
+      for (int q = 0; q < 6; ++q) csum[q] = s_cnt[q][threadIdx.x];
+    }
 #pragma unroll
     for (int q = 0; q < 6; ++q) {
       unsigned long long v = warp_sum(csum[q]);
