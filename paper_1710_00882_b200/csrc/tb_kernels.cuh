@@ -667,22 +667,41 @@ __global__ void __launch_bounds__(256) k_nl_atoms(int cell0, int cell1, int n_ow
               const float sx = (float)a * (float)g.width[0] - qi.x;
               const float sy = (float)b * (float)g.width[1] - qi.y;
               const float sz = (float)r * (float)g.width[2] - qi.z;
+              // hot loop: fp32 decision only; the rare borderline records of this
+              // cell are remembered in a bit mask and settled after it, so the
+              // exact test's code and its reconvergence stay out of the loop
+              unsigned maybe = 0u;
               for (int s = s0; s < s1; ++s) {
                 const float4 qj = __ldg(crel + s);
                 const float dx = qj.x + sx, dy = qj.y + sy, dz = qj.z + sz;
                 const float r2f = dx * dx + dy * dy + dz * dz;
-                bool hit = r2f < lo2;
-                if (!hit && r2f < hi2) {  // borderline: the exact test
+                const bool hit = r2f < lo2 && s != t;
+                if (r2f >= lo2 && r2f < hi2) maybe |= 1u << min(s - s0, 31);
+                if (hit) {
+                  if (cnt < TMPW) row[cnt] = __float_as_int(qj.w);
+                  ++cnt;
+                }
+              }
+              if (__builtin_expect(maybe != 0u, 0)) {
+                for (int s = s0; s < s1; ++s) {
+                  const int k = min(s - s0, 31);
+                  if (!(maybe >> k & 1u)) continue;
+                  // (beyond 31 records in a cell the last bit stands for all of
+                  // them: re-test each in fp32 first)
+                  const float4 qj = __ldg(crel + s);
+                  const float dx = qj.x + sx, dy = qj.y + sy, dz = qj.z + sz;
+                  const float r2f = dx * dx + dy * dy + dz * dz;
+                  if (!(r2f >= lo2 && r2f < hi2)) continue;
                   const double4 pj = cpos[s];
                   const double e0 = __dsub_rn(__dsub_rn(pj.x, pi.x), lx);
                   const double e1 = __dsub_rn(__dsub_rn(pj.y, pi.y), ly);
                   const double e2 = __dsub_rn(__dsub_rn(pj.z, pi.z), lz);
-                  hit = __dadd_rn(__dadd_rn(__dmul_rn(e0, e0), __dmul_rn(e1, e1)),
-                                  __dmul_rn(e2, e2)) < bc2;
-                }
-                if (hit && s != t) {
-                  if (cnt < TMPW) row[cnt] = __float_as_int(qj.w);
-                  ++cnt;
+                  const bool hit = __dadd_rn(__dadd_rn(__dmul_rn(e0, e0), __dmul_rn(e1, e1)),
+                                             __dmul_rn(e2, e2)) < bc2;
+                  if (hit && s != t) {
+                    if (cnt < TMPW) row[cnt] = __float_as_int(qj.w);
+                    ++cnt;
+                  }
                 }
               }
               continue;
