@@ -186,7 +186,11 @@ int tb_needs_rebuild(tb_context *ctx, const tb_nlist *nl, const double *position
  *   energy    1 double out (host), required virial[6] xx,yy,zz,xy,xz,yz, may be NULL
  *   stats     TB_NSTATS int64 (host), may be NULL
  * r_cut must not exceed the list's build r_cut (neighbor.py:334-337).
- * Synchronises the stream before returning. */
+ * Synchronises the stream before returning.  Host buffers that are pinned
+ * (page-locked) are the fast path: small systems get their forces written
+ * straight into host memory, large one-species systems are streamed in atom
+ * ranges so that both copy directions and the kernel overlap
+ * (TB_OPT_STREAM_RANGE); pageable buffers are staged and copied. */
 int tb_compute(tb_context *ctx, const tb_nlist *nl, const double *positions,
                const int32_t *species, double r_cut, int precision, int scatter,
                double *forces, double *per_atom, double *energy, double *virial,
