@@ -636,7 +636,9 @@ def gpu_arm(args):
                            else "flushed between timed steps (256 MiB write)"),
                     "launch": "each step is one CUDA-graph replay (Tersoff kernel + finalize)"},
         "e2e": e2e,
-        "gpu_launches": 2 * args.steps,
+        # per timed step: the Tersoff kernel(s) (row kernel + warp-chunk kernel when
+        # the list is split) and the finalize kernel
+        "gpu_launches": int(round((roof.get("kernel_launches_per_step", 1.0) + 1) * args.steps)),
         "roofline": roof,
         "clocks": sampler.summary(),
         "energy_eV": energy0,
