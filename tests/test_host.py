@@ -189,3 +189,26 @@ def test_unbuilt_library_fails_loudly(monkeypatch, tmp_path):
     monkeypatch.setattr(_native, "LIB_PATH", str(tmp_path / "missing.so"))
     with pytest.raises(_native.NativeUnavailable):
         _native.load_library()
+
+
+def test_option_and_status_codes_match_the_header():
+    """The Python mirror of tb_set_option's options, the precision / scatter
+    selectors and the status codes are the header's #defines."""
+    import re
+    from paper_1710_00882_b200 import _native
+    text = open(os.path.join(ROOT, "include", "tersoff_b200.h")).read()
+    defs = {m.group(1): int(m.group(2))
+            for m in re.finditer(r"^#define\s+(TB_[A-Z0-9_]+)\s+(-?\d+)\b", text, re.M)}
+    opts = {k: v for k, v in defs.items() if k.startswith("TB_OPT_")}
+    assert len(opts) >= 7 and len(set(opts.values())) == len(opts)
+    for name, value in opts.items():
+        assert getattr(_native, name[3:]) == value, name
+    assert _native.TB_ERR_UNSUPPORTED == defs["TB_ERR_UNSUPPORTED"]
+    assert _native.NSTATS == defs["TB_NSTATS"]
+    assert _native.PRECISION == {"double": defs["TB_PREC_DOUBLE"], "single": defs["TB_PREC_MIXED"],
+                                 "mixed": defs["TB_PREC_MIXED"]}
+    for k, name in enumerate(("TB_OK", "TB_ERR_CONFIG", "TB_ERR_INPUT", "TB_ERR_CUDA",
+                              "TB_ERR_ARG", "TB_ERR_UNSUPPORTED")):
+        assert defs[name] == k == getattr(_native, name)
+    assert _native.SCATTER == {"atomic": defs["TB_SCATTER_ATOMIC"],
+                               "gather": defs["TB_SCATTER_GATHER"]}
