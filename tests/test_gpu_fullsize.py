@@ -122,3 +122,35 @@ def test_config2_1000_step_nve_drift(oracle_mod, precision):
     if precision == "double":
         # the first 100 fs agree closely before chaos amplifies round-off
         assert np.max(np.abs(rec["total"][:11] - tot_ref[:11])) <= 1e-8 * abs(tot_ref[0])
+
+
+@pytest.mark.parametrize("precision", ["double", "single"])
+def test_fullsize_streamed_host_call(precision):
+    """Config 5 through compute() with pinned host buffers: tb_compute streams
+    the call in 32 atom ranges (csrc/tb_stream.cuh; warp-chunk kernel stages)
+    while the resident-buffer call above ran the row kernel -- the two kernel
+    paths and the streamed copies must agree at full size."""
+    import torch
+    st, t, nl, r64 = full(5)
+    n = st.natoms
+    pos = torch.empty((n, 3), dtype=torch.float64).pin_memory().numpy()
+    pos[:] = st.positions
+    out = B.ForceEnergyResult(torch.empty((n, 3), dtype=torch.float64).pin_memory().numpy(), 0.0,
+                              torch.empty(n, dtype=torch.float64).pin_memory().numpy(), {})
+    out.forces[:] = np.nan
+    out.per_atom_energy[:] = np.nan
+
+    class HostState:
+        pass
+
+    hs = HostState()
+    hs.positions, hs.species, hs.box = pos, st.species, st.box
+    res = B.compute(hs, nl, t, B.make_variant("B200", precision=precision), out=out)
+    assert np.isfinite(res.forces).all() and np.isfinite(res.per_atom_energy).all()
+    tol, etol = (1e-12, 1e-12) if precision == "double" else (MIXED_TOL, MIXED_E_TOL)
+    assert rel_f(res.forces, r64.forces) <= tol
+    assert abs(res.potential_energy - r64.potential_energy) <= etol * abs(r64.potential_energy)
+    assert np.abs(res.per_atom_energy - r64.per_atom_energy).max() <= \
+        (1e-12 if precision == "double" else 1e-4) * np.abs(r64.per_atom_energy).max()
+    assert res.stats["zeta_visits"] == r64.stats["zeta_visits"]
+    assert abs(res.potential_energy - res.per_atom_energy.sum()) <= 1e-9 * abs(res.potential_energy)
