@@ -597,8 +597,9 @@ __global__ void k_cell_rel(int n, const double4 *__restrict__ cpos,
 #define TB_NL_F32 1
 #endif
 // r^2 band around bc^2 inside which the fp32 pre-test defers to the exact fp64
-// test: the fp32 error of r^2 near bc^2 is ~1e-5 A^2 (cell-relative coordinates
-// below 2 bc, a handful of roundings)
+// test: the fp32 error of r^2 near bc^2 is ~4e-5 A^2 at bc = 3.6 A (cell-relative
+// coordinates below 2 bc, a handful of roundings: ~3e-6 relative); the band is
+// max(2e-3, 2e-5 bc^2)
 constexpr float NL_F32_BAND = 2e-3f;
 
 // Atom-centric single-pass scan for all-periodic grids (stencil_image == 2),
@@ -644,7 +645,9 @@ __global__ void __launch_bounds__(256) k_nl_atoms(int cell0, int cell1, int n_ow
       const bool f32 = TB_NL_F32 && crel != nullptr && stencil_image;
       float4 qi = make_float4(0.f, 0.f, 0.f, 0.f);
       if (f32) qi = crel[t];
-      const float lo2 = (float)bc2 - NL_F32_BAND, hi2 = (float)bc2 + NL_F32_BAND;
+      // (the band grows with the cutoff: the fp32 error of r^2 is relative, a few 1e-6)
+      const float band = fmaxf(NL_F32_BAND, 2e-5f * (float)bc2);
+      const float lo2 = (float)bc2 - band, hi2 = (float)bc2 + band;
 #pragma unroll 1
       for (int a = -1; a <= 1; ++a) {
         int x = cc[0] + a;
