@@ -468,3 +468,32 @@ def test_more_than_four_species(oracle_mod, S, precision):
         bad = fr.species.copy()
         bad[0] = S
         B.compute(Frame(pos, [L, L, L], (True, True, True), bad), nl, table)
+
+
+def test_neighbor_list_pairs_at_the_cutoff(oracle_mod):
+    """The list scan decides candidates in fp32 unless their r^2 is within a
+    band of the build cutoff, where the exact fp64 test runs (k_nl_atoms,
+    TB_NL_F32).  1000 isolated dimers at bc + delta, delta from 0 and +-1 ulp up
+    to +-1e-2 A on both sides of the band, random orientations, all-periodic
+    box of 24 cells per axis: the pair set must equal the oracle's."""
+    rng = np.random.default_rng(12345)
+    r_cut, skin = 3.0, 0.3
+    bc = r_cut + skin
+    L = 80.0
+    sites = np.stack(np.meshgrid(*[np.arange(10) * 8.0 + 2.0] * 3, indexing="ij"), -1).reshape(-1, 3)
+    deltas = np.array([0.0] + [s * m for m in (np.spacing(bc), 4 * np.spacing(bc), 1e-14, 1e-12,
+                                               1e-10, 1e-8, 1e-6, 1e-5, 1e-4, 2e-4, 3e-4, 5e-4,
+                                               1e-3, 1e-2) for s in (1.0, -1.0)])
+    u = rng.normal(size=(len(sites), 3))
+    u /= np.linalg.norm(u, axis=1)[:, None]
+    d = bc + deltas[np.arange(len(sites)) % len(deltas)]
+    a = sites + rng.uniform(0.0, 1.0, size=sites.shape)
+    pos = np.concatenate([a, a + u * d[:, None]])
+    pos %= L  # dimers across the periodic faces too
+    fr = Frame(pos, (L, L, L), (True, True, True))
+    nl = B.build_neighbor_list(fr, r_cut, skin)
+    off, nb = oracle_mod.build_neighbor_list(fr.positions, fr.box.lengths, fr.box.periodic,
+                                             r_cut, skin)
+    assert np.array_equal(nl.offsets, off) and np.array_equal(nl.neighbors, nb)
+    n_in = int(np.diff(off).sum()) // 2
+    assert 300 < n_in < 700  # both sides of the cutoff are populated
