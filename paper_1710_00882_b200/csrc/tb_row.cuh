@@ -151,6 +151,19 @@ __launch_bounds__(RowCfg<T>::nt, RowCfg<T>::minb)
     int cj[LM];
 #pragma unroll
     for (int q = 0; q < LM; ++q) cj[q] = jn[q];
+#ifdef TB_ROW_DEBUG
+    // debug builds: every index this lane dereferences is inside its array
+    // (compute-sanitizer is not available on the GPU pool)
+    {
+      bool ok = ci >= 0 && ci < a.n && co >= 0 && cL >= 0 && cL <= LM;
+#pragma unroll
+      for (int q = 0; q < LM; ++q) ok = ok && cj[q] >= 0 && cj[q] < a.n;
+      if (!ok) {
+        atomicExch(&a.err->overflow, 1);  // reported as an internal error
+        continue;
+      }
+    }
+#endif
     // ---- gathers of this atom ----
     double xi[3], xj[LM][3];
     load3(a.pos, ci, xi);
